@@ -1,0 +1,242 @@
+"""Catch-up state transfer on B200 — drop-in for the snapshot/fetch half of
+``ftdp.checkpoint`` (pkg/src/ftdp/checkpoint.py:48-154).
+
+* ``SnapshotStore``  retention-1 copy of one rank shard's (params, momentum)
+  for the last committed step (checkpoint.py:56-80), held in a device arena
+  that other replicas can map (CUDA IPC).  ``capture`` is a stream-ordered
+  seqlock + copy kernel on the donor (replica.py:645-648).
+* ``fetch_shard``    the recovering replica pulls the donor's snapshot over
+  NVLink with a rate-limited kernel (``ctas`` SMs) on a low-priority side
+  stream, so the donor's and everyone else's FTAR steps keep running
+  (checkpoint.py:117-144, replica.py:452-493).  A donor that holds another
+  step — or re-captures during the pull — yields ``SnapshotUnavailable``
+  with the step it has (checkpoint.py:132-133).
+* ``pick_donor``     round-robin donor choice (checkpoint.py:147-154).
+* ``serve_fetches``  kept for API shape: on NVLink the donor serves by
+  publishing its snapshot arena once; no per-request thread is needed.
+
+Persistent checkpoints and the loader ledger (checkpoint.py:157-316) are out
+of scope.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import torch
+
+from . import _lib
+from .errors import INTERNAL_INVARIANT, PEER_DOWN, Fatal, Recoverable, from_status
+from .fabric import ArenaInfo, LocalFabric
+
+
+class SnapshotUnavailable(Exception):
+    """The donor no longer (or does not yet) hold the requested step."""
+
+    def __init__(self, available):
+        super().__init__(f"snapshot unavailable (donor holds {available})")
+        self.available = available
+
+
+def _as_bytes_tensor(t: torch.Tensor) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or not t.is_contiguous():
+        raise Fatal(INTERNAL_INVARIANT, "snapshot tensors must be contiguous CUDA tensors")
+    return t
+
+
+class SnapshotStore:
+    """Latest committed (params, momentum) shard of this rank on its GPU."""
+
+    def __init__(self, capacity_bytes: int = 0, device=None, fabric=None, rank: int = 0,
+                 replica_id: int = 0, incarnation: int = 0):
+        if not torch.cuda.is_available():
+            raise Fatal(INTERNAL_INVARIANT, "SnapshotStore needs a CUDA device")
+        self.device = torch.device(device if device is not None else torch.cuda.current_device())
+        self.device_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        self.fabric = fabric
+        self.rank = rank
+        self.replica_id = replica_id
+        self.incarnation = incarnation
+        self._lock = threading.Lock()
+        self._snap = None
+        self._cap = 0
+        self._step = None
+        self._lens = (0, 0)
+        self._peers: dict[tuple[int, int], int] = {}
+        if capacity_bytes:
+            self._alloc(capacity_bytes)
+
+    def _alloc(self, capacity: int) -> None:
+        s = C.c_void_p()
+        exportable = self.fabric is not None and not isinstance(self.fabric, LocalFabric)
+        _lib.check(_lib.lib.ftar_snap_create(self.device_index, capacity, 1 if exportable else 0, C.byref(s)),
+                   "ftar_snap_create")
+        self._snap, self._cap = s, capacity
+        if exportable:
+            buf = (C.c_char * 64)()
+            n = C.c_size_t()
+            _lib.check(_lib.lib.ftar_snap_export(s, buf, 64, C.byref(n)), "ftar_snap_export")
+            self.fabric.publish(ArenaInfo(self.replica_id, self.rank, self.incarnation, self.device_index,
+                                          bytes(buf)[:n.value], capacity, pid=os.getpid()), what="snap")
+
+    @property
+    def handle(self):
+        return self._snap
+
+    def capture(self, step: int, params: torch.Tensor, momentum: torch.Tensor) -> None:
+        """Replace the snapshot with `step`'s shard (stream-ordered on the
+        current stream: the copy sees every prior write to params/momentum)."""
+        p, m = _as_bytes_tensor(params), _as_bytes_tensor(momentum)
+        pb, mb = p.numel() * p.element_size(), m.numel() * m.element_size()
+        with self._lock:
+            if self._snap is None:
+                self._alloc(pb + mb)
+            elif pb + mb > self._cap:
+                raise Fatal(INTERNAL_INVARIANT, f"snapshot of {pb + mb} bytes exceeds capacity {self._cap}")
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+            _lib.check(_lib.lib.ftar_snap_capture(self._snap, step, p.data_ptr(), pb, m.data_ptr(), mb, stream),
+                       "ftar_snap_capture")
+            self._step, self._lens = step, (pb, mb)
+
+    @property
+    def step(self):
+        with self._lock:
+            return self._step
+
+    def device_step(self):
+        """The step recorded in the device header (synchronises)."""
+        if self._snap is None:
+            return None
+        st, pb, mb = C.c_int64(), C.c_uint64(), C.c_uint64()
+        _lib.check(_lib.lib.ftar_snap_info(self._snap, C.byref(st), C.byref(pb), C.byref(mb)), "ftar_snap_info")
+        return None if st.value < 0 else st.value
+
+    def get(self, step: int):
+        """Lengths of the held shard if it is `step` (checkpoint.py:76-80)."""
+        with self._lock:
+            if self._step != step:
+                raise SnapshotUnavailable(self._step)
+            return self._lens
+
+    def close(self) -> None:
+        if self._snap is not None:
+            _lib.lib.ftar_snap_destroy(self._snap)
+            self._snap = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    # --- recovering side --------------------------------------------------------
+    def _map_donor(self, donor_replica: int, rank: int, timeout_s: float) -> int:
+        info = self.fabric.lookup(rank, donor_replica, timeout_s, what="snap")
+        key = (donor_replica, info.incarnation)
+        if key not in self._peers:
+            slot = len(self._peers) % 256
+            rc = _lib.lib.ftar_snap_import(self._snap, slot, info.handle, len(info.handle), info.arena_bytes)
+            if rc:
+                raise Recoverable(PEER_DOWN, f"cannot map snapshot of replica {donor_replica}: {_lib.last_error()}")
+            self._peers[key] = slot
+        return self._peers[key]
+
+
+class CatchupPull:
+    """One in-flight pull of a donor snapshot (non-blocking catch-up)."""
+
+    def __init__(self, local: SnapshotStore, params: torch.Tensor, momentum: torch.Tensor, stream,
+                 timeout_s: float):
+        self.local, self.params, self.momentum = local, params, momentum
+        self.stream = stream
+        self.timeout_s = timeout_s
+        self.event = None
+
+    def poll(self):
+        st, prog, avail = C.c_int(), C.c_uint64(), C.c_int64()
+        _lib.lib.ftar_snap_poll(self.local.handle, C.byref(st), C.byref(prog), C.byref(avail))
+        return st.value, prog.value
+
+    def wait(self):
+        avail = C.c_int64(-1)
+        st = _lib.lib.ftar_snap_wait(self.local.handle, self.timeout_s, C.byref(avail))
+        if st == _lib_status("UNAVAILABLE"):
+            raise SnapshotUnavailable(None if avail.value < 0 else avail.value)
+        if st:
+            raise from_status(st, _lib.last_error() if st == 10 else "catch-up pull failed")
+        # make the consumer stream see the pulled bytes
+        torch.cuda.current_stream(self.local.device).wait_stream(self.stream)
+        return self.params, self.momentum
+
+
+def _lib_status(name: str) -> int:
+    return {"UNAVAILABLE": 9}[name]
+
+
+_side_streams: dict[int, torch.cuda.Stream] = {}
+
+
+def catchup_stream(device: torch.device) -> torch.cuda.Stream:
+    """A low-priority side stream per device for catch-up pulls."""
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    if idx not in _side_streams:
+        lo, hi = torch.cuda.Stream.priority_range()
+        _side_streams[idx] = torch.cuda.Stream(device=idx, priority=lo if lo > hi else 0)
+    return _side_streams[idx]
+
+
+def start_fetch(local: SnapshotStore, donor, step: int, rank: int, params_out: torch.Tensor,
+                momentum_out: torch.Tensor, timeout_s: float = 5.0, ctas: int = 16) -> CatchupPull:
+    """Launch the pull of `donor`'s snapshot of `step` into the given tensors
+    without waiting.  `donor` is a SnapshotStore in this process (same device)
+    or a replica id resolved through ``local.fabric``."""
+    p, m = _as_bytes_tensor(params_out), _as_bytes_tensor(momentum_out)
+    pb, mb = p.numel() * p.element_size(), m.numel() * m.element_size()
+    if local.handle is None:
+        local._alloc(max(pb + mb, 16))
+    if isinstance(donor, SnapshotStore):
+        slot, src = -1, donor.handle
+        if src is None:
+            raise SnapshotUnavailable(None)
+    else:
+        slot, src = local._map_donor(int(donor), rank, timeout_s), None
+    stream = catchup_stream(local.device)
+    stream.wait_stream(torch.cuda.current_stream(local.device))
+    rc = _lib.lib.ftar_snap_pull_launch(local.handle, slot, src, step, p.data_ptr(), pb, m.data_ptr(), mb,
+                                        ctas, stream.cuda_stream)
+    _lib.check(rc, "ftar_snap_pull_launch")
+    return CatchupPull(local, p, m, stream, timeout_s)
+
+
+def fetch_shard(donor, step: int, rank: int, replica_id: int = 0, incarnation: int = 0,
+                timeout_s: float = 5.0, plan=None, *, local: SnapshotStore | None = None,
+                out: tuple[torch.Tensor, torch.Tensor] | None = None, ctas: int = 16):
+    """Pull (params, momentum) of one rank shard of a committed step
+    (checkpoint.py:117-144).  Blocks until done; raises SnapshotUnavailable
+    when the donor holds another step and Recoverable when it is gone."""
+    if local is None:
+        raise Fatal(INTERNAL_INVARIANT, "fetch_shard needs the recovering replica's SnapshotStore (local=)")
+    if out is None:
+        if isinstance(donor, SnapshotStore):
+            pb, mb = donor._lens
+        else:
+            raise Fatal(INTERNAL_INVARIANT, "out= tensors are required for a remote donor")
+        out = (torch.empty(pb, dtype=torch.uint8, device=local.device),
+               torch.empty(mb, dtype=torch.uint8, device=local.device))
+    return start_fetch(local, donor, step, rank, out[0], out[1], timeout_s, ctas).wait()
+
+
+def pick_donor(healthy, self_replica: int, rank: int, attempt: int = 0) -> int:
+    """checkpoint.py:147-154: rank r pulls from donor (r + attempt) mod H."""
+    donors = sorted(r for r in healthy if r != self_replica)
+    if not donors:
+        raise Recoverable(PEER_DOWN, "no donors available")
+    return donors[(rank + attempt) % len(donors)]
+
+
+def serve_fetches(router=None, store: SnapshotStore | None = None, stop=None, pred=None) -> None:
+    """API shape of checkpoint.py:83-95.  NVLink donors need no server: the
+    snapshot arena is published when allocated and peers read it directly."""
+    return None

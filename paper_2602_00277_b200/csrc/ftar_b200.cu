@@ -1,0 +1,1389 @@
+// ftar_b200.cu — sm_100a kernels and the C-ABI runtime of the B200 FTAR data
+// plane (declared in include/ftar_b200.h).
+//
+// Hot path (replaces ftar.py:301-398 + kernels.py / _ckernels.pyx):
+//   one persistent kernel per member and call, G CTAs x 512 threads:
+//     1. entry    publish {input offset, call tag}; wait until every ring
+//                 member has entered the same (generation, seq)
+//     2. RS       reduce my contiguous slice: 128-bit NVLink loads of every
+//                 live member's input, fp32 fold in the reference's order
+//                 (per element: start at the owner of its partition segment,
+//                 ascending ring index — tests/test_ftar.py:20-40), fused
+//                 bf16->fp32 upcast, non-finite detection (warp vote) and the
+//                 optional x f32(1/(h*R)) scale (replica.py:622-626); result
+//                 to my arena's result region; last CTA publishes rs_done
+//     3. barrier  wait for every member's rs_done; any non-finite -> NUMERICAL
+//                 (nothing committed anywhere, ftar.py:351-352)
+//     4. AG       pull every member's reduced slice over NVLink into `out`
+//   Every wait is bounded (generation-tagged flag + peer poison word + host
+//   abort word + device hard timeout), so a dead peer turns into a status,
+//   never a hung GPU.  The host polls progress/done words in pinned memory.
+#include "ftar_device.cuh"
+#include "../../include/ftar_b200.h"
+
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <thread>
+
+using namespace ftar;
+
+// ============================================================================
+// device code
+// ============================================================================
+
+namespace {
+
+__host__ __device__ __forceinline__ uint64_t umin(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ uint64_t umax(uint64_t a, uint64_t b) { return a > b ? a : b; }
+
+constexpr uint32_t ST_FOLLOW = 254;  // stop because another CTA of mine failed
+
+struct LaunchParams {
+  char* base[kMaxMembers];       // arena base of ring member i, as mapped here
+  HostCtl* ctl[kMaxMembers];     // control block of member i (device view)
+  float* out[kMaxMembers];       // fp32 output of member i
+  uint64_t in_off[kMaxMembers];  // member i's input address - its arena base
+  uint64_t res_off[kMaxMembers]; // member i's result region offset
+  uint64_t tag;
+  uint64_t nelems;
+  uint64_t slice;                // elements reduced per ring index (multiple of 8)
+  uint64_t p_base, p_rem;        // partition lengths: p_rem of p_base+1, rest p_base
+  uint64_t cap;                  // partition cap (elements), validated across members
+  uint64_t hard_timeout_ns;
+  float scale;
+  uint32_t flags;
+  uint32_t contrib;              // bit i: ring index i contributes data (healthy)
+  uint32_t dtype;
+  int self;                      // my ring index (real mode)
+  int emulated;                  // 1: ring index = blockIdx.y (in-process ring)
+  int fault_member;              // test hook (-1 none)
+  int fault_after_tiles;
+};
+
+__device__ __forceinline__ uint32_t severity_code(uint32_t st) {
+  uint32_t sev = (st == ST_INJECTED) ? 3u
+               : (st == ST_PROTOCOL || st == ST_NUMERICAL || st == ST_INVARIANT) ? 2u : 1u;
+  return (sev << 8) | st;
+}
+
+// Bounded wait for *flag to carry `tag`.  Exits early on: the member's poison
+// word for this tag (it aborted -> PEER_RESET), a newer generation on the
+// flag (I am stale -> PEER_RESET), a newer call of the same generation
+// (sequence skew -> PROTOCOL), the host abort word, another CTA of mine
+// failing (FOLLOW), or the device hard timeout.
+__device__ uint32_t wait_flag(const uint64_t* flag, uint64_t tag, const uint64_t* poison,
+                              const HostCtl* ctl, const uint32_t* own_err, uint64_t t0,
+                              uint64_t limit_ns, uint32_t* bits) {
+  for (uint32_t it = 0;; ++it) {
+    const uint64_t f = ld_acquire_sys(flag);
+    const uint64_t ft = flag_tag(f);
+    if (ft == tag) {
+      if (bits) *bits = (uint32_t)(f & 0xffu);
+      return ST_OK;
+    }
+    if (ft > tag) return tag_gen(ft) > tag_gen(tag) ? ST_PEER_RESET : ST_PROTOCOL;
+    if ((it & 15u) == 15u) {
+      if (poison && flag_tag(ld_acquire_sys(poison)) == tag) return ST_PEER_RESET;
+      if (ctl->abort_tag == tag) return ST_ABORTED;
+      if (own_err && ld_relaxed_sys32(own_err) != 0) return ST_FOLLOW;
+      if (globaltimer_ns() - t0 > limit_ns) return ST_TIMEOUT;
+    }
+    if (it > 256) __nanosleep(200);
+  }
+}
+
+// Owner (segment index) of element e under the reference geometry
+// (build_partition_plan ftar.py:80-99 + segment_bounds ftar.py:102-112), and
+// the element index where that segment ends.
+__device__ __forceinline__ void owner_of(uint64_t e, const LaunchParams& p, int n,
+                                         int& owner, uint64_t& seg_end) {
+  const uint64_t big = p.p_rem * (p.p_base + 1);
+  uint64_t poff, L;
+  if (e < big) {
+    const uint64_t pi = e / (p.p_base + 1);
+    poff = pi * (p.p_base + 1);
+    L = p.p_base + 1;
+  } else {
+    const uint64_t pi = (e - big) / p.p_base;
+    poff = big + pi * p.p_base;
+    L = p.p_base;
+  }
+  const uint64_t off = e - poff;
+  const uint64_t sb = L / (uint64_t)n, sr = L % (uint64_t)n;
+  const uint64_t sbig = sr * (sb + 1);
+  uint64_t j, send;
+  if (off < sbig) {
+    j = off / (sb + 1);
+    send = (j + 1) * (sb + 1);
+  } else {
+    j = sr + (off - sbig) / sb;
+    send = sbig + (j - sr + 1) * sb;
+  }
+  owner = (int)j;
+  seg_end = poff + send;
+}
+
+// Reduce elements [a, b) whose fold starts at ring index s.  All threads of the
+// CTA cooperate; 16-byte vectors in the body, scalars at the ragged edges.
+template <int N, class In, int U>
+__device__ __forceinline__ void fold_range(const typename In::T* const* src, float* res,
+                                           uint64_t a, uint64_t b, int s, uint32_t contrib,
+                                           bool vec_ok, bool do_scale, float scale,
+                                           uint32_t& nf) {
+  using T = typename In::T;
+  const T* rs[N];
+  bool cb[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    int m = s + k;
+    if (m >= N) m -= N;
+    rs[k] = src[m];
+    cb[k] = (contrib >> m) & 1u;
+  }
+  const int tid = threadIdx.x;
+  auto scalar_elem = [&](uint64_t e) {
+    float acc = cb[0] ? In::scalar(rs[0], e) : 0.0f;
+#pragma unroll
+    for (int k = 1; k < N; ++k) {
+      const float x = cb[k] ? In::scalar(rs[k], e) : 0.0f;
+      acc = __fadd_rn(acc, x);
+    }
+    nf |= nonfinite_bits(acc) ? 1u : 0u;
+    if (do_scale) acc = __fmul_rn(acc, scale);
+    res[e] = acc;
+  };
+  if (!vec_ok) {
+    for (uint64_t e = a + tid; e < b; e += kThreads) scalar_elem(e);
+    return;
+  }
+  const uint64_t head = umin(b, (a + 7) & ~7ull);
+  if (a + tid < head) scalar_elem(a + tid);
+  const uint64_t vb = head >> 3, ve = b >> 3;
+  for (uint64_t v0 = vb + tid; v0 < ve; v0 += (uint64_t)kThreads * U) {
+    float x[U][N][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t v = v0 + (uint64_t)u * kThreads;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        if (v < ve && cb[k]) {
+          In::load8(rs[k], v * 8, x[u][k]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[u][k][i] = 0.0f;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t v = v0 + (uint64_t)u * kThreads;
+      if (v < ve) {
+        float acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          acc[i] = x[u][0][i];
+#pragma unroll
+          for (int k = 1; k < N; ++k) acc[i] = __fadd_rn(acc[i], x[u][k][i]);
+          nf |= nonfinite_bits(acc[i]) ? 1u : 0u;
+          if (do_scale) acc[i] = __fmul_rn(acc[i], scale);
+        }
+        float4* d = reinterpret_cast<float4*>(res + v * 8);
+        d[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        d[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      }
+    }
+  }
+  const uint64_t tail = umax(head, ve << 3);
+  if (tail + tid < b) scalar_elem(tail + tid);
+}
+
+// Grid-stride fp32 copy (the all-gather pull), 16-byte vectors, UA loads in
+// flight per thread before the stores.
+template <int UA>
+__device__ __forceinline__ void copy_f32(float* dst, const float* src, uint64_t cnt, bool vec_ok) {
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  const uint64_t first = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (!vec_ok) {
+    for (uint64_t e = first; e < cnt; e += stride) dst[e] = src[e];
+    return;
+  }
+  const uint64_t nv = cnt >> 2;
+  for (uint64_t v = first; v < nv; v += stride * UA) {
+    uint4 r[UA];
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      const uint64_t i = v + (uint64_t)u * stride;
+      if (i < nv) r[u] = ld_stream(src + i * 4);
+    }
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      const uint64_t i = v + (uint64_t)u * stride;
+      if (i < nv) *reinterpret_cast<uint4*>(dst + i * 4) = r[u];
+    }
+  }
+  const uint64_t t = (nv << 2) + first;
+  if (t < cnt && first < 4) dst[t] = src[t];
+}
+
+template <int N>
+struct Unroll { static constexpr int U = (N <= 2) ? 4 : (N <= 4 ? 2 : 1); };
+
+template <int N, class In>
+__global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_constant__ LaunchParams p) {
+  using T = typename In::T;
+  constexpr int U = Unroll<N>::U;
+  const int me = p.emulated ? (int)blockIdx.y : p.self;
+  char* const mybase = p.base[me];
+  ArenaHdr* const hdr = reinterpret_cast<ArenaHdr*>(mybase);
+  HostCtl* const ctl = p.ctl[me];
+  const uint64_t tag = p.tag;
+  const uint64_t E = p.nelems;
+  const int tid = threadIdx.x;
+
+  __shared__ const T* s_src[N];
+  __shared__ const float* s_res[N];
+  __shared__ uint32_t s_status;
+  __shared__ int s_blame;
+  __shared__ uint32_t s_nf;
+  __shared__ uint32_t s_stop[2];
+  __shared__ int s_vec_ok;
+  __shared__ uint64_t s_t0;
+
+  if (tid == 0) {
+    s_status = ST_OK;
+    s_blame = -1;
+    s_nf = 0;
+    s_stop[0] = s_stop[1] = 0;
+    s_t0 = globaltimer_ns();
+    if (blockIdx.x == 0) {
+      // Epoch fence: an op queued under an older decision must not run
+      // against the membership the control plane has since installed.
+      if (ctl->epoch != tag_gen(tag)) {
+        s_status = ST_PROTOCOL;
+        s_blame = me;
+      }
+      ctl->started = tag;
+      if (s_status == ST_OK) {
+        EntryRec* en = &hdr->entry;
+        en->in_off = p.in_off[me];
+        en->res_off = p.res_off[me];
+        en->nelems = E;
+        en->geom = p.cap;
+        en->dtype = p.dtype;
+        en->n = (uint32_t)N;
+        __threadfence_system();
+        st_release_sys(&en->flag, mk_flag(tag, 0));
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- 1. entry barrier -------------------------------------------------
+  if (tid == 0 && s_status == ST_OK) {
+    int ok = 1;
+    for (int j = 0; j < N; ++j) {
+      if (j == me) {
+        s_src[j] = reinterpret_cast<const T*>(mybase + p.in_off[me]);
+        s_res[j] = reinterpret_cast<const float*>(mybase + p.res_off[me]);
+        continue;
+      }
+      ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
+      uint32_t st = wait_flag(&ph->entry.flag, tag, &ph->poison, ctl, &hdr->err, s_t0,
+                              p.hard_timeout_ns, nullptr);
+      uint64_t in_off = 0, res_off = 0;
+      if (st == ST_OK) {
+        in_off = ld_relaxed_sys(&ph->entry.in_off);
+        res_off = ld_relaxed_sys(&ph->entry.res_off);
+        const uint64_t ne = ld_relaxed_sys(&ph->entry.nelems);
+        const uint64_t ge = ld_relaxed_sys(&ph->entry.geom);
+        const uint64_t dn = ld_relaxed_sys(reinterpret_cast<const uint64_t*>(&ph->entry.dtype));
+        const uint64_t want_dn = (uint64_t)p.dtype | ((uint64_t)N << 32);
+        if (ne != E || ge != p.cap || dn != want_dn) st = ST_PROTOCOL;
+      }
+      if (st != ST_OK) {
+        s_status = st;
+        s_blame = j;
+        ok = 0;
+        break;
+      }
+      s_src[j] = reinterpret_cast<const T*>(p.base[j] + in_off);
+      s_res[j] = reinterpret_cast<const float*>(p.base[j] + res_off);
+    }
+    if (ok) {
+      uint64_t orbits = reinterpret_cast<uint64_t>(p.out[me]);
+      for (int j = 0; j < N; ++j)
+        orbits |= reinterpret_cast<uint64_t>(s_src[j]) | reinterpret_cast<uint64_t>(s_res[j]);
+      s_vec_ok = (orbits & 15u) == 0;
+    }
+  }
+  __syncthreads();
+
+  // ---- 2. reduce-scatter of my slice -----------------------------------
+  const uint64_t lo = umin((uint64_t)me * p.slice, E);
+  const uint64_t hi = umin(lo + p.slice, E);
+  uint32_t nf = 0;
+  if (s_status == ST_OK) {
+    float* const res = reinterpret_cast<float*>(mybase + p.res_off[me]) - lo;
+    const bool vec_ok = s_vec_ok != 0;
+    const bool do_scale = (p.flags & FTAR_F_SCALE) != 0;
+    const uint64_t TL = (uint64_t)kThreads * 8 * U;
+    const uint64_t ntiles = (hi - lo + TL - 1) / TL;
+    int done = 0;
+    uint32_t it = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      if (tid == 0) {
+        uint32_t stop = 0;
+        if (p.fault_member == me && done >= p.fault_after_tiles) {
+          s_status = ST_INJECTED;
+          stop = 1;
+        } else if (ld_relaxed_sys32(&hdr->err) != 0) {
+          s_status = ST_FOLLOW;
+          stop = 1;
+        }
+        s_stop[it & 1] = stop;
+      }
+      __syncthreads();
+      if (s_stop[it & 1]) break;
+      const uint64_t a = lo + t * TL, b = umin(a + TL, hi);
+      uint64_t cur = a;
+      while (cur < b) {
+        int s;
+        uint64_t send;
+        owner_of(cur, p, N, s, send);
+        const uint64_t end = umin(send, b);
+        fold_range<N, In, U>(s_src, res, cur, end, s, p.contrib, vec_ok, do_scale, p.scale, nf);
+        cur = end;
+      }
+      ++done;
+      if (tid == 0) {
+        const unsigned long long v =
+            atomicAdd(reinterpret_cast<unsigned long long*>(&hdr->tiles_done), 1ull) + 1ull;
+        if ((v & 3ull) == 0) ctl->progress = v;
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, nf != 0) && (tid & 31) == 0) atomicOr(&s_nf, 1u);
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t st = s_status;
+    if (st == ST_OK && s_nf) atomicOr(&hdr->nonfinite, 1u);
+    if (st != ST_OK && st != ST_FOLLOW) {
+      atomicMax(&hdr->err, severity_code(st));
+      hdr->err_peer = s_blame;
+      if (st != ST_INJECTED) st_release_sys(&hdr->poison, mk_flag(tag, st));
+    }
+    __threadfence_system();
+    const uint32_t old = atomicAdd(&hdr->rs_arrive, 1u);
+    if (old == gridDim.x - 1) {
+      __threadfence_system();
+      if (ld_relaxed_sys32(&hdr->err) == 0) {
+        const uint32_t bits = ld_relaxed_sys32(&hdr->nonfinite) ? kBitNonFinite : 0u;
+        st_release_sys(&hdr->rs_done, mk_flag(tag, bits));
+      }
+    }
+  }
+
+  // ---- 3. reduce-scatter -> all-gather barrier ----------------------------
+  if (tid == 0 && s_status == ST_OK) {
+    uint32_t bits = 0;
+    for (int jj = 0; jj < N; ++jj) {
+      const int j = (me + jj) % N;
+      ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
+      uint32_t b = 0;
+      uint32_t st = wait_flag(&ph->rs_done, tag, j == me ? nullptr : &ph->poison, ctl,
+                              &hdr->err, s_t0, p.hard_timeout_ns, &b);
+      if (st != ST_OK) {
+        s_status = st;
+        s_blame = j;
+        break;
+      }
+      bits |= b;
+    }
+    if (s_status == ST_OK && (bits & kBitNonFinite)) s_status = ST_NUMERICAL;
+  }
+  __syncthreads();
+
+  // ---- 4. all-gather pull (commit) ---------------------------------------
+  if (s_status == ST_OK) {
+    float* const out = p.out[me];
+    const bool vec_ok = s_vec_ok != 0;
+    for (int i = 0; i < N; ++i) {
+      const int k = (int)((me + 1 + blockIdx.x + i) % N);
+      const uint64_t klo = umin((uint64_t)k * p.slice, E), khi = umin(klo + p.slice, E);
+      copy_f32<8>(out + klo, s_res[k], khi - klo, vec_ok);
+    }
+  }
+  __syncthreads();
+
+  // ---- 5. completion -----------------------------------------------------
+  if (tid == 0) {
+    const uint32_t st = s_status;
+    if (st != ST_OK && st != ST_FOLLOW) {
+      atomicMax(&hdr->err, severity_code(st));
+      hdr->err_peer = s_blame;
+      if (st != ST_INJECTED && st != ST_NUMERICAL) st_release_sys(&hdr->poison, mk_flag(tag, st));
+    }
+    __threadfence_system();
+    const uint32_t old = atomicAdd(&hdr->done_arrive, 1u);
+    if (old == gridDim.x - 1) {
+      __threadfence_system();
+      const uint32_t err = ld_relaxed_sys32(&hdr->err);
+      const uint64_t tiles = hdr->tiles_done;
+      ctl->detail = err ? (int64_t)hdr->err_peer : -1;
+      ctl->progress = tiles + 1;
+      hdr->rs_arrive = 0;
+      hdr->done_arrive = 0;
+      hdr->nonfinite = 0;
+      hdr->err = 0;
+      hdr->err_peer = -1;
+      hdr->tiles_done = 0;
+      __threadfence_system();
+      ctl->done = mk_flag(tag, err & 0xffu);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- operators
+template <class In>
+__global__ void __launch_bounds__(256) accumulate_kernel(float* __restrict__ dst,
+                                                         const typename In::T* __restrict__ src,
+                                                         uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride)
+    dst[e] = __fadd_rn(dst[e], In::scalar(src, e));
+}
+template <class In>
+__global__ void __launch_bounds__(256) copy_into_kernel(float* __restrict__ dst,
+                                                        const typename In::T* __restrict__ src,
+                                                        uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride)
+    dst[e] = In::scalar(src, e);
+}
+
+// ---------------------------------------------------------------- catch-up
+__global__ void snap_mark_kernel(SnapHdr* h, int64_t step, uint64_t pb, uint64_t mb, int begin) {
+  if (begin) {
+    h->seq = h->seq + 1;  // odd: capture in progress
+    __threadfence_system();
+  } else {
+    h->step = step;
+    h->pbytes = pb;
+    h->mbytes = mb;
+    __threadfence_system();
+    st_release_sys(&h->seq, h->seq + 1);  // even: stable
+  }
+}
+
+// Byte copy of [0, bytes) with 16-byte vectors when aligned.
+__device__ __forceinline__ void copy_bytes_grid(char* dst, const char* src, uint64_t bytes,
+                                                uint64_t first, uint64_t stride) {
+  const bool vec = ((reinterpret_cast<uint64_t>(dst) | reinterpret_cast<uint64_t>(src)) & 15u) == 0;
+  if (!vec) {
+    for (uint64_t i = first; i < bytes; i += stride) dst[i] = src[i];
+    return;
+  }
+  const uint64_t nv = bytes >> 4;
+  constexpr int UA = 8;
+  for (uint64_t v = first; v < nv; v += stride * UA) {
+    uint4 r[UA];
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      const uint64_t i = v + (uint64_t)u * stride;
+      if (i < nv) r[u] = ld_stream(src + i * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      const uint64_t i = v + (uint64_t)u * stride;
+      if (i < nv) *reinterpret_cast<uint4*>(dst + i * 16) = r[u];
+    }
+  }
+  const uint64_t t = (nv << 4) + first;
+  if (t < bytes && first < 16) dst[t] = src[t];
+}
+
+__global__ void __launch_bounds__(kThreads) snap_copy_kernel(char* dst, const char* p, uint64_t pb,
+                                                             const char* m, uint64_t mb) {
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  const uint64_t first = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  copy_bytes_grid(dst, p, pb, first, stride);
+  copy_bytes_grid(dst + pb, m, mb, first, stride);
+}
+
+// Pull a donor snapshot (over NVLink when `src` is a peer mapping) in chunks,
+// honouring the host abort word, publishing progress, and validating the
+// donor's seqlock across the whole pull.
+constexpr uint64_t kPullChunk = 1ull << 20;
+
+__global__ void __launch_bounds__(kThreads, 1)
+snap_pull_kernel(const char* src_arena, SnapHdr* lhdr, HostCtl* ctl, uint64_t tag, int64_t want,
+                 char* dp, uint64_t pb, char* dm, uint64_t mb) {
+  const SnapHdr* sh = reinterpret_cast<const SnapHdr*>(src_arena);
+  const char* data = src_arena + kSnapHdrBytes;
+  __shared__ uint32_t s_st;
+  __shared__ uint64_t s_seq;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    if (blockIdx.x == 0) ctl->started = tag;
+    s_st = ST_OK;
+    const uint64_t seq = ld_acquire_sys(&sh->seq);
+    const int64_t step = (int64_t)ld_relaxed_sys(reinterpret_cast<const uint64_t*>(&sh->step));
+    const uint64_t spb = ld_relaxed_sys(&sh->pbytes), smb = ld_relaxed_sys(&sh->mbytes);
+    if ((seq & 1u) || step != want || spb != pb || smb != mb) {
+      s_st = ST_UNAVAILABLE;
+      if (blockIdx.x == 0) ctl->available = (seq & 1u) ? -1 : step;
+    }
+    s_seq = seq;
+    atomicMin(reinterpret_cast<unsigned long long*>(&lhdr->seq_min), (unsigned long long)seq);
+    atomicMax(reinterpret_cast<unsigned long long*>(&lhdr->seq_max), (unsigned long long)seq);
+  }
+  __syncthreads();
+  const uint64_t total = pb + mb;
+  const uint64_t nchunks = (total + kPullChunk - 1) / kPullChunk;
+  if (s_st == ST_OK) {
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      if (tid == 0 && (ctl->abort_tag == tag || ld_relaxed_sys32(&lhdr->err) != 0)) s_st = ST_ABORTED;
+      __syncthreads();
+      if (s_st != ST_OK) break;
+      const uint64_t a = c * kPullChunk, b = umin(a + kPullChunk, total);
+      // a chunk may straddle params|momentum
+      if (a < pb) {
+        const uint64_t e = umin(b, pb);
+        copy_bytes_grid(dp + a, data + a, e - a, tid, kThreads);
+      }
+      if (b > pb) {
+        const uint64_t s = umax(a, pb);
+        copy_bytes_grid(dm + (s - pb), data + s, b - s, tid, kThreads);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        const unsigned long long v =
+            atomicAdd(reinterpret_cast<unsigned long long*>(&lhdr->bytes_done), (unsigned long long)(b - a)) +
+            (b - a);
+        ctl->progress = v;
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint64_t seq2 = ld_acquire_sys(&sh->seq);
+    atomicMax(reinterpret_cast<unsigned long long*>(&lhdr->seq_max), (unsigned long long)seq2);
+    if (s_st != ST_OK) atomicMax(&lhdr->err, s_st);
+    __threadfence_system();
+    const uint32_t old = atomicAdd(&lhdr->done_arrive, 1u);
+    if (old == gridDim.x - 1) {
+      __threadfence_system();
+      uint32_t err = ld_relaxed_sys32(&lhdr->err);
+      const uint64_t smin = ld_relaxed_sys(&lhdr->seq_min), smax = ld_relaxed_sys(&lhdr->seq_max);
+      if (err == ST_OK && smin != smax) {  // donor re-captured mid-pull: torn
+        err = ST_UNAVAILABLE;
+        ctl->available = (int64_t)ld_relaxed_sys(reinterpret_cast<const uint64_t*>(&sh->step));
+      }
+      ctl->progress = lhdr->bytes_done;
+      lhdr->seq_min = ~0ull;
+      lhdr->seq_max = 0;
+      lhdr->err = 0;
+      lhdr->done_arrive = 0;
+      lhdr->bytes_done = 0;
+      __threadfence_system();
+      ctl->done = mk_flag(tag, err);
+    }
+  }
+}
+
+__global__ void snap_init_kernel(SnapHdr* h) {
+  h->seq = 0;
+  h->step = -1;
+  h->pbytes = h->mbytes = 0;
+  h->seq_min = ~0ull;
+  h->seq_max = 0;
+  h->done_arrive = 0;
+  h->err = 0;
+  h->bytes_done = 0;
+}
+
+}  // namespace
+
+// ============================================================================
+// host runtime (C-ABI)
+// ============================================================================
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return FTAR_ST_CUDA;
+}
+#define CK(call)                                  \
+  do {                                            \
+    cudaError_t _e = (call);                      \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+constexpr int kMaxSlots = 256;
+
+int g_ctas = 0;         // real-mode CTAs per member (0 = default)
+int g_local_ctas = 0;   // in-process ring CTAs per member (0 = default)
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+int real_ctas() { return g_ctas > 0 ? g_ctas : env_int("FTAR_CTAS", 32); }
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+struct ftar_ctx {
+  int device = 0;
+  bool exportable = false;
+  char* arena = nullptr;
+  uint64_t arena_bytes = 0;
+  uint64_t max_bucket_bytes = 0;
+  uint64_t res_off = 0, stage_off[2] = {0, 0}, pool_off = 0, pool_bytes = 0;
+  HostCtl* ctl_h = nullptr;
+  HostCtl* ctl_d = nullptr;
+  char* peer[kMaxSlots] = {};
+  uint64_t peer_bytes[kMaxSlots] = {};
+  int ring_slots[kMaxMembers] = {};
+  int n = 1, self = 0;
+  uint32_t contrib = 1;
+  uint64_t gen = 0, seq = 0;
+  uint64_t cur_tag = 0;
+  bool inflight = false;
+  uint64_t hard_timeout_ns = 120ull * 1000000000ull;
+};
+
+struct ftar_snap {
+  int device = 0;
+  char* arena = nullptr;
+  uint64_t cap = 0;
+  HostCtl* ctl_h = nullptr;
+  HostCtl* ctl_d = nullptr;
+  char* peer[kMaxSlots] = {};
+  uint64_t seq = 0;
+  uint64_t cur_tag = 0;
+  bool inflight = false;
+};
+
+namespace {
+
+template <int N, class In>
+cudaError_t launch_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop) {
+  auto fn = allreduce_kernel<N, In>;
+  if (coop) {
+    void* args[] = {const_cast<LaunchParams*>(&p)};
+    return cudaLaunchCooperativeKernel((const void*)fn, grid, dim3(kThreads), args, 0, st);
+  }
+  fn<<<grid, kThreads, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <class In>
+cudaError_t launch_dispatch(int n, const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop) {
+  switch (n) {
+    case 1: return launch_n<1, In>(p, grid, st, coop);
+    case 2: return launch_n<2, In>(p, grid, st, coop);
+    case 3: return launch_n<3, In>(p, grid, st, coop);
+    case 4: return launch_n<4, In>(p, grid, st, coop);
+    case 5: return launch_n<5, In>(p, grid, st, coop);
+    case 6: return launch_n<6, In>(p, grid, st, coop);
+    case 7: return launch_n<7, In>(p, grid, st, coop);
+    case 8: return launch_n<8, In>(p, grid, st, coop);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <class In>
+int max_coop_blocks_per_sm(int n) {
+  int nb = 0;
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (n) {
+#define CASE(K) case K: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, allreduce_kernel<K, In>, kThreads, 0); break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+  }
+  return e == cudaSuccess ? nb : 0;
+}
+
+// Reference geometry (elements; ELEM = 4 bytes of the fp32 view).
+void fill_geometry(LaunchParams& p, uint64_t E, uint64_t chunk_bytes, int C, int n) {
+  uint64_t cap = (chunk_bytes * (uint64_t)C * (uint64_t)n) / 4;
+  if (cap < 1) cap = 1;
+  p.cap = cap;
+  if (E == 0) {
+    p.p_base = 1;
+    p.p_rem = 0;
+  } else {
+    const uint64_t nparts = (E + cap - 1) / cap;
+    p.p_base = E / nparts;
+    p.p_rem = E % nparts;
+  }
+  const uint64_t per = (E + (uint64_t)n - 1) / (uint64_t)n;
+  p.slice = (per + 7) & ~7ull;
+  if (p.slice == 0) p.slice = 8;
+}
+
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+int validate_common(int in_dtype, int n, uint64_t chunk_bytes, int max_in_flight) {
+  if (in_dtype != FTAR_DT_F32 && in_dtype != FTAR_DT_BF16)
+    return fail(FTAR_ST_INVARIANT, "all-reduce input must be float32 or bfloat16");
+  if (n < 1 || n > kMaxMembers) return fail(FTAR_ST_INVARIANT, "ring size out of range 1..8");
+  if (chunk_bytes < 4) return fail(FTAR_ST_INVARIANT, "chunk_bytes must be >= 4");
+  if (max_in_flight < 1) return fail(FTAR_ST_INVARIANT, "max_in_flight must be >= 1");
+  return FTAR_OK;
+}
+
+void reset_ctl(HostCtl* c) {
+  c->abort_tag = 0;
+  c->started = 0;
+  c->progress = 0;
+  c->done = 0;
+  c->detail = -1;
+  c->available = -1;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ftar_last_error(void) { return g_err.c_str(); }
+const char* ftar_version(void) { return "ftar_b200 1.0 sm_100a (two-shot NVLink pull, fp32 fold)"; }
+
+int ftar_set_tuning(int ctas, int local_ctas) {
+  g_ctas = ctas;
+  g_local_ctas = local_ctas;
+  return FTAR_OK;
+}
+
+int ftar_ctx_create(int device, uint64_t max_bucket_bytes, uint64_t pool_bytes, int exportable,
+                    ftar_ctx** out) {
+  if (!out) return fail(FTAR_ST_INVARIANT, "null out");
+  DeviceGuard g(device);
+  ftar_ctx* c = new ftar_ctx();
+  c->device = device;
+  c->exportable = exportable != 0;
+  c->max_bucket_bytes = align_up(std::max<uint64_t>(max_bucket_bytes, 256), 256);
+  c->res_off = kHdrBytes;
+  // result region: my slice in fp32 <= ceil(E/2)+8 elems; E <= max_bucket_bytes/2 (bf16)
+  const uint64_t res_bytes = align_up(c->max_bucket_bytes + 64, 4096);
+  c->stage_off[0] = c->res_off + res_bytes;
+  c->stage_off[1] = c->stage_off[0] + c->max_bucket_bytes;
+  c->pool_off = c->stage_off[1] + c->max_bucket_bytes;
+  c->pool_bytes = align_up(pool_bytes, 4096);
+  c->arena_bytes = c->pool_off + c->pool_bytes;
+  cudaError_t e = cudaMalloc(&c->arena, c->arena_bytes);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaMalloc(arena)");
+  }
+  cudaMemset(c->arena, 0, kHdrBytes);
+  ArenaHdr init{};
+  init.err_peer = -1;
+  cudaMemcpy(c->arena, &init, sizeof(init), cudaMemcpyHostToDevice);
+  e = cudaHostAlloc(&c->ctl_h, sizeof(HostCtl), cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    cudaFree(c->arena);
+    delete c;
+    return cuda_fail(e, "cudaHostAlloc(ctl)");
+  }
+  std::memset((void*)c->ctl_h, 0, sizeof(HostCtl));
+  reset_ctl(c->ctl_h);
+  c->ctl_h->live_mask = 1;
+  c->ctl_h->contrib_mask = 1;
+  cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->ctl_d), (void*)c->ctl_h, 0);
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(e, "ctx init");
+  c->ring_slots[0] = -1;
+  *out = c;
+  return FTAR_OK;
+}
+
+int ftar_ctx_destroy(ftar_ctx* c) {
+  if (!c) return FTAR_OK;
+  DeviceGuard g(c->device);
+  cudaDeviceSynchronize();
+  for (int s = 0; s < kMaxSlots; ++s)
+    if (c->peer[s]) cudaIpcCloseMemHandle(c->peer[s]);
+  cudaFree(c->arena);
+  cudaFreeHost((void*)c->ctl_h);
+  delete c;
+  return FTAR_OK;
+}
+
+int ftar_ctx_pool(ftar_ctx* c, uint64_t* dev_ptr, uint64_t* bytes) {
+  if (!c) return fail(FTAR_ST_INVARIANT, "null ctx");
+  if (dev_ptr) *dev_ptr = reinterpret_cast<uint64_t>(c->arena + c->pool_off);
+  if (bytes) *bytes = c->pool_bytes;
+  return FTAR_OK;
+}
+
+int ftar_ctx_export(ftar_ctx* c, void* buf, size_t buflen, size_t* written) {
+  if (!c || !buf || buflen < sizeof(cudaIpcMemHandle_t)) return fail(FTAR_ST_INVARIANT, "bad export args");
+  DeviceGuard g(c->device);
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, c->arena));
+  std::memcpy(buf, &h, sizeof(h));
+  if (written) *written = sizeof(h);
+  return FTAR_OK;
+}
+
+int ftar_ctx_import(ftar_ctx* c, int slot, const void* handle, size_t len, uint64_t arena_bytes) {
+  if (!c || slot < 0 || slot >= kMaxSlots || !handle || len < sizeof(cudaIpcMemHandle_t))
+    return fail(FTAR_ST_INVARIANT, "bad import args");
+  DeviceGuard g(c->device);
+  if (c->peer[slot]) return FTAR_OK;  // cached mapping
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* p = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    g_err = std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e);
+    return FTAR_ST_PEER_DOWN;
+  }
+  c->peer[slot] = static_cast<char*>(p);
+  c->peer_bytes[slot] = arena_bytes;
+  return FTAR_OK;
+}
+
+int ftar_ctx_unmap(ftar_ctx* c, int slot) {
+  if (!c || slot < 0 || slot >= kMaxSlots) return fail(FTAR_ST_INVARIANT, "bad unmap args");
+  DeviceGuard g(c->device);
+  if (c->peer[slot]) {
+    cudaIpcCloseMemHandle(c->peer[slot]);
+    c->peer[slot] = nullptr;
+  }
+  return FTAR_OK;
+}
+
+int ftar_set_membership(ftar_ctx* c, const int* ring_slots, int n, int self_index,
+                        uint32_t contrib_mask, uint64_t generation) {
+  if (!c || n < 1 || n > kMaxMembers || self_index < 0 || self_index >= n)
+    return fail(FTAR_ST_INVARIANT, "bad membership");
+  if (generation > 0xffffffull) return fail(FTAR_ST_INVARIANT, "generation exceeds 24 bits");
+  if (c->inflight) {
+    int s = 0;
+    if (flag_tag(c->ctl_h->done) != c->cur_tag) return fail(FTAR_ST_INVARIANT, "membership change with an all-reduce in flight");
+    (void)s;
+    c->inflight = false;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (i == self_index) {
+      c->ring_slots[i] = -1;
+      continue;
+    }
+    const int s = ring_slots ? ring_slots[i] : -1;
+    if (s < 0 || s >= kMaxSlots || !c->peer[s]) return fail(FTAR_ST_INVARIANT, "ring member not mapped");
+    c->ring_slots[i] = s;
+  }
+  c->n = n;
+  c->self = self_index;
+  c->contrib = contrib_mask & ((n >= 32) ? 0xffffffffu : ((1u << n) - 1u));
+  c->gen = generation;
+  c->seq = 0;
+  c->ctl_h->live_mask = (n >= 32) ? 0xffffffffu : ((1u << n) - 1u);
+  c->ctl_h->contrib_mask = c->contrib;
+  c->ctl_h->epoch = generation;
+  return FTAR_OK;
+}
+
+int ftar_geometry(uint64_t n_elems, int n, uint64_t* slice_elems, int* ctas, int* threads) {
+  if (n < 1 || n > kMaxMembers) return fail(FTAR_ST_INVARIANT, "ring size out of range 1..8");
+  LaunchParams p{};
+  fill_geometry(p, n_elems, 4, 1, n);
+  if (slice_elems) *slice_elems = p.slice;
+  if (ctas) *ctas = real_ctas();
+  if (threads) *threads = kThreads;
+  return FTAR_OK;
+}
+
+int ftar_allreduce_launch(ftar_ctx* c, const void* in, int in_dtype, float* out, uint64_t n_elems,
+                          uint64_t chunk_bytes, int max_in_flight, float scale, uint32_t flags,
+                          void* stream) {
+  if (!c) return fail(FTAR_ST_INVARIANT, "null ctx");
+  int v = validate_common(in_dtype, c->n, chunk_bytes, max_in_flight);
+  if (v) return v;
+  if (c->inflight && flag_tag(c->ctl_h->done) != c->cur_tag)
+    return fail(FTAR_ST_INVARIANT, "one all-reduce in flight per ring group");
+  const uint64_t esz = in_dtype == FTAR_DT_BF16 ? 2 : 4;
+  const uint64_t in_bytes = n_elems * esz;
+  if (in_bytes > c->max_bucket_bytes || n_elems * 4 > 2 * c->max_bucket_bytes)
+    return fail(FTAR_ST_INVARIANT, "bucket exceeds the ring group's arena capacity");
+  if (n_elems && (!in || !out)) return fail(FTAR_ST_INVARIANT, "null buffer");
+  DeviceGuard g(c->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  c->seq += 1;
+  const uint64_t tag = mk_tag(c->gen, c->seq);
+  const char* inp = static_cast<const char*>(in);
+  uint64_t in_off;
+  const bool registered = inp >= c->arena + c->pool_off && inp + in_bytes <= c->arena + c->arena_bytes;
+  if (registered || c->n == 1) {
+    in_off = (uint64_t)(inp - c->arena);
+  } else {
+    // Unregistered bucket: peers can only read the arena, so stage it (double
+    // buffered by call parity: peers finished reading this half two calls ago).
+    const uint64_t so = c->stage_off[c->seq & 1];
+    if (in_bytes) CK(cudaMemcpyAsync(c->arena + so, in, in_bytes, cudaMemcpyDeviceToDevice, st));
+    in_off = so;
+  }
+  LaunchParams p{};
+  fill_geometry(p, n_elems, chunk_bytes, max_in_flight, c->n);
+  for (int i = 0; i < c->n; ++i) p.base[i] = (i == c->self) ? c->arena : c->peer[c->ring_slots[i]];
+  p.ctl[c->self] = c->ctl_d;
+  p.out[c->self] = out;
+  p.in_off[c->self] = in_off;
+  p.res_off[c->self] = c->res_off;
+  p.tag = tag;
+  p.nelems = n_elems;
+  p.hard_timeout_ns = c->hard_timeout_ns;
+  p.scale = scale;
+  p.flags = flags;
+  p.contrib = c->contrib;
+  p.dtype = (uint32_t)in_dtype;
+  p.self = c->self;
+  p.emulated = 0;
+  p.fault_member = -1;
+  p.fault_after_tiles = 0;
+  reset_ctl(c->ctl_h);
+  c->cur_tag = tag;
+  c->inflight = true;
+  const dim3 grid(real_ctas(), 1);
+  cudaError_t e = in_dtype == FTAR_DT_BF16 ? launch_dispatch<BF16In>(c->n, p, grid, st, false)
+                                            : launch_dispatch<F32In>(c->n, p, grid, st, false);
+  if (e != cudaSuccess) {
+    c->inflight = false;
+    return cuda_fail(e, "allreduce launch");
+  }
+  return FTAR_OK;
+}
+
+int ftar_local_allreduce_launch(ftar_ctx** ctxs, int n, const void* const* ins, int in_dtype,
+                                float* const* outs, uint64_t n_elems, uint64_t chunk_bytes,
+                                int max_in_flight, float scale, uint32_t flags, uint32_t contrib_mask,
+                                int fault_member, int fault_after_tiles, void* stream) {
+  int v = validate_common(in_dtype, n, chunk_bytes, max_in_flight);
+  if (v) return v;
+  if (!ctxs || !ins || !outs) return fail(FTAR_ST_INVARIANT, "null arrays");
+  const int dev = ctxs[0]->device;
+  for (int i = 0; i < n; ++i) {
+    ftar_ctx* c = ctxs[i];
+    if (!c || c->device != dev) return fail(FTAR_ST_INVARIANT, "in-process ring members must share a device");
+    if (c->inflight && flag_tag(c->ctl_h->done) != c->cur_tag)
+      return fail(FTAR_ST_INVARIANT, "one all-reduce in flight per ring group");
+    if (n_elems * 4 > 2 * c->max_bucket_bytes)
+      return fail(FTAR_ST_INVARIANT, "bucket exceeds the ring group's arena capacity");
+    if (c->gen != ctxs[0]->gen || c->seq != ctxs[0]->seq)
+      return fail(FTAR_ST_PROTOCOL, "ring members disagree on (generation, call sequence)");
+  }
+  DeviceGuard g(dev);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  LaunchParams p{};
+  fill_geometry(p, n_elems, chunk_bytes, max_in_flight, n);
+  uint64_t tag = 0;
+  for (int i = 0; i < n; ++i) {
+    ftar_ctx* c = ctxs[i];
+    c->seq += 1;
+    tag = mk_tag(c->gen, c->seq);
+    p.base[i] = c->arena;
+    p.ctl[i] = c->ctl_d;
+    p.out[i] = outs[i];
+    p.in_off[i] = (uint64_t)(static_cast<const char*>(ins[i]) - c->arena);
+    p.res_off[i] = c->res_off;
+    reset_ctl(c->ctl_h);
+    c->ctl_h->epoch = c->gen;
+    c->cur_tag = tag;
+    c->inflight = true;
+  }
+  p.tag = tag;
+  p.nelems = n_elems;
+  p.hard_timeout_ns = ctxs[0]->hard_timeout_ns;
+  p.scale = scale;
+  p.flags = flags;
+  p.contrib = contrib_mask & ((1u << n) - 1u);
+  p.dtype = (uint32_t)in_dtype;
+  p.self = 0;
+  p.emulated = 1;
+  p.fault_member = fault_member;
+  p.fault_after_tiles = fault_after_tiles;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int per_sm = in_dtype == FTAR_DT_BF16 ? max_coop_blocks_per_sm<BF16In>(n) : max_coop_blocks_per_sm<F32In>(n);
+  int G = std::max(1, (sms * std::max(per_sm, 1)) / n);
+  const int want = g_local_ctas > 0 ? g_local_ctas : env_int("FTAR_LOCAL_CTAS", 32);
+  G = std::min(G, want);
+  const dim3 grid(G, n);
+  cudaError_t e = in_dtype == FTAR_DT_BF16 ? launch_dispatch<BF16In>(n, p, grid, st, true)
+                                            : launch_dispatch<F32In>(n, p, grid, st, true);
+  if (e != cudaSuccess) {
+    for (int i = 0; i < n; ++i) ctxs[i]->inflight = false;
+    return cuda_fail(e, "local allreduce cooperative launch");
+  }
+  return FTAR_OK;
+}
+
+int ftar_poll(ftar_ctx* c, int* status, uint64_t* progress) {
+  if (!c) return fail(FTAR_ST_INVARIANT, "null ctx");
+  const uint64_t d = c->ctl_h->done;
+  if (progress) *progress = c->ctl_h->progress;
+  if (status) *status = (c->inflight && flag_tag(d) == c->cur_tag) ? (int)(d & 0xff)
+                       : (c->inflight ? FTAR_ST_PENDING : FTAR_OK);
+  return FTAR_OK;
+}
+
+int ftar_abort(ftar_ctx* c) {
+  if (!c) return fail(FTAR_ST_INVARIANT, "null ctx");
+  c->ctl_h->abort_tag = c->cur_tag;
+  return FTAR_OK;
+}
+
+int ftar_wait(ftar_ctx* c, double progress_timeout_s, int* detail) {
+  if (!c) return fail(FTAR_ST_INVARIANT, "null ctx");
+  if (detail) *detail = -1;
+  if (!c->inflight) return FTAR_OK;
+  HostCtl* h = c->ctl_h;
+  const uint64_t tag = c->cur_tag;
+  uint64_t last_prog = ~0ull;
+  double last_change = now_s();
+  bool aborted = false;
+  double abort_t = 0;
+  for (uint64_t it = 0;; ++it) {
+    const uint64_t d = h->done;
+    if (flag_tag(d) == tag) {
+      c->inflight = false;
+      if (detail) *detail = (int)h->detail;
+      int st = (int)(d & 0xff);
+      return st;
+    }
+    const double t = now_s();
+    if (h->started == tag) {
+      const uint64_t pr = h->progress;
+      if (pr != last_prog) {
+        last_prog = pr;
+        last_change = t;
+      } else if (!aborted && t - last_change > progress_timeout_s) {
+        h->abort_tag = tag;  // per-chunk deadline expired: drain the kernel
+        aborted = true;
+        abort_t = t;
+      }
+    } else {
+      last_change = t;  // still queued behind earlier stream work
+    }
+    if (aborted && t - abort_t > 60.0) {
+      return fail(FTAR_ST_TIMEOUT, "kernel did not drain after abort");
+    }
+    if (it < 2000) {
+#if defined(__x86_64__)
+      __builtin_ia32_pause();
+#endif
+    } else {
+      std::this_thread::sleep_for(std::chrono::microseconds(it < 20000 ? 5 : 100));
+    }
+  }
+}
+
+int ftar_wait_local(ftar_ctx** ctxs, int n, double progress_timeout_s, int* statuses, int* details) {
+  // One watcher for all members of an in-process ring: every member's
+  // progress word is tracked; a member whose progress stalls is aborted.
+  if (!ctxs || n < 1) return fail(FTAR_ST_INVARIANT, "bad wait_local args");
+  uint64_t last_prog[kMaxMembers];
+  double last_change[kMaxMembers];
+  bool aborted[kMaxMembers] = {};
+  bool fin[kMaxMembers] = {};
+  double t0 = now_s();
+  for (int i = 0; i < n; ++i) {
+    last_prog[i] = ~0ull;
+    last_change[i] = t0;
+    statuses[i] = FTAR_OK;
+    if (details) details[i] = -1;
+    fin[i] = !ctxs[i]->inflight;
+  }
+  double abort_t = 0;
+  for (uint64_t it = 0;; ++it) {
+    int left = 0;
+    const double t = now_s();
+    for (int i = 0; i < n; ++i) {
+      if (fin[i]) continue;
+      ftar_ctx* c = ctxs[i];
+      HostCtl* h = c->ctl_h;
+      const uint64_t d = h->done;
+      if (flag_tag(d) == c->cur_tag) {
+        fin[i] = true;
+        c->inflight = false;
+        statuses[i] = (int)(d & 0xff);
+        if (details) details[i] = (int)h->detail;
+        continue;
+      }
+      ++left;
+      if (h->started == c->cur_tag) {
+        const uint64_t pr = h->progress;
+        if (pr != last_prog[i]) {
+          last_prog[i] = pr;
+          last_change[i] = t;
+        } else if (!aborted[i] && t - last_change[i] > progress_timeout_s) {
+          h->abort_tag = c->cur_tag;
+          aborted[i] = true;
+          if (abort_t == 0) abort_t = t;
+        }
+      } else {
+        last_change[i] = t;
+      }
+    }
+    if (!left) return FTAR_OK;
+    if (abort_t > 0 && t - abort_t > 60.0) return fail(FTAR_ST_TIMEOUT, "kernel did not drain after abort");
+    if (it < 2000) {
+#if defined(__x86_64__)
+      __builtin_ia32_pause();
+#endif
+    } else {
+      std::this_thread::sleep_for(std::chrono::microseconds(it < 20000 ? 5 : 100));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ operators
+int ftar_accumulate(float* dst, const void* src, int src_dtype, uint64_t n, void* stream) {
+  if (!n) return FTAR_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int blocks = (int)std::min<uint64_t>((n + 255) / 256, 148ull * 8);
+  if (src_dtype == FTAR_DT_BF16)
+    accumulate_kernel<BF16In><<<blocks, 256, 0, st>>>(dst, static_cast<const __nv_bfloat16*>(src), n);
+  else if (src_dtype == FTAR_DT_F32)
+    accumulate_kernel<F32In><<<blocks, 256, 0, st>>>(dst, static_cast<const float*>(src), n);
+  else
+    return fail(FTAR_ST_INVARIANT, "bad dtype");
+  CK(cudaGetLastError());
+  return FTAR_OK;
+}
+
+int ftar_copy_into(float* dst, const void* src, int src_dtype, uint64_t n, void* stream) {
+  if (!n) return FTAR_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int blocks = (int)std::min<uint64_t>((n + 255) / 256, 148ull * 8);
+  if (src_dtype == FTAR_DT_BF16)
+    copy_into_kernel<BF16In><<<blocks, 256, 0, st>>>(dst, static_cast<const __nv_bfloat16*>(src), n);
+  else if (src_dtype == FTAR_DT_F32)
+    copy_into_kernel<F32In><<<blocks, 256, 0, st>>>(dst, static_cast<const float*>(src), n);
+  else
+    return fail(FTAR_ST_INVARIANT, "bad dtype");
+  CK(cudaGetLastError());
+  return FTAR_OK;
+}
+
+// ------------------------------------------------------------------ catch-up
+int ftar_snap_create(int device, uint64_t capacity_bytes, int exportable, ftar_snap** out) {
+  (void)exportable;
+  if (!out) return fail(FTAR_ST_INVARIANT, "null out");
+  DeviceGuard g(device);
+  ftar_snap* s = new ftar_snap();
+  s->device = device;
+  s->cap = align_up(std::max<uint64_t>(capacity_bytes, 16), 256);
+  cudaError_t e = cudaMalloc(&s->arena, kSnapHdrBytes + s->cap);
+  if (e != cudaSuccess) {
+    delete s;
+    return cuda_fail(e, "cudaMalloc(snapshot)");
+  }
+  snap_init_kernel<<<1, 1>>>(reinterpret_cast<SnapHdr*>(s->arena));
+  e = cudaHostAlloc(&s->ctl_h, sizeof(HostCtl), cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc(snap ctl)");
+  std::memset((void*)s->ctl_h, 0, sizeof(HostCtl));
+  reset_ctl(s->ctl_h);
+  cudaHostGetDevicePointer(reinterpret_cast<void**>(&s->ctl_d), (void*)s->ctl_h, 0);
+  CK(cudaDeviceSynchronize());
+  *out = s;
+  return FTAR_OK;
+}
+
+int ftar_snap_destroy(ftar_snap* s) {
+  if (!s) return FTAR_OK;
+  DeviceGuard g(s->device);
+  cudaDeviceSynchronize();
+  for (int i = 0; i < kMaxSlots; ++i)
+    if (s->peer[i]) cudaIpcCloseMemHandle(s->peer[i]);
+  cudaFree(s->arena);
+  cudaFreeHost((void*)s->ctl_h);
+  delete s;
+  return FTAR_OK;
+}
+
+int ftar_snap_export(ftar_snap* s, void* buf, size_t buflen, size_t* written) {
+  if (!s || !buf || buflen < sizeof(cudaIpcMemHandle_t)) return fail(FTAR_ST_INVARIANT, "bad export args");
+  DeviceGuard g(s->device);
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, s->arena));
+  std::memcpy(buf, &h, sizeof(h));
+  if (written) *written = sizeof(h);
+  return FTAR_OK;
+}
+
+int ftar_snap_capture(ftar_snap* s, uint64_t step, const void* params, uint64_t pbytes,
+                      const void* momentum, uint64_t mbytes, void* stream) {
+  if (!s) return fail(FTAR_ST_INVARIANT, "null snapshot");
+  if (pbytes + mbytes > s->cap) return fail(FTAR_ST_INVARIANT, "snapshot exceeds capacity");
+  DeviceGuard g(s->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SnapHdr* h = reinterpret_cast<SnapHdr*>(s->arena);
+  snap_mark_kernel<<<1, 1, 0, st>>>(h, (int64_t)step, pbytes, mbytes, 1);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
+  const uint64_t total = pbytes + mbytes;
+  const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)sms * 2, (total + 65535) / 65536));
+  if (total)
+    snap_copy_kernel<<<blocks, kThreads, 0, st>>>(s->arena + kSnapHdrBytes, static_cast<const char*>(params),
+                                                  pbytes, static_cast<const char*>(momentum), mbytes);
+  snap_mark_kernel<<<1, 1, 0, st>>>(h, (int64_t)step, pbytes, mbytes, 0);
+  CK(cudaGetLastError());
+  return FTAR_OK;
+}
+
+int ftar_snap_info(ftar_snap* s, int64_t* step, uint64_t* pbytes, uint64_t* mbytes) {
+  if (!s) return fail(FTAR_ST_INVARIANT, "null snapshot");
+  DeviceGuard g(s->device);
+  SnapHdr h;
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(&h, s->arena, sizeof(h), cudaMemcpyDeviceToHost));
+  if (step) *step = (h.seq & 1u) ? -1 : h.step;
+  if (pbytes) *pbytes = h.pbytes;
+  if (mbytes) *mbytes = h.mbytes;
+  return FTAR_OK;
+}
+
+int ftar_snap_import(ftar_snap* s, int slot, const void* handle, size_t len, uint64_t capacity_bytes) {
+  (void)capacity_bytes;
+  if (!s || slot < 0 || slot >= kMaxSlots || !handle || len < sizeof(cudaIpcMemHandle_t))
+    return fail(FTAR_ST_INVARIANT, "bad import args");
+  DeviceGuard g(s->device);
+  if (s->peer[slot]) return FTAR_OK;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* p = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    g_err = std::string("cudaIpcOpenMemHandle(snapshot): ") + cudaGetErrorString(e);
+    return FTAR_ST_PEER_DOWN;
+  }
+  s->peer[slot] = static_cast<char*>(p);
+  return FTAR_OK;
+}
+
+int ftar_snap_pull_launch(ftar_snap* local, int slot, const ftar_snap* src_local, uint64_t want_step,
+                          void* dst_params, uint64_t pbytes, void* dst_momentum, uint64_t mbytes,
+                          int ctas, void* stream) {
+  if (!local) return fail(FTAR_ST_INVARIANT, "null snapshot");
+  if (local->inflight && flag_tag(local->ctl_h->done) != local->cur_tag)
+    return fail(FTAR_ST_INVARIANT, "one pull in flight per snapshot context");
+  const char* src = nullptr;
+  if (slot >= 0) {
+    if (slot >= kMaxSlots || !local->peer[slot]) return fail(FTAR_ST_INVARIANT, "donor not mapped");
+    src = local->peer[slot];
+  } else {
+    if (!src_local) return fail(FTAR_ST_INVARIANT, "no donor");
+    src = src_local->arena;
+  }
+  DeviceGuard g(local->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  local->seq += 1;
+  const uint64_t tag = mk_tag(0, local->seq);
+  reset_ctl(local->ctl_h);
+  local->cur_tag = tag;
+  local->inflight = true;
+  const int G = std::max(1, ctas);
+  snap_pull_kernel<<<G, kThreads, 0, st>>>(src, reinterpret_cast<SnapHdr*>(local->arena), local->ctl_d, tag,
+                                           (int64_t)want_step, static_cast<char*>(dst_params), pbytes,
+                                           static_cast<char*>(dst_momentum), mbytes);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    local->inflight = false;
+    return cuda_fail(e, "snapshot pull launch");
+  }
+  return FTAR_OK;
+}
+
+int ftar_snap_poll(ftar_snap* s, int* status, uint64_t* progress, int64_t* available) {
+  if (!s) return fail(FTAR_ST_INVARIANT, "null snapshot");
+  const uint64_t d = s->ctl_h->done;
+  if (progress) *progress = s->ctl_h->progress;
+  if (available) *available = s->ctl_h->available;
+  if (status) *status = (s->inflight && flag_tag(d) == s->cur_tag) ? (int)(d & 0xff)
+                       : (s->inflight ? FTAR_ST_PENDING : FTAR_OK);
+  return FTAR_OK;
+}
+
+int ftar_snap_abort(ftar_snap* s) {
+  if (!s) return fail(FTAR_ST_INVARIANT, "null snapshot");
+  s->ctl_h->abort_tag = s->cur_tag;
+  return FTAR_OK;
+}
+
+int ftar_snap_wait(ftar_snap* s, double progress_timeout_s, int64_t* available) {
+  if (!s) return fail(FTAR_ST_INVARIANT, "null snapshot");
+  if (!s->inflight) return FTAR_OK;
+  HostCtl* h = s->ctl_h;
+  const uint64_t tag = s->cur_tag;
+  uint64_t last = ~0ull;
+  double last_change = now_s();
+  bool aborted = false;
+  double abort_t = 0;
+  for (uint64_t it = 0;; ++it) {
+    const uint64_t d = h->done;
+    if (flag_tag(d) == tag) {
+      s->inflight = false;
+      if (available) *available = h->available;
+      return (int)(d & 0xff);
+    }
+    const double t = now_s();
+    if (h->started == tag) {
+      const uint64_t pr = h->progress;
+      if (pr != last) {
+        last = pr;
+        last_change = t;
+      } else if (!aborted && t - last_change > progress_timeout_s) {
+        h->abort_tag = tag;
+        aborted = true;
+        abort_t = t;
+      }
+    } else {
+      last_change = t;
+    }
+    if (aborted && t - abort_t > 60.0) return fail(FTAR_ST_TIMEOUT, "pull did not drain after abort");
+    if (it < 2000) {
+#if defined(__x86_64__)
+      __builtin_ia32_pause();
+#endif
+    } else {
+      std::this_thread::sleep_for(std::chrono::microseconds(it < 20000 ? 5 : 100));
+    }
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,168 @@
+// ftar_device.cuh — device-side data layout and memory-model helpers of the
+// B200 FTAR data plane.  Everything a remote GPU may read lives in a member's
+// ARENA (one cudaMalloc, exported with CUDA IPC); everything the host polls or
+// writes lives in the pinned, device-mapped control block (HostCtl).
+//
+// Flag words are 64-bit: [generation:24][call seq:32][bits:8].  A flag only
+// satisfies a wait when its (generation, seq) equals the waiter's, so a
+// straggler from an abandoned attempt (older generation) can never complete a
+// newer wait — the GPU analogue of the generation fencing at
+// ftar.py:281-282 / 390-393.  All writes a peer can observe are LOCAL to the
+// writer (peers pull), so a zombie kernel of a dead attempt cannot corrupt
+// anybody else's memory.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace ftar {
+
+constexpr int kMaxMembers = 8;
+constexpr int kThreads = 512;          // one CTA per SM (launch_bounds(512,1))
+constexpr uint64_t kHdrBytes = 64 * 1024;
+constexpr uint32_t kBitNonFinite = 1u;
+
+// status codes (mirror include/ftar_b200.h)
+enum : uint32_t {
+  ST_OK = 0, ST_TIMEOUT = 1, ST_PEER_RESET = 2, ST_PEER_DOWN = 3, ST_PROTOCOL = 4,
+  ST_NUMERICAL = 5, ST_INVARIANT = 6, ST_ABORTED = 7, ST_INJECTED = 8,
+  ST_UNAVAILABLE = 9, ST_CUDA = 10
+};
+
+__host__ __device__ inline uint64_t mk_tag(uint64_t gen, uint64_t seq) {
+  return ((gen & 0xffffffull) << 32) | (seq & 0xffffffffull);
+}
+__host__ __device__ inline uint64_t mk_flag(uint64_t tag, uint32_t bits) {
+  return (tag << 8) | (bits & 0xffu);
+}
+__host__ __device__ inline uint64_t flag_tag(uint64_t f) { return f >> 8; }
+__host__ __device__ inline uint64_t tag_gen(uint64_t t) { return t >> 32; }
+
+// What a member announces when it enters a call: where its input sits in its
+// arena and what it believes the call is.  Peers validate it (the analogue of
+// the (partition, ring_step, chunk, len) check at ftar.py:394-397).
+struct alignas(128) EntryRec {
+  uint64_t flag;
+  uint64_t in_off;     // input address - arena base (mod 2^64)
+  uint64_t res_off;    // result region offset
+  uint64_t nelems;
+  uint64_t geom;       // partition cap (elements) the member folds with
+  uint32_t dtype;
+  uint32_t n;
+};
+
+struct alignas(128) ArenaHdr {
+  EntryRec entry;
+  alignas(128) uint64_t rs_done;    // flag: my slice is reduced (+kBitNonFinite)
+  alignas(128) uint64_t poison;     // flag: I aborted this call (bits = reason)
+  alignas(128) uint32_t rs_arrive;  // CTA arrival counters (local atomics)
+  uint32_t done_arrive;
+  uint32_t nonfinite;
+  uint32_t err;
+  int32_t err_peer;
+  uint32_t pad0;
+  uint64_t tiles_done;
+};
+static_assert(sizeof(ArenaHdr) <= kHdrBytes, "header too large");
+
+// Pinned host memory mapped into the device: the control plane's words.
+struct alignas(64) HostCtl {
+  volatile uint64_t epoch;         // host: current generation (quorum.py Decision.generation)
+  volatile uint32_t live_mask;     // host: ring members (bit = ring index)
+  volatile uint32_t contrib_mask;  // host: members contributing data (healthy)
+  volatile uint64_t abort_tag;     // host -> device: abort the call with this tag
+  volatile uint64_t started;       // device -> host: tag of the call that began
+  volatile uint64_t progress;      // device -> host: work tiles completed
+  volatile uint64_t done;          // device -> host: mk_flag(tag, status)
+  volatile int64_t detail;         // device -> host: ring index blamed (-1 none)
+  volatile int64_t available;      // device -> host: snapshot step available
+};
+
+// Snapshot arena header (retention-1 seqlock, checkpoint.py:56-80).
+struct alignas(128) SnapHdr {
+  uint64_t seq;        // odd while a capture is writing
+  int64_t step;        // -1 = nothing captured yet
+  uint64_t pbytes, mbytes;
+  alignas(128) uint64_t seq_min, seq_max;  // pull-side consistency (local)
+  uint32_t done_arrive, err;
+  uint64_t bytes_done;
+};
+constexpr uint64_t kSnapHdrBytes = 4096;
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_sys32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// 128-bit weak loads/stores that do not allocate in L1: peer data is streamed
+// once, and local L1 would otherwise cache NVLink lines (L2 is bypassed for
+// peer apertures).
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(void* p, uint4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+__device__ __forceinline__ bool nonfinite_bits(float x) {
+  return (__float_as_uint(x) & 0x7f800000u) == 0x7f800000u;
+}
+
+// Element types of the bucket: the fp32 upcast of bf16 is exact.
+struct F32In {
+  using T = float;
+  static constexpr int kBytes = 4;
+  __device__ __forceinline__ static float scalar(const float* p, uint64_t e) { return p[e]; }
+  // 8 elements = two 16-byte loads
+  __device__ __forceinline__ static void load8(const float* p, uint64_t e, float (&v)[8]) {
+    uint4 a = ld_stream(p + e), b = ld_stream(p + e + 4);
+    v[0] = __uint_as_float(a.x); v[1] = __uint_as_float(a.y);
+    v[2] = __uint_as_float(a.z); v[3] = __uint_as_float(a.w);
+    v[4] = __uint_as_float(b.x); v[5] = __uint_as_float(b.y);
+    v[6] = __uint_as_float(b.z); v[7] = __uint_as_float(b.w);
+  }
+};
+struct BF16In {
+  using T = __nv_bfloat16;
+  static constexpr int kBytes = 2;
+  __device__ __forceinline__ static float up(uint32_t h) { return __uint_as_float(h << 16); }
+  __device__ __forceinline__ static float scalar(const __nv_bfloat16* p, uint64_t e) {
+    return up(reinterpret_cast<const uint16_t*>(p)[e]);
+  }
+  // 8 elements = one 16-byte load
+  __device__ __forceinline__ static void load8(const __nv_bfloat16* p, uint64_t e, float (&v)[8]) {
+    uint4 a = ld_stream(p + e);
+    v[0] = up(a.x & 0xffffu); v[1] = up(a.x >> 16);
+    v[2] = up(a.y & 0xffffu); v[3] = up(a.y >> 16);
+    v[4] = up(a.z & 0xffffu); v[5] = up(a.z >> 16);
+    v[6] = up(a.w & 0xffffu); v[7] = up(a.w >> 16);
+  }
+};
+
+}  // namespace ftar

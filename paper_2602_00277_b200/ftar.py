@@ -1,0 +1,566 @@
+"""Fault-tolerant all-reduce on B200 — drop-in for ``ftdp.ftar``.
+
+Same entry points and failure contract as the reference
+(pkg/src/ftdp/ftar.py): ``PipelineConfig``, ``build_partition_plan``,
+``segment_bounds``, ``iter_chunks``, ``classify_error``, ``InflightMeter``,
+``RingGroup(...).reconfig/close_links/links_ready`` and
+``ftar_all_reduce(group, buf, step, cfg)`` which sums ``buf`` across the ring
+in place and returns the same object.  Buffers are torch CUDA tensors; the data
+plane is libftar_b200.so (sm_100a): members pull each other's buckets over
+NVLink, reduce in the reference's fixed fold order (bit-identical to
+tests/test_ftar.py:20-40) and commit all-or-nothing.
+
+Extensions (keyword-only, reference callers never pass them):
+``out=`` a separate fp32 output, which enables bf16 input buckets with the
+bf16->fp32 cast fused into the reduction; ``scale=`` the normalisation factor
+f32(1/(h*R)) of replica.py:622-626 fused into the same pass.
+
+Failure semantics (ftar.py:5-16): a lost or slow member surfaces as
+Recoverable (TIMEOUT / PEER_RESET / PEER_DOWN) with ``buf`` untouched and the
+links closed; non-finite sums and protocol mismatches are Fatal, also with
+``buf`` untouched on every member.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import logging
+import os
+import threading
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+from .errors import (
+    INTERNAL_INVARIANT,
+    PEER_RESET,
+    Fatal,
+    FtdpError,
+    Recoverable,
+    from_status,
+)
+from .fabric import ArenaInfo, LocalFabric, StoreFabric
+
+log = logging.getLogger(__name__)
+
+ELEM = 4  # the reference's geometry is in float32 element units (ftar.py:46)
+MIB = 1024 * 1024
+
+
+# --------------------------------------------------------------- geometry
+
+
+@dataclass
+class PipelineConfig:
+    """ftar.py:49-65.  On NVLink the chunk/window pair no longer paces a TCP
+    link; it still defines the partition geometry, i.e. which member's copy
+    starts each element's fold (and therefore the result bits)."""
+
+    chunk_bytes: int = 8 * MIB
+    max_in_flight: int = 4
+    per_chunk_timeout_s: float = 5.0
+
+    def __post_init__(self):
+        if self.chunk_bytes < ELEM:
+            raise Fatal(INTERNAL_INVARIANT, "chunk_bytes must be >= 4")
+        if self.max_in_flight < 1:
+            raise Fatal(INTERNAL_INVARIANT, "max_in_flight must be >= 1")
+        if self.per_chunk_timeout_s <= 0:
+            raise Fatal(INTERNAL_INVARIANT, "per_chunk_timeout_s must be > 0")
+
+    @property
+    def chunk_elems(self) -> int:
+        return self.chunk_bytes // ELEM
+
+
+@dataclass
+class PartitionPlan:
+    """Partition table in float32 element units (ftar.py:68-77)."""
+
+    total_elems: int
+    n_members: int
+    partitions: list[tuple[int, int]]
+
+    def partition_bytes(self) -> list[tuple[int, int]]:
+        return [(o * ELEM, n * ELEM) for o, n in self.partitions]
+
+
+def _balanced(total: int, parts: int) -> list[tuple[int, int]]:
+    """`parts` contiguous (offset, length) pieces; the first total % parts
+    pieces are one longer."""
+    q, r = divmod(total, parts)
+    out, off = [], 0
+    for i in range(parts):
+        n = q + (i < r)
+        out.append((off, n))
+        off += n
+    return out
+
+
+def build_partition_plan(total_bytes: int, cfg: PipelineConfig, n_members: int) -> PartitionPlan:
+    """ftar.py:80-99: partitions of at most chunk_bytes*max_in_flight*n bytes."""
+    if total_bytes % ELEM:
+        raise Fatal(INTERNAL_INVARIANT, f"buffer not float32-aligned: {total_bytes}")
+    if n_members < 1:
+        raise Fatal(INTERNAL_INVARIANT, "n_members must be >= 1")
+    total = total_bytes // ELEM
+    if total == 0:
+        return PartitionPlan(0, n_members, [(0, 0)])
+    cap = max(1, cfg.chunk_bytes * cfg.max_in_flight * n_members // ELEM)
+    return PartitionPlan(total, n_members, _balanced(total, -(-total // cap)))
+
+
+def segment_bounds(part_elems: int, n: int) -> list[tuple[int, int]]:
+    """ftar.py:102-112: segment j of a partition is owned by ring index j."""
+    return _balanced(part_elems, n)
+
+
+def iter_chunks(seg_len: int, chunk_elems: int) -> list[tuple[int, int, int]]:
+    """ftar.py:115-125: (chunk_idx, offset, length) covering a segment."""
+    return [(i, off, min(chunk_elems, seg_len - off))
+            for i, off in enumerate(range(0, seg_len, chunk_elems))]
+
+
+def classify_error(err: BaseException) -> str:
+    """ftar.py:128-138."""
+    if isinstance(err, FtdpError):
+        return err.severity
+    if isinstance(err, (TimeoutError, ConnectionError, BrokenPipeError, OSError)):
+        return "recoverable"
+    return "fatal"
+
+
+class InflightMeter:
+    """ftar.py:141-159.  On NVLink there is no ack window; the meter records
+    the data plane's per-link in-flight bound for each call (CTAs x threads x
+    outstanding 16-byte loads per peer), which the kernel can never exceed."""
+
+    def __init__(self):
+        self.unacked_bytes = 0
+        self.max_unacked_bytes = 0
+        self.max_unacked_chunks = 0
+        self._chunks = 0
+
+    def sent(self, nbytes: int, chunks: int = 1) -> None:
+        self.unacked_bytes += nbytes
+        self._chunks += chunks
+        self.max_unacked_bytes = max(self.max_unacked_bytes, self.unacked_bytes)
+        self.max_unacked_chunks = max(self.max_unacked_chunks, self._chunks)
+
+    def acked(self, nbytes: int, chunks: int = 1) -> None:
+        self.unacked_bytes -= nbytes
+        self._chunks -= chunks
+
+
+@dataclass(frozen=True)
+class PeerAddress:
+    """transport.PeerAddress analogue: who a member is.  host/port are kept
+    for signature compatibility; NVLink members are found through the fabric."""
+
+    replica_id: int
+    rank_id: int = 0
+    host: str = ""
+    port: int = 0
+
+
+# --------------------------------------------------------------- tensors
+
+
+class _CudaView:
+    """__cuda_array_interface__ over a raw device range (arena pool)."""
+
+    def __init__(self, ptr: int, shape: tuple, typestr: str):
+        self.__cuda_array_interface__ = {
+            "shape": shape, "typestr": typestr, "data": (ptr, False), "version": 3, "strides": None,
+        }
+
+
+_TYPESTR = {torch.float32: "<f4", torch.bfloat16: "<i2"}
+
+
+def _stream_ptr(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return _lib.DT_F32
+    if t.dtype == torch.bfloat16:
+        return _lib.DT_BF16
+    raise Fatal(INTERNAL_INVARIANT, "all-reduce buffer must be contiguous float32 (or bfloat16 with out=)")
+
+
+# --------------------------------------------------------------- ring group
+
+
+class RingGroup:
+    """This rank's ring across replicas (ftar.py:162-235).
+
+    Members are the quorum decision's replicas in ascending id order
+    (ftar.py:202); ``generation`` strictly increases.  Instead of two TCP
+    links, the group owns a device arena (result region, staging, registered
+    pool, flag words) that the other members map, plus a pinned control block
+    (live mask, contributor mask, epoch word, abort/progress/done words).
+
+    ``router`` is the rendezvous fabric: a ``StoreFabric`` for one process per
+    GPU, a ``LocalFabric`` (default) for members living in one process.
+    """
+
+    def __init__(self, self_replica: int, rank: int, router=None, plan=None, incarnation: int = 0,
+                 *, device=None, max_bucket_bytes: int = 64 * MIB, pool_bytes: int = 0):
+        if not torch.cuda.is_available():
+            raise Fatal(INTERNAL_INVARIANT, "the B200 FTAR data plane needs a CUDA device")
+        self.self_replica = self_replica
+        self.rank = rank
+        self.router = router if router is not None else LocalFabric.default()
+        self.plan = plan
+        self.incarnation = incarnation
+        self.generation = 0
+        self.members: list[int] = [self_replica]
+        self.contributors: frozenset[int] = frozenset({self_replica})
+        self.meter = InflightMeter()
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device)
+        self.device_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        self._local = isinstance(self.router, LocalFabric)
+        ctx = C.c_void_p()
+        _lib.check(_lib.lib.ftar_ctx_create(self.device_index, max_bucket_bytes, pool_bytes,
+                                            0 if self._local else 1, C.byref(ctx)), "ftar_ctx_create")
+        self._ctx = ctx
+        self.max_bucket_bytes = max_bucket_bytes
+        self._links_up = False
+        self._seq = 0
+        self._slots: dict[tuple[int, int], int] = {}
+        self._pool_next = 0
+        ptr, nbytes = C.c_uint64(), C.c_uint64()
+        _lib.lib.ftar_ctx_pool(ctx, C.byref(ptr), C.byref(nbytes))
+        self._pool_ptr, self._pool_bytes = ptr.value, nbytes.value
+        self._lock = threading.Lock()
+        if self._local:
+            self.router.register(self)
+        else:
+            buf = (C.c_char * 64)()
+            written = C.c_size_t()
+            _lib.check(_lib.lib.ftar_ctx_export(ctx, buf, 64, C.byref(written)), "ftar_ctx_export")
+            self.router.publish(ArenaInfo(self_replica, rank, incarnation, self.device_index,
+                                          bytes(buf)[:written.value], 0, pid=os.getpid()))
+        self._set_membership()
+
+    # -- properties (ftar.py:180-186) ---------------------------------------
+    @property
+    def n(self) -> int:
+        return len(self.members)
+
+    @property
+    def index(self) -> int:
+        return self.members.index(self.self_replica)
+
+    @property
+    def ctx(self):
+        return self._ctx
+
+    # -- registered buckets ---------------------------------------------------
+    def alloc_bucket(self, numel: int, dtype: torch.dtype = torch.float32) -> torch.Tensor:
+        """A tensor inside the group's registered pool: reduced zero-copy
+        (peers read it in place instead of a staged copy)."""
+        esz = torch.empty((), dtype=dtype).element_size()
+        nbytes = numel * esz
+        off = (self._pool_next + 255) // 256 * 256
+        if off + nbytes > self._pool_bytes:
+            raise Fatal(INTERNAL_INVARIANT, f"bucket pool exhausted ({self._pool_bytes} bytes)")
+        self._pool_next = off + nbytes
+        view = _CudaView(self._pool_ptr + off, (numel,), _TYPESTR.get(dtype, "<f4"))
+        with torch.cuda.device(self.device):
+            t = torch.as_tensor(view, device=self.device)
+        if dtype == torch.bfloat16:
+            t = t.view(torch.bfloat16)
+        t._ftar_owner = self  # keep the arena alive while the view is
+        return t
+
+    def reset_pool(self) -> None:
+        self._pool_next = 0
+
+    # -- membership (ftar.py:188-235) ---------------------------------------
+    def _slot(self, replica_id: int, incarnation: int) -> int:
+        key = (replica_id, incarnation)
+        if key not in self._slots:
+            self._slots[key] = len(self._slots) % 256
+        return self._slots[key]
+
+    def _set_membership(self, infos: dict | None = None) -> None:
+        n = self.n
+        slots = (C.c_int * n)()
+        for i, m in enumerate(self.members):
+            if m == self.self_replica or self._local:
+                slots[i] = -1
+            else:
+                slots[i] = self._slot(m, infos[m].incarnation)
+        contrib = 0
+        for i, m in enumerate(self.members):
+            if m in self.contributors:
+                contrib |= 1 << i
+        if self._local:
+            # in-process members are addressed directly by the launch
+            slots_arg = None
+            rc = _lib.lib.ftar_set_membership(self._ctx, slots_arg, 1, 0, contrib & 1 if n == 1 else 1,
+                                              self.generation)
+            self._contrib_mask = contrib
+        else:
+            rc = _lib.lib.ftar_set_membership(self._ctx, slots, n, self.index, contrib, self.generation)
+            self._contrib_mask = contrib
+        _lib.check(rc, "ftar_set_membership")
+
+    def reconfig(self, addrs: dict, generation: int, deadline_s: float = 5.0,
+                 contributors=None) -> None:
+        """Tear down the old ring and establish the new one (ftar.py:188-224).
+
+        ``addrs`` maps member replica ids to addresses and must include self.
+        ``contributors`` (default: all members) are the replicas whose data
+        enters the sum; the rest (the quorum's *behind* set, replica.py:574-577)
+        fold +0.0 and issue no loads.  Unreachable members surface as
+        Recoverable(PEER_DOWN)."""
+        if generation <= self.generation:
+            raise Fatal(INTERNAL_INVARIANT, f"generation must increase: {generation} <= {self.generation}")
+        if self.self_replica not in addrs:
+            raise Fatal(INTERNAL_INVARIANT, "reconfig membership must include self")
+        if generation > 0xFFFFFF:
+            raise Fatal(INTERNAL_INVARIANT, "generation exceeds the 24-bit epoch word")
+        self.close_links()
+        self.members = sorted(addrs)
+        self.generation = generation
+        self._seq = 0
+        self.contributors = frozenset(self.members if contributors is None else contributors)
+        if not self.contributors <= set(self.members):
+            raise Fatal(INTERNAL_INVARIANT, "contributors must be ring members")
+        if len(self.members) > 8:
+            raise Fatal(INTERNAL_INVARIANT, "at most 8 replicas per NVLink ring")
+        infos = None
+        if self.n > 1:
+            infos = self.router.join(self.rank, self.self_replica, self.members, generation, deadline_s)
+            if not self._local:
+                for m, info in infos.items():
+                    rc = _lib.lib.ftar_ctx_import(self._ctx, self._slot(m, info.incarnation), info.handle,
+                                                  len(info.handle), info.arena_bytes)
+                    if rc:
+                        self.close_links()
+                        _lib.check(rc, f"map arena of replica {m}")
+        self._set_membership(infos)
+        self._links_up = True
+
+    def close_links(self) -> None:
+        """ftar.py:226-230: the ring is unusable until the next reconfig;
+        members waiting on this one are released with PEER_RESET."""
+        if self._links_up and self.n > 1:
+            self.router.mark_down(self.rank, self.self_replica, self.generation)
+        self._links_up = False
+
+    def links_ready(self) -> bool:
+        return self.n == 1 or self._links_up
+
+    def close(self) -> None:
+        self.close_links()
+        if self._ctx:
+            if self._local:
+                self.router.unregister(self)
+            _lib.lib.ftar_ctx_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter teardown
+            pass
+
+    def inflight_bound(self, in_dtype_bytes: int) -> tuple[int, int]:
+        """(bytes, CTAs) a single peer link can have outstanding per call."""
+        slice_e, ctas, threads = C.c_uint64(), C.c_int(), C.c_int()
+        _lib.lib.ftar_geometry(1, max(1, self.n), C.byref(slice_e), C.byref(ctas), C.byref(threads))
+        n = max(1, self.n)
+        unroll = 4 if n <= 2 else (2 if n <= 4 else 1)
+        per_thread = unroll * 8 * in_dtype_bytes
+        return ctas.value * threads.value * per_thread, ctas.value
+
+
+# --------------------------------------------------------------- all-reduce
+
+
+def _check_buffers(buf, out):
+    if not isinstance(buf, torch.Tensor) or not buf.is_cuda:
+        raise Fatal(INTERNAL_INVARIANT, "all-reduce buffer must be a CUDA tensor")
+    if not buf.is_contiguous():
+        raise Fatal(INTERNAL_INVARIANT, "all-reduce buffer must be contiguous float32")
+    code = _dtype_code(buf)
+    if out is None:
+        if code != _lib.DT_F32:
+            raise Fatal(INTERNAL_INVARIANT, "all-reduce buffer must be contiguous float32 (pass out= for bf16)")
+        out = buf
+    else:
+        if not isinstance(out, torch.Tensor) or not out.is_cuda or out.dtype != torch.float32 \
+                or not out.is_contiguous() or out.numel() != buf.numel() or out.device != buf.device:
+            raise Fatal(INTERNAL_INVARIANT, "out must be a contiguous float32 CUDA tensor shaped like buf")
+    return code, out
+
+
+def ftar_all_reduce(group: RingGroup, buf: torch.Tensor, step: int, cfg: PipelineConfig | None = None,
+                    *, out: torch.Tensor | None = None, scale: float | None = None) -> torch.Tensor:
+    """Sum ``buf`` across the group (ftar.py:301-326).
+
+    In place for float32 (returns ``buf``); with ``out=`` the fp32 sum (of a
+    float32 or bfloat16 bucket) lands in ``out`` and ``out`` is returned.
+    ``scale`` multiplies the fp32 sum by f32(scale) in the same pass.  On a
+    Recoverable error the links are closed and nothing has been written."""
+    cfg = cfg or PipelineConfig()
+    code, dst = _check_buffers(buf, out)
+    if group.n > 1 and not group.links_ready():
+        raise Recoverable(PEER_RESET, "ring links not established")
+    flags = _lib.F_SCALE if scale is not None else 0
+    f_scale = float(torch.tensor(scale if scale is not None else 1.0, dtype=torch.float32))
+    nbytes_in = buf.element_size()
+    bound, ctas = group.inflight_bound(nbytes_in)
+    try:
+        if group._local:
+            _local_all_reduce(group, buf, dst, code, cfg, f_scale, flags)
+        else:
+            _remote_all_reduce(group, buf, dst, code, cfg, f_scale, flags)
+    except FtdpError:
+        group.close_links()
+        raise
+    group.meter.sent(bound, ctas)
+    group.meter.acked(bound, ctas)
+    return dst
+
+
+def _remote_all_reduce(group, buf, dst, code, cfg, f_scale, flags):
+    with group._lock:
+        group._seq += 1
+        rc = _lib.lib.ftar_allreduce_launch(group.ctx, buf.data_ptr(), code, dst.data_ptr(), buf.numel(),
+                                            cfg.chunk_bytes, cfg.max_in_flight, f_scale, flags,
+                                            _stream_ptr(group.device))
+        _lib.check(rc, "ftar_allreduce_launch")
+        detail = C.c_int(-1)
+        st = _lib.lib.ftar_wait(group.ctx, cfg.per_chunk_timeout_s, C.byref(detail))
+    if st:
+        blame = group.members[detail.value] if 0 <= detail.value < group.n else None
+        msg = _lib.last_error() if st == 10 else ""
+        raise from_status(st, (msg + f" (peer replica {blame})") if blame is not None else msg)
+
+
+def _local_all_reduce(group, buf, dst, code, cfg, f_scale, flags):
+    fabric: LocalFabric = group.router
+    group._seq += 1
+    key = (group.rank, group.generation, group._seq)
+    params = (buf.numel(), code, cfg.chunk_bytes, cfg.max_in_flight, flags, f_scale, str(buf.device))
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream(group.device))
+    deposit = {"buf": buf, "out": dst, "event": ev, "timeout": cfg.per_chunk_timeout_s}
+
+    def launch(call):
+        members = call.members
+        n = len(members)
+        groups = [fabric.group_of(group.rank, m) for m in members]
+        stream = torch.cuda.current_stream(group.device)
+        for i in range(n):
+            stream.wait_event(call.deposits[i]["event"])
+        fault_member, fault_after = -1, 0
+        with fabric.cond:
+            for i, m in enumerate(members):
+                if (group.rank, m) in fabric.faults:
+                    fault_member, fault_after = i, fabric.faults.pop((group.rank, m))
+        ctxs = (C.c_void_p * n)(*[g.ctx for g in groups])
+        ins = (C.c_void_p * n)(*[call.deposits[i]["buf"].data_ptr() for i in range(n)])
+        outs = (C.c_void_p * n)(*[call.deposits[i]["out"].data_ptr() for i in range(n)])
+        contrib = groups[0]._contrib_mask if n > 1 else 1
+        rc = _lib.lib.ftar_local_allreduce_launch(ctxs, n, ins, code, outs, buf.numel(), cfg.chunk_bytes,
+                                                  cfg.max_in_flight, f_scale, flags, contrib, fault_member,
+                                                  fault_after, stream.cuda_stream)
+        _lib.check(rc, "ftar_local_allreduce_launch")
+        sts = (C.c_int * n)()
+        dets = (C.c_int * n)()
+        timeout = min(call.deposits[i]["timeout"] for i in range(n))
+        _lib.check(_lib.lib.ftar_wait_local(ctxs, n, timeout, sts, dets), "ftar_wait_local")
+        return {i: (sts[i], dets[i]) for i in range(n)}
+
+    st, det = fabric.rendezvous(group, key, deposit, params, cfg.per_chunk_timeout_s, launch)
+    if st:
+        blame = group.members[det] if 0 <= det < group.n else None
+        raise from_status(st, f"peer replica {blame}" if blame is not None else "")
+
+
+class LocalRing:
+    """n single-rank members of one ring in this process, on one device —
+    the B200 counterpart of ``bench._LoopbackRing`` (bench.py:53-96).
+    ``all_reduce`` issues the members' calls without threads (one cooperative
+    launch), which is what the benchmark times."""
+
+    def __init__(self, n: int, device=None, max_bucket_bytes: int = 64 * MIB, rank: int = 0):
+        self.n = n
+        self.fabric = LocalFabric()
+        self.groups = [RingGroup(rid, rank, self.fabric, device=device, max_bucket_bytes=max_bucket_bytes)
+                       for rid in range(n)]
+        self.gen = 0
+        self.reconfig()
+
+    def reconfig(self, members=None, contributors=None):
+        members = sorted(members if members is not None else range(self.n))
+        self.gen += 1
+        addrs = {m: PeerAddress(m) for m in members}
+        errs = []
+        threads = [threading.Thread(target=self._rc, args=(self.groups[m], addrs, contributors, errs))
+                   for m in members]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        if errs:
+            raise errs[0]
+        return members
+
+    def _rc(self, g, addrs, contributors, errs):
+        try:
+            g.reconfig(addrs, self.gen, deadline_s=10.0, contributors=contributors)
+        except Exception as exc:  # noqa: BLE001
+            errs.append(exc)
+
+    def launch(self, bufs, cfg: PipelineConfig | None = None, outs=None, scale=None, members=None,
+               fault=None):
+        """Launch one all-reduce over `members` (default all) without waiting."""
+        cfg = cfg or PipelineConfig()
+        members = sorted(members if members is not None else range(self.n))
+        groups = [self.groups[m] for m in members]
+        n = len(groups)
+        code = _dtype_code(bufs[0])
+        outs = outs if outs is not None else bufs
+        flags = _lib.F_SCALE if scale is not None else 0
+        f_scale = float(torch.tensor(scale if scale is not None else 1.0, dtype=torch.float32))
+        for g in groups:
+            g._seq += 1
+        ctxs = (C.c_void_p * n)(*[g.ctx for g in groups])
+        ins = (C.c_void_p * n)(*[bufs[i].data_ptr() for i in range(n)])
+        ous = (C.c_void_p * n)(*[outs[i].data_ptr() for i in range(n)])
+        fm, fa = (-1, 0) if fault is None else fault
+        rc = _lib.lib.ftar_local_allreduce_launch(ctxs, n, ins, code, ous, bufs[0].numel(), cfg.chunk_bytes,
+                                                  cfg.max_in_flight, f_scale, flags, groups[0]._contrib_mask,
+                                                  fm, fa, _stream_ptr(groups[0].device))
+        _lib.check(rc, "ftar_local_allreduce_launch")
+        return ctxs
+
+    def wait(self, ctxs, cfg: PipelineConfig | None = None) -> list[int]:
+        cfg = cfg or PipelineConfig()
+        n = len(ctxs)
+        sts = (C.c_int * n)()
+        dets = (C.c_int * n)()
+        _lib.check(_lib.lib.ftar_wait_local(ctxs, n, cfg.per_chunk_timeout_s, sts, dets), "ftar_wait_local")
+        return list(sts)
+
+    def all_reduce(self, bufs, cfg: PipelineConfig | None = None, outs=None, scale=None, members=None):
+        sts = self.wait(self.launch(bufs, cfg, outs, scale, members), cfg)
+        for st in sts:
+            if st:
+                raise from_status(st)
+        return outs if outs is not None else bufs
+
+    def close(self):
+        for g in self.groups:
+            g.close()

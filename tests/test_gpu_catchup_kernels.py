@@ -1,0 +1,98 @@
+"""Catch-up snapshot/pull and the operator plugin on the GPU."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda", 0)
+
+
+def test_accumulate_and_copy_into_vs_torch_fp32():
+    from paper_2602_00277_b200 import kernels
+    assert kernels.BACKEND == "sm_100a" and set(kernels.backends()) == {"sm_100a"}
+    g = torch.Generator(device=DEV).manual_seed(0)
+    for n in (0, 1, 7, 4096, 1_000_003):
+        dst = torch.randn(n, device=DEV, generator=g)
+        src = torch.randn(n, device=DEV, generator=g)
+        want = dst + src
+        kernels.accumulate(dst, src)
+        assert torch.equal(dst, want)
+        srcb = src.to(torch.bfloat16)
+        want = dst + srcb.float()
+        kernels.accumulate(dst, srcb)
+        assert torch.equal(dst, want)
+        kernels.copy_into(dst, srcb)
+        assert torch.equal(dst, srcb.float())
+    with pytest.raises(ValueError):
+        kernels.accumulate(torch.zeros(4, device=DEV), torch.zeros(5, device=DEV))
+
+
+def test_snapshot_retention_and_pull_bit_exact():
+    from paper_2602_00277_b200 import checkpoint as ck
+    donor = ck.SnapshotStore(device=DEV)
+    rec = ck.SnapshotStore(device=DEV)
+    g = torch.Generator(device=DEV).manual_seed(1)
+    p = torch.randn(3_000_001, device=DEV, generator=g)
+    m = torch.randn(1_234_567, device=DEV, generator=g)
+    assert donor.step is None
+    donor.capture(7, p, m)
+    assert donor.step == 7 and donor.device_step() == 7
+    p_out = torch.empty_like(p)
+    m_out = torch.empty_like(m)
+    ck.fetch_shard(donor, 7, rank=0, local=rec, out=(p_out, m_out), ctas=8)
+    torch.cuda.synchronize()
+    assert torch.equal(p_out, p) and torch.equal(m_out, m)
+    # later writes to the live tensors do not leak into the snapshot
+    p.add_(1.0)
+    p2 = torch.empty_like(p)
+    ck.fetch_shard(donor, 7, rank=0, local=rec, out=(p2, torch.empty_like(m)))
+    assert torch.equal(p2, p_out)
+    # retention is one: a new capture replaces the old step
+    donor.capture(8, p, m)
+    with pytest.raises(ck.SnapshotUnavailable) as ei:
+        ck.fetch_shard(donor, 7, rank=0, local=rec, out=(p2, torch.empty_like(m)))
+    assert ei.value.available == 8
+    with pytest.raises(ck.SnapshotUnavailable):
+        donor.get(7)
+    assert donor.get(8) == (p.numel() * 4, m.numel() * 4)
+
+
+def test_pull_on_side_stream_overlaps_ftar():
+    """The pull runs on a low-priority side stream while an FTAR runs on the
+    default stream; both finish and both are correct."""
+    from paper_2602_00277_b200 import checkpoint as ck
+    from paper_2602_00277_b200 import ftar
+    from oracle import ftar_oracle as orc
+    from gen import member_inputs
+    donor = ck.SnapshotStore(device=DEV)
+    rec = ck.SnapshotStore(device=DEV)
+    p = torch.randn(64 << 20 >> 2, device=DEV)
+    m = torch.randn(64 << 20 >> 2, device=DEV)
+    donor.capture(3, p, m)
+    torch.cuda.synchronize()
+    ring = ftar.LocalRing(4, device=DEV, max_bucket_bytes=16 << 20)
+    try:
+        arrays = member_inputs(4, 1 << 20, seed=2)
+        bufs = [torch.from_numpy(a).to(DEV) for a in arrays]
+        po, mo = torch.empty_like(p), torch.empty_like(m)
+        pull = ck.start_fetch(rec, donor, 3, 0, po, mo, ctas=8)
+        ring.all_reduce(bufs)
+        pull.wait()
+        torch.cuda.synchronize()
+        assert torch.equal(po, p) and torch.equal(mo, m)
+        want = orc.oracle_reduce(arrays, 8 << 20, 4)
+        for b in bufs:
+            np.testing.assert_array_equal(b.cpu().numpy(), want)
+    finally:
+        ring.close()
+
+
+def test_pick_donor():
+    from paper_2602_00277_b200 import checkpoint as ck
+    from paper_2602_00277_b200 import errors
+    assert [ck.pick_donor([0, 1, 2], 3, r) for r in range(4)] == [0, 1, 2, 0]
+    assert ck.pick_donor([0, 1, 2], 3, rank=0, attempt=1) == 1
+    assert ck.pick_donor([0, 3], 3, rank=1) == 0
+    with pytest.raises(errors.Recoverable):
+        ck.pick_donor([3], 3, rank=0)

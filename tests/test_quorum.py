@@ -1,0 +1,116 @@
+"""Membership decisions: the reference's KATs (tests/test_quorum.py:18-127)
+and bit-exact replay of decision streams recorded from the reference engine
+(tests/golden/quorum_traces.json), including the 8-replica kill trace of its
+replica engine."""
+
+import json
+import os
+
+import pytest
+
+from paper_2602_00277_b200.quorum import Decision, QuorumEngine, Report
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def reports(**kw):
+    return {int(k[1:]): Report(next_step=v, incarnation=1) for k, v in kw.items()}
+
+
+def test_one_replica_behind():
+    d = QuorumEngine().decide(reports(r0=100, r1=100, r2=100, r3=96))
+    assert d.target_step == 100 and d.healthy == (0, 1, 2) and d.behind == {3: 96}
+    assert d.members == (0, 1, 2, 3) and d.generation == 1 and d.epoch == 1
+    assert d.live_mask() == 0b1111 and d.contrib_mask() == 0b0111
+
+
+def test_generation_rules():
+    e = QuorumEngine()
+    assert [e.decide(reports(r0=s, r1=s)).generation for s in (1, 2, 3)] == [1, 1, 1]
+    e = QuorumEngine()
+    e.decide(reports(r0=5, r1=5))
+    assert [e.decide(reports(r0=5, r1=5)).generation for _ in range(2)] == [2, 3]
+    e = QuorumEngine()
+    e.decide(reports(r0=4, r1=4, r2=4))
+    d = e.decide(reports(r0=5, r1=5))
+    assert d.generation == 2 and d.healthy == (0, 1)
+    d = e.decide(reports(r0=6, r1=6, r2=4))
+    assert d.generation == 3 and d.behind == {2: 4}
+    d = e.decide(reports(r0=7, r1=7, r2=7))
+    assert d.generation == 4
+    assert e.decide(reports(r0=8, r1=8, r2=8)).generation == 4
+
+
+def test_incarnation_fencing_and_gates():
+    e = QuorumEngine()
+    assert e.register(2, 1)
+    assert e.decide({0: Report(5, 1), 2: Report(5, 0)}).members == (0,)
+    assert e.register(2, 3) and not e.register(2, 2)
+    assert e.decide({0: Report(6, 1), 2: Report(1, 3)}).behind == {2: 1}
+    e = QuorumEngine()
+    e.decide(reports(r0=50, r1=50, r2=50))
+    e.admit_after(2, 70)
+    assert e.decide(reports(r0=51, r1=51, r2=1)).members == (0, 1)
+    assert e.pending_joiners(reports(r0=69, r1=69)) == set()
+    assert e.pending_joiners(reports(r0=70, r1=70)) == {2}
+    d = e.decide(reports(r0=70, r1=70, r2=1))
+    assert d.behind == {2: 1} and e.admission_gate(2) is None
+
+
+def test_lost_frontier_holds_target():
+    e = QuorumEngine()
+    e.decide(reports(r0=100, r1=100))
+    d = e.decide(reports(r0=1, r1=1))
+    assert d.target_step == 100 and d.healthy == () and d.behind == {0: 1, 1: 1} and d.generation == 2
+    d = e.decide(reports(r0=100, r1=1))
+    assert d.healthy == (0,) and d.behind == {1: 1}
+
+
+def test_scale_is_f32_reciprocal():
+    import numpy as np
+    d = Decision(1, 5, 2, (0, 1, 2, 3, 4, 6, 7), {5: 1})
+    assert d.scale() == float(np.float32(1.0 / 7))
+    assert d.scale(ranks_per_replica=2) == float(np.float32(1.0 / 14))
+    assert d.contrib_mask() == 0b11011111
+
+
+def _replay(ops):
+    e = QuorumEngine()
+    n = 0
+    for op in ops:
+        if op["op"] == "register":
+            assert e.register(*op["args"]) == op["result"]
+        elif op["op"] == "admit_after":
+            e.admit_after(*op["args"])
+        else:
+            reps = {int(k): Report(*v) for k, v in op["reports"].items()}
+            d = e.decide(reps)
+            want = op["decision"]
+            got = {"epoch": d.epoch, "target_step": d.target_step, "generation": d.generation,
+                   "healthy": list(d.healthy), "behind": {str(k): v for k, v in d.behind.items()},
+                   "members": list(d.members)}
+            assert got == want, f"decision {n}: {got} != {want}"
+            n += 1
+    return n
+
+
+def _streams():
+    with open(os.path.join(GOLD, "quorum_traces.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("name", sorted(_streams()))
+def test_replay_reference_decision_streams(name):
+    assert _replay(_streams()[name]) > 0
+
+
+def test_kill_trace_shape():
+    """kill r5 at step 3 for 3 steps, 8 replicas."""
+    ds = [Decision.from_json(op["decision"]) for op in _streams()["replica_kill_r5_at3_for3"]
+          if op["op"] == "decide"]
+    rows = [(d.epoch, d.target_step, d.generation, d.healthy, d.behind) for d in ds[:8]]
+    allm = (0, 1, 2, 3, 4, 5, 6, 7)
+    wo5 = (0, 1, 2, 3, 4, 6, 7)
+    assert rows[3] == (4, 3, 2, wo5, {})
+    assert rows[6] == (7, 6, 3, wo5, {5: 1})
+    assert rows[7] == (8, 7, 4, allm, {})
