@@ -1,0 +1,437 @@
+#!/usr/bin/env python
+"""FTAR bus bandwidth on B200 (driver contract; one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ftar|reference]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+
+Workload (BASELINE.json metric "FTAR bus GB/s vs bucket size at 2/4/8 B200"):
+  * N >= 2: one replica per GPU (north_star), a 256 MiB fp32 gradient bucket
+    per replica in the group's registered pool, reduced in place with the
+    fused normalisation x f32(1/N) (replica.py:622-626) — the bucket class
+    the >= 64 MB target names; the two-shot NVLink pull kernel.
+  * N = 1: the metric's multi-replica configs do not fit one GPU, so the
+    replicas are emulated: 4 replicas (config 1's replica count) of the same
+    bucket on cuda:0, reduced by the in-process one-shot kernel.  That number
+    is HBM-bound, and its roofline says so.
+  value = busbw = (E*in_bytes / t_step) * 2(n-1)/n (NCCL convention), t_step
+  from CUDA events over the K timed steps, max over ranks.
+  e2e   = the same metric through the public API with host buffers: pinned
+  host -> device copy of the step's bucket(s), the all-reduce, and the
+  device -> host read of the reduced bucket(s), all inside the timed region.
+  The reference arm (--impl reference) times the C port of the reference's
+  CPU ring (oracle/ftar_ref.c) on this host with all its threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MIB = 1024 * 1024
+NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md measured peer copy per direction (fallback; 900 nominal)
+NVLINK_NOMINAL_GBS = 900.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """SM clocks + throttle reasons sampled DURING the timed region through
+    NVML (polled every ~2 ms on a thread; the timed region can be a few ms)."""
+
+    REASONS = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown")]
+
+    def __init__(self, cuda_index: int):
+        self.cuda_index = cuda_index
+        self.samples = []
+        self.stop = threading.Event()
+        self.err = None
+        self.max_mhz = None
+
+    def __enter__(self):
+        try:
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            pr = torch.cuda.get_device_properties(self.cuda_index)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            try:
+                self.h = nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:  # noqa: BLE001
+                self.h = nv.nvmlDeviceGetHandleByIndex(self.cuda_index)
+            self.nv = nv
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+        except Exception as exc:  # noqa: BLE001
+            self.err = str(exc)[:120]
+        return self
+
+    def _poll(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, rs))
+            except Exception as exc:  # noqa: BLE001
+                self.err = str(exc)[:120]
+                return
+            time.sleep(0.002)
+
+    def __exit__(self, *exc):
+        self.stop.set()
+        if hasattr(self, "thread"):
+            self.thread.join(timeout=1)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0,
+                    "error": self.err}
+        reasons = set()
+        for _, rs in self.samples:
+            for name, attr in self.REASONS:
+                if rs & getattr(self.nv, attr, 0):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm for sm, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(self.samples), "source": "nvml"}
+
+
+def busbw(elem_bytes_total: float, t: float, n: int) -> float:
+    return (elem_bytes_total / t) * (2 * (n - 1) / n) / 1e9 if n > 1 else (elem_bytes_total / t) / 1e9
+
+
+# --------------------------------------------------------------------------- CPU
+
+
+def cpu_ring_rate(n: int, elems: int, seconds: float = 10.0, steps: int | None = None, warmup: int = 0):
+    """The C port of the reference ring on this host (oracle/ftar_ref.c)."""
+    import numpy as np
+    from oracle import cref
+    cref.build()
+    cores = os.cpu_count() or 1
+    tpm = max(1, cores // n)
+    rng = np.random.default_rng(0)
+    bufs = [rng.standard_normal(elems).astype(np.float32) for _ in range(n)]
+    for b in bufs:
+        b *= np.float32(1e-3)
+    for _ in range(warmup):
+        cref.ring_allreduce(bufs, 8 * MIB, 4, tpm)
+    times = []
+    t_end = time.perf_counter() + seconds
+    while (steps is not None and len(times) < steps) or (steps is None and (time.perf_counter() < t_end or len(times) < 3)):
+        t0 = time.perf_counter()
+        cref.ring_allreduce(bufs, 8 * MIB, 4, tpm)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    return {"value": round(busbw(elems * 4, t, n), 3), "unit": "GB/s", "cores": n * tpm, "kind": "port",
+            "sample": f"{n} replicas x {elems} fp32 (the full bucket) through the C port of the reference ring "
+                      f"(oracle/ftar_ref.c: staging copy, N-1 RS + N-1 AG ring steps, per-partition commit; "
+                      f"TCP hop replaced by shared memory), {len(times)} calls, {t * 1e3:.2f} ms/call",
+            "ms_per_call": t * 1e3, "calls": len(times)}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    n = max(args.gpus, 1) if args.gpus > 1 else args.replicas
+    r = cpu_ring_rate(n, args.bucket_mib * MIB // 4, steps=args.steps, warmup=min(args.warmup, 1))
+    cfg = workload_config(args, n)
+    line = {"metric": METRIC, "value": r["value"], "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(r["ms_per_call"], 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
+            "impl": "reference",
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU
+
+METRIC = "FTAR bus GB/s vs bucket size at 2/4/8 B200 (% NVLink peak); catch-up ms/GB"
+
+
+def workload_config(args, n):
+    elems = args.bucket_mib * MIB // 4
+    emu = args.gpus <= 1
+    return {"workload": ("config3-class bucket, replicas emulated on one GPU (N=1)" if emu
+                         else "config3-class bucket, one replica per GPU over NVLink"),
+            "replicas": n, "bucket_elems_per_replica": elems,
+            "bucket_bytes_per_replica": elems * (2 if args.dtype == "bf16" else 4),
+            "in_dtype": args.dtype, "out_dtype": "f32", "chunk_bytes": 8 * MIB, "max_in_flight": 4,
+            "fused": "x f32(1/n) normalisation" + (", bf16->fp32 cast" if args.dtype == "bf16" else ""),
+            "result": "in place" if args.inplace else "out-of-place fp32 (out=)",
+            "kernel": "in-process one-shot (cooperative)" if emu else "two-shot NVLink pull",
+            "l2": "inputs larger than L2 (126 MB) per GPU; no flush needed",
+            "parallelism": f"dp{n}" + (" (emulated)" if emu else "")}
+
+
+def timed_loop(fn, steps, stream, torch):
+    """Run fn() `steps` times; CUDA events per launch and around the loop."""
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(steps):
+        ev[i][0].record(stream)
+        fn()
+        ev[i][1].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    per = [a.elapsed_time(b) for a, b in ev]
+    return t_start.elapsed_time(t_end) / 1e3, sum(per) / len(per) / 1e3
+
+
+def run_single(args):
+    import torch
+    from paper_2602_00277_b200 import ftar
+    dev = torch.device("cuda", 0)
+    n = args.replicas
+    elems = args.bucket_mib * MIB // 4
+    tdtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    in_bytes = 2 if args.dtype == "bf16" else 4
+    ring = ftar.LocalRing(n, device=dev, max_bucket_bytes=elems * in_bytes)
+    g = torch.Generator(device=dev).manual_seed(0)
+    bufs = [torch.randn(elems, device=dev, generator=g).to(tdtype) for _ in range(n)]
+    outs = bufs if args.inplace else [torch.empty(elems, device=dev) for _ in range(n)]
+    cfg = ftar.PipelineConfig()
+    scale = 1.0 / n
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        ring.all_reduce(bufs, cfg, outs=outs, scale=scale)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    with ClockSampler(0) as clk:
+        total, per_launch = timed_loop(step, args.steps, stream, torch)
+    t_step = total / args.steps
+    value = busbw(elems * in_bytes, t_step, n)
+    peaks = measured_peaks()
+    alg_bytes = n * elems * (in_bytes + 4)
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    roof = {"bound": "hbm", "achieved": round(alg_bytes / per_launch / 1e9, 1), "peak": hbm_peak,
+            "unit": "GB/s", "frac": round(alg_bytes / per_launch / 1e9 / hbm_peak, 4), "traffic": args.traffic,
+            "kernel": "local_oneshot_kernel",
+            "algorithmic_bytes_per_launch": alg_bytes,
+            "definition": "n*E*(in_bytes+4): every replica's bucket read once, every replica's fp32 result "
+                          "written once; peak = MEASURED_PEAKS.json hbm_gbs (measured copy)",
+            "avg_launch_ms": round(per_launch * 1e3, 4)}
+    # e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        hosts = [b.cpu().pin_memory() for b in bufs]
+        hout = [torch.empty(elems, dtype=torch.float32).pin_memory() for _ in range(n)]
+
+        def e2e_step():
+            for h, b in zip(hosts, bufs):
+                b.copy_(h, non_blocking=True)
+            ring.all_reduce(bufs, cfg, outs=outs, scale=scale)
+            for o, h in zip(outs, hout):
+                h.copy_(o, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        ke = max(3, min(args.steps, 10))
+        tot, _ = timed_loop(e2e_step, ke, stream, torch)
+        e2e = {"value": round(busbw(elems * in_bytes, tot / ke, n), 3), "unit": "GB/s",
+               "h2d_bytes_per_step": n * elems * in_bytes, "d2h_bytes_per_step": n * elems * 4,
+               "ms_per_step": round(tot / ke * 1e3, 3), "steps": ke}
+    cpu = None if args.no_cpu_baseline else cpu_ring_rate(n, elems, seconds=args.cpu_seconds)
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if args.dtype == "f32" else "bf16->f32", "data": "synthetic (torch.randn buckets)",
+            "config": workload_config(args, n), "roofline": roof,
+            "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": e2e, "gpu_launches": args.steps, "clocks": clk.summary(),
+            "algbw_gbs": round(elems * in_bytes / t_step / 1e9, 3)}
+    ring.close()
+    print(json.dumps(line), flush=True)
+
+
+def run_multi(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2602_00277_b200 import ftar
+    from paper_2602_00277_b200.fabric import StoreFabric
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n = world
+    elems = args.bucket_mib * MIB // 4
+    tdtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    in_bytes = 2 if args.dtype == "bf16" else 4
+    store = dist.PrefixStore("ftar_bench", dist.distributed_c10d._get_default_store())
+    fabric = StoreFabric(store)
+    group = ftar.RingGroup(rank, 0, fabric, device=dev, max_bucket_bytes=elems * in_bytes,
+                           pool_bytes=elems * (in_bytes + 4) + 4096)
+    group.reconfig({r: ftar.PeerAddress(r) for r in range(n)}, 1, deadline_s=60.0)
+    g = torch.Generator(device=dev).manual_seed(rank)
+    buf = group.alloc_bucket(elems, tdtype)
+    buf.copy_(torch.randn(elems, device=dev, generator=g).to(tdtype))
+    out = buf if args.inplace else group.alloc_bucket(elems, torch.float32)
+    cfg = ftar.PipelineConfig()
+    scale = 1.0 / n
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        ftar.ftar_all_reduce(group, buf, 0, cfg, out=None if out is buf else out, scale=scale)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    with ClockSampler(local_rank) as clk:
+        total, per_launch = timed_loop(step, args.steps, stream, torch)
+    dist.barrier()
+    phases = phase_us(group)
+    tt = torch.tensor([total, per_launch], dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    total, per_launch = tt.tolist()
+    t_step = total / args.steps
+    value = busbw(elems * in_bytes, t_step, n)
+    nv_bytes = (n - 1) / n * elems * (in_bytes + 4)
+    roof = {"bound": "nvlink", "achieved": round(nv_bytes / per_launch / 1e9, 1), "peak": NVLINK_PEER_GBS,
+            "unit": "GB/s", "frac": round(nv_bytes / per_launch / 1e9 / NVLINK_PEER_GBS, 4), "traffic": None,
+            "kernel": "allreduce_kernel (two-shot NVLink pull)",
+            "algorithmic_bytes_per_launch": int(nv_bytes),
+            "definition": "NVLink ingress per GPU (n-1)/n*E*(in_bytes+4): RS pulls every peer's slice of my "
+                          "segment, AG pulls every peer's fp32 result; peak = 770 GB/s measured peer copy "
+                          "per direction (B200_PROFILING.md fallback; MEASURED_PEAKS.json has no NVLink entry)",
+            "frac_of_nominal_900": round(nv_bytes / per_launch / 1e9 / NVLINK_NOMINAL_GBS, 4),
+            "avg_launch_ms": round(per_launch * 1e3, 4)}
+    e2e = None
+    if not args.no_e2e:
+        host = buf.cpu().pin_memory()
+        hout = torch.empty(elems, dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            buf.copy_(host, non_blocking=True)
+            step()
+            hout.copy_(out, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ke = max(3, min(args.steps, 10))
+        tot, _ = timed_loop(e2e_step, ke, stream, torch)
+        t = torch.tensor([tot], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(busbw(elems * in_bytes, t.item() / ke, n), 3), "unit": "GB/s",
+               "h2d_bytes_per_step": elems * in_bytes, "d2h_bytes_per_step": elems * 4,
+               "ms_per_step": round(t.item() / ke * 1e3, 3), "steps": ke, "per": "rank (each GPU its own PCIe)"}
+    nccl = None
+    if not args.no_nccl:
+        nccl = nccl_busbw(args, n, elems, tdtype, dev, stream)
+    group.close()
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": n, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32" if args.dtype == "f32" else "bf16->f32", "data": "synthetic (torch.randn buckets)",
+                "config": workload_config(args, n), "roofline": roof, "cpu_baseline": None,
+                "e2e": e2e, "gpu_launches": args.steps, "clocks": clk.summary(),
+                "algbw_gbs": round(elems * in_bytes / t_step / 1e9, 3),
+                "pct_nvlink_nominal": round(100 * value / NVLINK_NOMINAL_GBS, 2),
+                "phases_us_rank0": phases,
+                "nccl_allreduce": nccl}
+        print(json.dumps(line), flush=True)
+
+
+def phase_us(group):
+    """Durations of the last call's kernel phases from its %globaltimer stamps."""
+    import ctypes as C
+    from paper_2602_00277_b200 import _lib
+    t = (C.c_uint64 * 6)()
+    _lib.lib.ftar_phase_times(group.ctx, t, 6)
+    t = list(t)
+    if not t[0] or not t[4]:
+        return None
+    names = ["entry_wait", "reduce_scatter", "rs_to_ag_barrier", "all_gather"]
+    return {k: round((t[i + 1] - t[i]) / 1e3, 1) for i, k in enumerate(names) if t[i + 1] >= t[i]}
+
+
+def nccl_busbw(args, n, elems, tdtype, dev, stream):
+    """NCCL all_reduce on the same bucket (comparison only, never on the FTAR path)."""
+    import torch
+    import torch.distributed as dist
+    try:
+        pg = dist.new_group(backend="nccl")
+        x = torch.randn(elems, device=dev).to(tdtype)
+        for _ in range(max(2, args.warmup)):
+            dist.all_reduce(x, group=pg)
+        torch.cuda.synchronize()
+        dist.barrier()
+        total, _ = timed_loop(lambda: dist.all_reduce(x, group=pg), args.steps, stream, torch)
+        t = torch.tensor([total], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        in_bytes = 2 if tdtype == torch.bfloat16 else 4
+        return {"busbw_gbs": round(busbw(elems * in_bytes, t.item() / args.steps, n), 3),
+                "dtype": str(tdtype).replace("torch.", ""), "ms_per_step": round(t.item() / args.steps * 1e3, 4)}
+    except Exception as exc:  # noqa: BLE001
+        return {"error": str(exc)[:200]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ftar", "reference"], default="ftar")
+    ap.add_argument("--dtype", choices=["f32", "bf16"], default="f32")
+    ap.add_argument("--bucket-mib", type=int, default=256, help="fp32-equivalent MiB per replica (E = MiB*2^20/4)")
+    ap.add_argument("--replicas", type=int, default=4, help="emulated replicas at N=1")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch, if captured")
+    ap.add_argument("--inplace", action="store_true", help="reduce fp32 buckets in place (reference API shape)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ftar" else args.warmup
+    if args.dtype == "bf16":
+        args.inplace = False
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    elif world > 1:
+        run_multi(args, rank, world, local_rank)
+    else:
+        run_single(args)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -48,6 +48,8 @@ extern "C" {
 
 /* ---- launch flags ---- */
 #define FTAR_F_SCALE     1u   /* multiply the fp32 sum by `scale` (replica.py:622-626) */
+#define FTAR_F_PROTOCOL  2u   /* in-process ring: run the two-shot flag protocol kernel
+                                 (as one GPU per member would) instead of the one-shot */
 
 typedef struct ftar_ctx ftar_ctx;
 
@@ -81,6 +83,9 @@ int ftar_ctx_export(ftar_ctx* ctx, void* buf, size_t buflen, size_t* written);
  * RingGroup.reconfig ftar.py:206-224. */
 int ftar_ctx_import(ftar_ctx* ctx, int slot, const void* handle, size_t len,
                     uint64_t arena_bytes);
+/* Single-process multi-GPU: map `other` (a context of this process on
+ * another device) as member `slot` through peer access (no IPC). */
+int ftar_ctx_link_local(ftar_ctx* ctx, int slot, ftar_ctx* other);
 /* Drop a member mapping (RingGroup.close_links ftar.py:226-230). */
 int ftar_ctx_unmap(ftar_ctx* ctx, int slot);
 
@@ -172,6 +177,22 @@ int ftar_snap_pull_launch(ftar_snap* local, int slot, const ftar_snap* src_local
 int ftar_snap_poll(ftar_snap* s, int* status, uint64_t* progress, int64_t* available);
 int ftar_snap_abort(ftar_snap* s);
 int ftar_snap_wait(ftar_snap* s, double progress_timeout_s, int64_t* available);
+
+/* ------------------------------------------------------------- diagnostics
+ * Streaming SM copy (dst/src may be peer addresses) with `ctas` CTAs, and
+ * peer-access enabling for single-process multi-GPU probes.  Not on the
+ * FTAR path; used to characterise NVLink pull vs push bandwidth. */
+int ftar_probe_copy(void* dst, const void* src, uint64_t bytes, int ctas, void* stream);
+/* %globaltimer stamps of the last call's phases (start, entry passed,
+ * reduce-scatter published, all-gather barrier passed, end). */
+int ftar_phase_times(ftar_ctx* ctx, uint64_t* out, int n);
+/* Per-CTA %globaltimer at the end of reduce-scatter / all-gather (last call). */
+int ftar_debug_cta_times(ftar_ctx* ctx, uint64_t* rs_end, uint64_t* ag_end, int n);
+int ftar_peer_enable(int device, int peer);
+/* Access-pattern probe: mode 0 c=a+b, 1 c=b, 2 loads only, 3 all-local;
+ * layout 0 grid-stride, 1 contiguous span per CTA. */
+int ftar_probe_pattern(float* c, const float* a, const float* b, uint64_t n, int mode, int layout,
+                       int unroll, int ctas, int device, void* stream);
 
 #ifdef __cplusplus
 }

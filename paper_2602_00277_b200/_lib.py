@@ -35,6 +35,7 @@ SIGNATURES = {
     "ftar_ctx_export": (i32, [c_ctx_p, vp, C.c_size_t, C.POINTER(C.c_size_t)]),
     "ftar_ctx_import": (i32, [c_ctx_p, i32, vp, C.c_size_t, u64]),
     "ftar_ctx_unmap": (i32, [c_ctx_p, i32]),
+    "ftar_ctx_link_local": (i32, [c_ctx_p, i32, c_ctx_p]),
     "ftar_set_membership": (i32, [c_ctx_p, C.POINTER(i32), i32, i32, u32, u64]),
     "ftar_allreduce_launch": (i32, [c_ctx_p, vp, i32, vp, u64, u64, i32, C.c_float, u32, vp]),
     "ftar_local_allreduce_launch": (i32, [C.POINTER(c_ctx_p), i32, C.POINTER(vp), i32,
@@ -57,11 +58,17 @@ SIGNATURES = {
     "ftar_snap_poll": (i32, [c_snap_p, C.POINTER(i32), C.POINTER(u64), C.POINTER(i64)]),
     "ftar_snap_abort": (i32, [c_snap_p]),
     "ftar_snap_wait": (i32, [c_snap_p, dbl, C.POINTER(i64)]),
+    "ftar_probe_copy": (i32, [vp, vp, u64, i32, vp]),
+    "ftar_peer_enable": (i32, [i32, i32]),
+    "ftar_phase_times": (i32, [c_ctx_p, C.POINTER(u64), i32]),
+    "ftar_debug_cta_times": (i32, [c_ctx_p, C.POINTER(u64), C.POINTER(u64), i32]),
+    "ftar_probe_pattern": (i32, [vp, vp, vp, u64, i32, i32, i32, i32, i32, vp]),
 }
 
 DT_F32 = 0
 DT_BF16 = 1
 F_SCALE = 1
+F_PROTOCOL = 2
 
 
 def header_symbols(path: str = _HDR) -> list[str]:

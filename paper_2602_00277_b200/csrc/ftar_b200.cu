@@ -21,6 +21,7 @@
 #include "ftar_device.cuh"
 #include "../../include/ftar_b200.h"
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <atomic>
@@ -43,6 +44,7 @@ __host__ __device__ __forceinline__ uint64_t umin(uint64_t a, uint64_t b) { retu
 __host__ __device__ __forceinline__ uint64_t umax(uint64_t a, uint64_t b) { return a > b ? a : b; }
 
 constexpr uint32_t ST_FOLLOW = 254;  // stop because another CTA of mine failed
+constexpr uint32_t kFlagDirect = 1u << 8;  // internal launch flag: RS writes my slice of out
 
 struct LaunchParams {
   char* base[kMaxMembers];       // arena base of ring member i, as mapped here
@@ -64,6 +66,8 @@ struct LaunchParams {
   int emulated;                  // 1: ring index = blockIdx.y (in-process ring)
   int fault_member;              // test hook (-1 none)
   int fault_after_tiles;
+  int rs_layout;                 // 0: contiguous span per CTA, 1: grid-strided tiles
+  int diag;                      // timing diagnostics: 1 = RS stores skipped, 2 = RS reads local only
 };
 
 __device__ __forceinline__ uint32_t severity_code(uint32_t st) {
@@ -129,14 +133,65 @@ __device__ __forceinline__ void owner_of(uint64_t e, const LaunchParams& p, int 
   seg_end = poff + send;
 }
 
+// Where folded values go: one fp32 array (result region or output), two
+// (result region + my slice of `out`), or every member's output (in-process
+// one-shot).  Arrays are indexed by global element; put4 writes 16 B/lane.
+struct SinkOne {
+  float* p;
+  __device__ __forceinline__ void put1(uint64_t e, float x) const { p[e] = x; }
+  __device__ __forceinline__ void put4(uint64_t e, const uint4& v) const { *reinterpret_cast<uint4*>(p + e) = v; }
+};
+struct SinkNone {  // diagnostics: results computed, never stored
+  float* p;
+  __device__ __forceinline__ void put1(uint64_t e, float x) const {
+    if (__float_as_uint(x) == 0x7fc00001u) p[e] = x;
+  }
+  __device__ __forceinline__ void put4(uint64_t e, const uint4& v) const {
+    if (v.x == 0x7fc00001u && v.y == 0x7fc00001u) *reinterpret_cast<uint4*>(p + e) = v;
+  }
+};
+struct SinkTwo {
+  float* p;
+  float* q;
+  __device__ __forceinline__ void put1(uint64_t e, float x) const { p[e] = x; q[e] = x; }
+  __device__ __forceinline__ void put4(uint64_t e, const uint4& v) const {
+    *reinterpret_cast<uint4*>(p + e) = v;
+    st_stream(q + e, v);
+  }
+};
+template <int N>
+struct SinkAll {
+  float* const* outs;
+  __device__ __forceinline__ void put1(uint64_t e, float x) const {
+#pragma unroll
+    for (int j = 0; j < N; ++j) outs[j][e] = x;
+  }
+  __device__ __forceinline__ void put4(uint64_t e, const uint4& v) const {
+#pragma unroll
+    for (int j = 0; j < N; ++j) st_stream(outs[j] + e, v);
+  }
+};
+
+// 4-element vectors each thread keeps in flight per source: ~16 loads per
+// thread per round whatever the ring size.
+template <int N, class In>
+struct Unroll {
+  static constexpr int U0 = (16 * 16 / (int)sizeof(typename In::Raw)) / N;  // ~256 B of loads per thread
+  static constexpr int U = U0 < 1 ? 1 : (U0 > 16 ? 16 : U0);
+};
+
 // Reduce elements [a, b) whose fold starts at ring index s.  All threads of the
-// CTA cooperate; 16-byte vectors in the body, scalars at the ragged edges.
-template <int N, class In, int U>
-__device__ __forceinline__ void fold_range(const typename In::T* const* src, float* res,
+// CTA cooperate; each round a thread issues U x N coalesced vector loads
+// (unconditionally: out-of-range vectors re-read a valid one and are masked,
+// non-contributors read and are zeroed by select) before the first add, so no
+// branch separates the loads; scalars at the ragged edges.
+template <int N, class In, int U, class Sink>
+__device__ __forceinline__ void fold_range(const typename In::T* const* src, const Sink& sink,
                                            uint64_t a, uint64_t b, int s, uint32_t contrib,
                                            bool vec_ok, bool do_scale, float scale,
                                            uint32_t& nf) {
   using T = typename In::T;
+  using Raw = typename In::Raw;
   const T* rs[N];
   bool cb[N];
 #pragma unroll
@@ -150,57 +205,91 @@ __device__ __forceinline__ void fold_range(const typename In::T* const* src, flo
   auto scalar_elem = [&](uint64_t e) {
     float acc = cb[0] ? In::scalar(rs[0], e) : 0.0f;
 #pragma unroll
-    for (int k = 1; k < N; ++k) {
-      const float x = cb[k] ? In::scalar(rs[k], e) : 0.0f;
-      acc = __fadd_rn(acc, x);
-    }
+    for (int k = 1; k < N; ++k) acc = __fadd_rn(acc, cb[k] ? In::scalar(rs[k], e) : 0.0f);
     nf |= nonfinite_bits(acc) ? 1u : 0u;
     if (do_scale) acc = __fmul_rn(acc, scale);
-    res[e] = acc;
+    sink.put1(e, acc);
   };
   if (!vec_ok) {
     for (uint64_t e = a + tid; e < b; e += kThreads) scalar_elem(e);
     return;
   }
-  const uint64_t head = umin(b, (a + 7) & ~7ull);
+  const uint64_t head = umin(b, (a + 3) & ~3ull);
   if (a + tid < head) scalar_elem(a + tid);
-  const uint64_t vb = head >> 3, ve = b >> 3;
-  for (uint64_t v0 = vb + tid; v0 < ve; v0 += (uint64_t)kThreads * U) {
-    float x[U][N][8];
+  const uint64_t vb = head >> 2, ve = b >> 2;
+  if (vb < ve) {
+    for (uint64_t v0 = vb + tid; v0 < ve; v0 += (uint64_t)kThreads * U) {
+      Raw raw[U][N];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t v = v0 + (uint64_t)u * kThreads;
+      for (int u = 0; u < U; ++u) {
+        const uint64_t v = v0 + (uint64_t)u * kThreads;
+        const uint64_t vv = v < ve ? v : vb;  // clamp: keep the load unconditional
 #pragma unroll
-      for (int k = 0; k < N; ++k) {
-        if (v < ve && cb[k]) {
-          In::load8(rs[k], v * 8, x[u][k]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) x[u][k][i] = 0.0f;
-        }
+        for (int k = 0; k < N; ++k) raw[u][k] = In::load4(rs[k], vv * 4);
       }
-    }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t v = v0 + (uint64_t)u * kThreads;
-      if (v < ve) {
-        float acc[8];
+      for (int u = 0; u < U; ++u) {
+        const uint64_t v = v0 + (uint64_t)u * kThreads;
+        float acc[4], x[4];
+        In::cvt4(cb[0] ? raw[u][0] : In::zero(), acc);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          acc[i] = x[u][0][i];
+        for (int k = 1; k < N; ++k) {
+          In::cvt4(cb[k] ? raw[u][k] : In::zero(), x);
 #pragma unroll
-          for (int k = 1; k < N; ++k) acc[i] = __fadd_rn(acc[i], x[u][k][i]);
-          nf |= nonfinite_bits(acc[i]) ? 1u : 0u;
-          if (do_scale) acc[i] = __fmul_rn(acc[i], scale);
+          for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], x[i]);
         }
-        float4* d = reinterpret_cast<float4*>(res + v * 8);
-        d[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-        d[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        if (v < ve) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            nf |= nonfinite_bits(acc[i]) ? 1u : 0u;
+            if (do_scale) acc[i] = __fmul_rn(acc[i], scale);
+          }
+          sink.put4(v * 4, make_uint4(__float_as_uint(acc[0]), __float_as_uint(acc[1]),
+                                      __float_as_uint(acc[2]), __float_as_uint(acc[3])));
+        }
       }
     }
   }
-  const uint64_t tail = umax(head, ve << 3);
+  const uint64_t tail = umax(head, ve << 2);
   if (tail + tid < b) scalar_elem(tail + tid);
+}
+
+// Fold [lo, hi) in grid-strided tiles (the CTAs' working set stays one
+// compact window, which keeps NVLink/TLB locality), caching the current owner
+// run so owner_of only runs when a tile crosses a segment boundary.
+template <int N, class In, class Sink>
+__device__ __forceinline__ int fold_tiles(const LaunchParams& p, const typename In::T* const* src,
+                                          const Sink& sink, uint64_t lo, uint64_t hi, bool vec_ok,
+                                          bool do_scale, uint32_t& nf, HostCtl* ctl, int max_tiles) {
+  constexpr int U = Unroll<N, In>::U;
+  const uint64_t TL = (uint64_t)kThreads * 4 * U;
+  int done = 0;
+  int s = 0;
+  uint64_t sbeg = 1, send = 0;  // cached run [sbeg, send) with owner s
+  uint64_t first = lo + (uint64_t)blockIdx.x * TL, step = (uint64_t)gridDim.x * TL;
+  if (p.rs_layout == 0) {  // one contiguous span per CTA
+    const uint64_t per = ((hi - lo + gridDim.x - 1) / gridDim.x + 7) & ~7ull;
+    first = umin(lo + (uint64_t)blockIdx.x * per, hi);
+    hi = umin(first + per, hi);
+    step = TL;
+  }
+  for (uint64_t a = first; a < hi; a += step) {
+    if (done >= max_tiles) return -1;
+    const uint64_t b = umin(a + TL, hi);
+    uint64_t cur = a;
+    while (cur < b) {
+      if (cur < sbeg || cur >= send) {
+        owner_of(cur, p, N, s, send);
+        sbeg = cur;
+      }
+      const uint64_t end = umin(send, b);
+      fold_range<N, In, U>(src, sink, cur, end, s, p.contrib, vec_ok, do_scale, p.scale, nf);
+      cur = end;
+    }
+    ++done;
+    if (threadIdx.x == 0 && (done & 63) == 0) ctl->progress = ((uint64_t)blockIdx.x << 32) | (uint64_t)done;
+  }
+  return done;
 }
 
 // Grid-stride fp32 copy (the all-gather pull), 16-byte vectors, UA loads in
@@ -214,30 +303,28 @@ __device__ __forceinline__ void copy_f32(float* dst, const float* src, uint64_t 
     return;
   }
   const uint64_t nv = cnt >> 2;
-  for (uint64_t v = first; v < nv; v += stride * UA) {
-    uint4 r[UA];
+  if (nv) {
+    for (uint64_t v = first; v < nv; v += stride * UA) {
+      uint4 r[UA];
 #pragma unroll
-    for (int u = 0; u < UA; ++u) {
-      const uint64_t i = v + (uint64_t)u * stride;
-      if (i < nv) r[u] = ld_stream(src + i * 4);
-    }
+      for (int u = 0; u < UA; ++u) {
+        const uint64_t i = v + (uint64_t)u * stride;
+        r[u] = ld_stream(src + (i < nv ? i : 0) * 4);
+      }
 #pragma unroll
-    for (int u = 0; u < UA; ++u) {
-      const uint64_t i = v + (uint64_t)u * stride;
-      if (i < nv) *reinterpret_cast<uint4*>(dst + i * 4) = r[u];
+      for (int u = 0; u < UA; ++u) {
+        const uint64_t i = v + (uint64_t)u * stride;
+        if (i < nv) *reinterpret_cast<uint4*>(dst + i * 4) = r[u];
+      }
     }
   }
   const uint64_t t = (nv << 2) + first;
   if (t < cnt && first < 4) dst[t] = src[t];
 }
 
-template <int N>
-struct Unroll { static constexpr int U = (N <= 2) ? 4 : (N <= 4 ? 2 : 1); };
-
 template <int N, class In>
 __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_constant__ LaunchParams p) {
   using T = typename In::T;
-  constexpr int U = Unroll<N>::U;
   const int me = p.emulated ? (int)blockIdx.y : p.self;
   char* const mybase = p.base[me];
   ArenaHdr* const hdr = reinterpret_cast<ArenaHdr*>(mybase);
@@ -245,13 +332,18 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
   const uint64_t tag = p.tag;
   const uint64_t E = p.nelems;
   const int tid = threadIdx.x;
+  const uint64_t lo = umin((uint64_t)me * p.slice, E);
+  const uint64_t hi = umin(lo + p.slice, E);
+  // direct: my reduced slice goes straight into `out` (out-of-place calls);
+  // res_off then addresses element `lo` of my out inside my arena, so peers
+  // pull my slice from there (p.res_off is already that when out is registered)
+  const bool direct = (p.flags & kFlagDirect) != 0;
 
   __shared__ const T* s_src[N];
   __shared__ const float* s_res[N];
   __shared__ uint32_t s_status;
   __shared__ int s_blame;
   __shared__ uint32_t s_nf;
-  __shared__ uint32_t s_stop[2];
   __shared__ int s_vec_ok;
   __shared__ uint64_t s_t0;
 
@@ -259,7 +351,6 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
     s_status = ST_OK;
     s_blame = -1;
     s_nf = 0;
-    s_stop[0] = s_stop[1] = 0;
     s_t0 = globaltimer_ns();
     if (blockIdx.x == 0) {
       // Epoch fence: an op queued under an older decision must not run
@@ -269,6 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         s_blame = me;
       }
       ctl->started = tag;
+      ctl->tphase[0] = s_t0;
       if (s_status == ST_OK) {
         EntryRec* en = &hdr->entry;
         en->in_off = p.in_off[me];
@@ -289,8 +381,8 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
     int ok = 1;
     for (int j = 0; j < N; ++j) {
       if (j == me) {
-        s_src[j] = reinterpret_cast<const T*>(mybase + p.in_off[me]);
-        s_res[j] = reinterpret_cast<const float*>(mybase + p.res_off[me]);
+        s_src[j] = reinterpret_cast<const T*>(reinterpret_cast<uint64_t>(mybase) + p.in_off[me]);
+        s_res[j] = reinterpret_cast<const float*>(reinterpret_cast<uint64_t>(mybase) + p.res_off[me]);
         continue;
       }
       ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
@@ -312,8 +404,8 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         ok = 0;
         break;
       }
-      s_src[j] = reinterpret_cast<const T*>(p.base[j] + in_off);
-      s_res[j] = reinterpret_cast<const float*>(p.base[j] + res_off);
+      s_src[j] = reinterpret_cast<const T*>(reinterpret_cast<uint64_t>(p.base[j]) + in_off);
+      s_res[j] = reinterpret_cast<const float*>(reinterpret_cast<uint64_t>(p.base[j]) + res_off);
     }
     if (ok) {
       uint64_t orbits = reinterpret_cast<uint64_t>(p.out[me]);
@@ -321,53 +413,36 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         orbits |= reinterpret_cast<uint64_t>(s_src[j]) | reinterpret_cast<uint64_t>(s_res[j]);
       s_vec_ok = (orbits & 15u) == 0;
     }
+    if (blockIdx.x == 0) {
+      ctl->tphase[1] = globaltimer_ns();
+      hdr->dbg_t1 = ctl->tphase[1];
+    }
   }
   __syncthreads();
 
-  // ---- 2. reduce-scatter of my slice -----------------------------------
-  const uint64_t lo = umin((uint64_t)me * p.slice, E);
-  const uint64_t hi = umin(lo + p.slice, E);
+  // ---- 2. reduce-scatter of my slice: one contiguous span per CTA --------
   uint32_t nf = 0;
+  int done = 0;
   if (s_status == ST_OK) {
-    float* const res = reinterpret_cast<float*>(mybase + p.res_off[me]) - lo;
     const bool vec_ok = s_vec_ok != 0;
     const bool do_scale = (p.flags & FTAR_F_SCALE) != 0;
-    const uint64_t TL = (uint64_t)kThreads * 8 * U;
-    const uint64_t ntiles = (hi - lo + TL - 1) / TL;
-    int done = 0;
-    uint32_t it = 0;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      if (tid == 0) {
-        uint32_t stop = 0;
-        if (p.fault_member == me && done >= p.fault_after_tiles) {
-          s_status = ST_INJECTED;
-          stop = 1;
-        } else if (ld_relaxed_sys32(&hdr->err) != 0) {
-          s_status = ST_FOLLOW;
-          stop = 1;
-        }
-        s_stop[it & 1] = stop;
-      }
+    const int max_tiles = (p.fault_member == me) ? p.fault_after_tiles : 0x7fffffff;
+    float* const res = const_cast<float*>(s_res[me]) - lo;  // indexed by global element
+    if (p.diag == 1) {
+      done = fold_tiles<N, In>(p, s_src, SinkNone{res}, lo, hi, vec_ok, do_scale, nf, ctl, max_tiles);
+    } else if (p.diag == 2) {
+      __shared__ const T* s_loc[N];
+      if (tid < N) s_loc[tid] = s_src[me];
       __syncthreads();
-      if (s_stop[it & 1]) break;
-      const uint64_t a = lo + t * TL, b = umin(a + TL, hi);
-      uint64_t cur = a;
-      while (cur < b) {
-        int s;
-        uint64_t send;
-        owner_of(cur, p, N, s, send);
-        const uint64_t end = umin(send, b);
-        fold_range<N, In, U>(s_src, res, cur, end, s, p.contrib, vec_ok, do_scale, p.scale, nf);
-        cur = end;
-      }
-      ++done;
-      if (tid == 0) {
-        const unsigned long long v =
-            atomicAdd(reinterpret_cast<unsigned long long*>(&hdr->tiles_done), 1ull) + 1ull;
-        if ((v & 3ull) == 0) ctl->progress = v;
-      }
+      done = fold_tiles<N, In>(p, s_loc, SinkOne{res}, lo, hi, vec_ok, do_scale, nf, ctl, max_tiles);
+    } else if (direct && res != p.out[me]) {
+      done = fold_tiles<N, In>(p, s_src, SinkTwo{res, p.out[me]}, lo, hi, vec_ok, do_scale, nf, ctl, max_tiles);
+    } else {
+      done = fold_tiles<N, In>(p, s_src, SinkOne{res}, lo, hi, vec_ok, do_scale, nf, ctl, max_tiles);
     }
+    if (done < 0 && tid == 0) s_status = ST_INJECTED;
   }
+  if (tid == 0 && blockIdx.x < 256) hdr->dbg_rs_end[blockIdx.x] = globaltimer_ns();
   if (__any_sync(0xffffffffu, nf != 0) && (tid & 31) == 0) atomicOr(&s_nf, 1u);
   __syncthreads();
   if (tid == 0) {
@@ -378,14 +453,24 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
       hdr->err_peer = s_blame;
       if (st != ST_INJECTED) st_release_sys(&hdr->poison, mk_flag(tag, st));
     }
-    __threadfence_system();
+    if (done > 0) atomicAdd(reinterpret_cast<unsigned long long*>(&hdr->tiles_done), (unsigned long long)done);
+    // arrival: gpu-scope release (the CTA's writes, ordered by the bar.sync
+    // above, before the counter); the last CTA then publishes with ONE
+    // sys-scope fence + release store, which is cumulative over everything
+    // the counter chain made it observe.  Per-CTA sys fences cost ~100 us.
+    __threadfence();
     const uint32_t old = atomicAdd(&hdr->rs_arrive, 1u);
     if (old == gridDim.x - 1) {
+      __threadfence();
+      hdr->dbg_fence[0] = globaltimer_ns();
       __threadfence_system();
+      hdr->dbg_fence[1] = globaltimer_ns();
       if (ld_relaxed_sys32(&hdr->err) == 0) {
         const uint32_t bits = ld_relaxed_sys32(&hdr->nonfinite) ? kBitNonFinite : 0u;
         st_release_sys(&hdr->rs_done, mk_flag(tag, bits));
+        ctl->tphase[2] = globaltimer_ns();
       }
+      ctl->progress = hdr->tiles_done;
     }
   }
 
@@ -406,6 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
       bits |= b;
     }
     if (s_status == ST_OK && (bits & kBitNonFinite)) s_status = ST_NUMERICAL;
+    if (blockIdx.x == 0) ctl->tphase[3] = globaltimer_ns();
   }
   __syncthreads();
 
@@ -413,13 +499,16 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
   if (s_status == ST_OK) {
     float* const out = p.out[me];
     const bool vec_ok = s_vec_ok != 0;
+    // every CTA starts on a different peer so all links stay busy
     for (int i = 0; i < N; ++i) {
       const int k = (int)((me + 1 + blockIdx.x + i) % N);
+      if (direct && k == me) continue;  // written during the reduce-scatter
       const uint64_t klo = umin((uint64_t)k * p.slice, E), khi = umin(klo + p.slice, E);
       copy_f32<8>(out + klo, s_res[k], khi - klo, vec_ok);
     }
   }
   __syncthreads();
+  if (tid == 0 && blockIdx.x < 256) hdr->dbg_ag_end[blockIdx.x] = globaltimer_ns();
 
   // ---- 5. completion -----------------------------------------------------
   if (tid == 0) {
@@ -429,14 +518,18 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
       hdr->err_peer = s_blame;
       if (st != ST_INJECTED && st != ST_NUMERICAL) st_release_sys(&hdr->poison, mk_flag(tag, st));
     }
-    __threadfence_system();
+    __threadfence();
     const uint32_t old = atomicAdd(&hdr->done_arrive, 1u);
     if (old == gridDim.x - 1) {
+      __threadfence();
+      hdr->dbg_fence[2] = globaltimer_ns();
       __threadfence_system();
+      hdr->dbg_fence[3] = globaltimer_ns();
       const uint32_t err = ld_relaxed_sys32(&hdr->err);
       const uint64_t tiles = hdr->tiles_done;
       ctl->detail = err ? (int64_t)hdr->err_peer : -1;
       ctl->progress = tiles + 1;
+      ctl->tphase[4] = globaltimer_ns();
       hdr->rs_arrive = 0;
       hdr->done_arrive = 0;
       hdr->nonfinite = 0;
@@ -597,6 +690,180 @@ snap_pull_kernel(const char* src_arena, SnapHdr* lhdr, HostCtl* ctl, uint64_t ta
   }
 }
 
+// ---------------------------------------------------------------- in-process one-shot
+// All members of an in-process ring live on this GPU, so no member has to
+// wait for another: one cooperative grid folds every element from all member
+// inputs (same reference fold order and fusions as the protocol kernel),
+// stages the fp32 sums once, and — only if every sum is finite — broadcasts
+// them to all member outputs.  HBM traffic: n*in + 4 (stage write) + 4 (stage
+// read) + n*4 bytes per element, vs the minimum n*(in+4).
+struct LocalParams {
+  const void* in[kMaxMembers];
+  float* out[kMaxMembers];
+  HostCtl* ctl[kMaxMembers];
+  float* stage;             // nullptr: direct mode (outputs never alias inputs)
+  uint32_t* flags;          // [0] nonfinite
+  uint64_t tag[kMaxMembers];
+  uint64_t nelems;
+  uint64_t p_base, p_rem;
+  float scale;
+  uint32_t flags_in;
+  uint32_t contrib;
+};
+
+template <int N, class In>
+__global__ void __launch_bounds__(kThreads, 1) local_oneshot_kernel(const __grid_constant__ LocalParams p) {
+  using T = typename In::T;
+  constexpr int U = Unroll<N, In>::U;
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ const T* s_src[N];
+  __shared__ uint32_t s_nf;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_nf = 0;
+    for (int j = 0; j < N; ++j) s_src[j] = static_cast<const T*>(p.in[j]);
+    if (blockIdx.x == 0)
+      for (int j = 0; j < N; ++j) p.ctl[j]->started = p.tag[j];
+  }
+  __syncthreads();
+  LaunchParams g{};
+  g.p_base = p.p_base;
+  g.p_rem = p.p_rem;
+  uint64_t orbits = reinterpret_cast<uint64_t>(p.stage);
+  for (int j = 0; j < N; ++j) orbits |= reinterpret_cast<uint64_t>(p.in[j]) | reinterpret_cast<uint64_t>(p.out[j]);
+  const bool vec_ok = (orbits & 15u) == 0;
+  const bool do_scale = (p.flags_in & FTAR_F_SCALE) != 0;
+  const uint64_t E = p.nelems;
+  const uint64_t TL = (uint64_t)kThreads * 8 * U;
+  const uint64_t ntiles = (E + TL - 1) / TL;
+  uint32_t nf = 0;
+  const bool direct = p.stage == nullptr;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint64_t a = t * TL, b = umin(a + TL, E);
+    uint64_t cur = a;
+    while (cur < b) {
+      int s;
+      uint64_t send;
+      owner_of(cur, g, N, s, send);
+      const uint64_t end = umin(send, b);
+      if (direct)
+        fold_range<N, In, U>(s_src, SinkAll<N>{p.out}, cur, end, s, p.contrib, vec_ok, do_scale, p.scale, nf);
+      else
+        fold_range<N, In, U>(s_src, SinkOne{p.stage}, cur, end, s, p.contrib, vec_ok, do_scale, p.scale, nf);
+      cur = end;
+    }
+  }
+  if (__any_sync(0xffffffffu, nf != 0) && (tid & 31) == 0) atomicOr(&s_nf, 1u);
+  __syncthreads();
+  if (tid == 0 && s_nf) atomicOr(p.flags, 1u);
+  grid.sync();
+  const bool bad = ld_relaxed_sys32(p.flags) != 0;
+  if (!bad && !direct) {
+    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+    const uint64_t first = (uint64_t)blockIdx.x * kThreads + tid;
+    if (vec_ok) {
+      const uint64_t nv = E >> 2;
+      constexpr int UB = 4;
+      for (uint64_t v = first; v < nv; v += stride * UB) {
+        uint4 r[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+          const uint64_t i = v + (uint64_t)u * stride;
+          if (i < nv) r[u] = ld_stream(p.stage + i * 4);
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            const uint64_t i = v + (uint64_t)u * stride;
+            if (i < nv) st_stream(p.out[j] + i * 4, r[u]);
+          }
+      }
+      const uint64_t tl = (nv << 2) + first;
+      if (tl < E && first < 4)
+        for (int j = 0; j < N; ++j) p.out[j][tl] = p.stage[tl];
+    } else {
+      for (uint64_t e = first; e < E; e += stride) {
+        const float x = p.stage[e];
+        for (int j = 0; j < N; ++j) p.out[j][e] = x;
+      }
+    }
+  }
+  grid.sync();
+  if (blockIdx.x == 0 && tid == 0) {
+    const uint32_t st = bad ? ST_NUMERICAL : ST_OK;
+    *p.flags = 0;
+    __threadfence_system();
+    for (int j = 0; j < N; ++j) {
+      p.ctl[j]->detail = -1;
+      p.ctl[j]->progress = ntiles + 1;
+      p.ctl[j]->done = mk_flag(p.tag[j], st);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- diagnostics
+// Streaming copy used to characterise the NVLink path (pull = remote src,
+// push = remote dst) at a given CTA count; not on the FTAR path.
+__global__ void __launch_bounds__(kThreads) probe_copy_kernel(char* dst, const char* src, uint64_t bytes) {
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  const uint64_t first = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  copy_bytes_grid(dst, src, bytes, first, stride);
+}
+
+// Access-pattern probe (diagnostic): elements are fp32; a = local, b = remote.
+//  mode 0: c[i] = a[i] + b[i]    (reduce-scatter-like, N = 2)
+//  mode 1: c[i] = b[i]           (all-gather-like)
+//  mode 2: s += a[i] + b[i], no store (loads only)
+//  mode 3: c[i] = a[i] + a2[i]   (all local)
+// layout 0: grid-stride 16-byte vectors; layout 1: contiguous span per CTA.
+// `unroll` vectors per thread in flight per source.
+template <int UNR>
+__global__ void __launch_bounds__(kThreads, 1) probe_pattern_kernel(float* c, const float* a, const float* b,
+                                                                    uint64_t n, int mode, int layout) {
+  const uint64_t nv = n >> 2;
+  uint64_t first, stride, end;
+  if (layout == 0) {
+    first = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+    stride = (uint64_t)gridDim.x * kThreads;
+    end = nv;
+  } else {
+    const uint64_t per = (nv + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = umin((uint64_t)blockIdx.x * per, nv);
+    first = lo + threadIdx.x;
+    stride = kThreads;
+    end = umin(lo + per, nv);
+  }
+  float acc = 0.f;
+  for (uint64_t v = first; v < end; v += stride * UNR) {
+    uint4 ra[UNR], rb[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const uint64_t i = v + (uint64_t)u * stride;
+      const uint64_t ii = i < end ? i : first;
+      ra[u] = ld_stream(a + ii * 4);
+      rb[u] = ld_stream((mode == 3 ? a + (nv - 1 - ii) * 4 : b + ii * 4));
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const uint64_t i = v + (uint64_t)u * stride;
+      if (i < end) {
+        uint4 r = rb[u];
+        if (mode != 1) {
+          r.x = __float_as_uint(__uint_as_float(ra[u].x) + __uint_as_float(rb[u].x));
+          r.y = __float_as_uint(__uint_as_float(ra[u].y) + __uint_as_float(rb[u].y));
+          r.z = __float_as_uint(__uint_as_float(ra[u].z) + __uint_as_float(rb[u].z));
+          r.w = __float_as_uint(__uint_as_float(ra[u].w) + __uint_as_float(rb[u].w));
+        }
+        if (mode == 2) acc += __uint_as_float(r.x);
+        else *reinterpret_cast<uint4*>(c + i * 4) = r;
+      }
+    }
+  }
+  if (mode == 2 && acc == 123456.f) c[0] = acc;
+}
+
 __global__ void snap_init_kernel(SnapHdr* h) {
   h->seq = 0;
   h->step = -1;
@@ -655,6 +922,8 @@ int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 int real_ctas() { return g_ctas > 0 ? g_ctas : env_int("FTAR_CTAS", 32); }
+int rs_layout() { return env_int("FTAR_RS_LAYOUT", 0); }
+int diag_mode() { return env_int("FTAR_DIAG", 0); }
 
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -673,6 +942,7 @@ struct ftar_ctx {
   HostCtl* ctl_d = nullptr;
   char* peer[kMaxSlots] = {};
   uint64_t peer_bytes[kMaxSlots] = {};
+  bool peer_local[kMaxSlots] = {};  // linked in-process (no IPC handle to close)
   int ring_slots[kMaxMembers] = {};
   int n = 1, self = 0;
   uint32_t contrib = 1;
@@ -728,6 +998,31 @@ int max_coop_blocks_per_sm(int n) {
   cudaError_t e = cudaErrorInvalidValue;
   switch (n) {
 #define CASE(K) case K: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, allreduce_kernel<K, In>, kThreads, 0); break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+  }
+  return e == cudaSuccess ? nb : 0;
+}
+
+template <class In>
+cudaError_t oneshot_dispatch(int n, const LocalParams& lp, dim3 grid, cudaStream_t st) {
+  void* args[] = {const_cast<LocalParams*>(&lp)};
+  const void* fn = nullptr;
+  switch (n) {
+#define CASE(K) case K: fn = (const void*)local_oneshot_kernel<K, In>; break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaLaunchCooperativeKernel(fn, grid, dim3(kThreads), args, 0, st);
+}
+
+template <class In>
+int oneshot_blocks_per_sm(int n) {
+  int nb = 0;
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (n) {
+#define CASE(K) case K: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, local_oneshot_kernel<K, In>, kThreads, 0); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
   }
@@ -794,8 +1089,10 @@ int ftar_ctx_create(int device, uint64_t max_bucket_bytes, uint64_t pool_bytes, 
   c->exportable = exportable != 0;
   c->max_bucket_bytes = align_up(std::max<uint64_t>(max_bucket_bytes, 256), 256);
   c->res_off = kHdrBytes;
-  // result region: my slice in fp32 <= ceil(E/2)+8 elems; E <= max_bucket_bytes/2 (bf16)
-  const uint64_t res_bytes = align_up(c->max_bucket_bytes + 64, 4096);
+  // result region: the fp32 image of a whole bucket (E <= max_bucket_bytes/2
+  // for bf16 -> 2x bytes); the protocol kernel uses my slice of it, the
+  // in-process one-shot kernel stages the whole fp32 sum in member 0's.
+  const uint64_t res_bytes = align_up(2 * c->max_bucket_bytes + 64, 4096);
   c->stage_off[0] = c->res_off + res_bytes;
   c->stage_off[1] = c->stage_off[0] + c->max_bucket_bytes;
   c->pool_off = c->stage_off[1] + c->max_bucket_bytes;
@@ -833,7 +1130,7 @@ int ftar_ctx_destroy(ftar_ctx* c) {
   DeviceGuard g(c->device);
   cudaDeviceSynchronize();
   for (int s = 0; s < kMaxSlots; ++s)
-    if (c->peer[s]) cudaIpcCloseMemHandle(c->peer[s]);
+    if (c->peer[s] && !c->peer_local[s]) cudaIpcCloseMemHandle(c->peer[s]);
   cudaFree(c->arena);
   cudaFreeHost((void*)c->ctl_h);
   delete c;
@@ -876,12 +1173,29 @@ int ftar_ctx_import(ftar_ctx* c, int slot, const void* handle, size_t len, uint6
   return FTAR_OK;
 }
 
+int ftar_ctx_link_local(ftar_ctx* c, int slot, ftar_ctx* other) {
+  // Single-process multi-GPU: map member `other` (another device of this
+  // process) as `slot` through peer access instead of CUDA IPC.
+  if (!c || !other || slot < 0 || slot >= kMaxSlots) return fail(FTAR_ST_INVARIANT, "bad link args");
+  if (c->peer[slot] && c->peer[slot] != other->arena) return fail(FTAR_ST_INVARIANT, "slot in use");
+  if (c->device != other->device) {
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceEnablePeerAccess(other->device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "enable peer access");
+    cudaGetLastError();
+  }
+  c->peer[slot] = other->arena;
+  c->peer_local[slot] = true;
+  return FTAR_OK;
+}
+
 int ftar_ctx_unmap(ftar_ctx* c, int slot) {
   if (!c || slot < 0 || slot >= kMaxSlots) return fail(FTAR_ST_INVARIANT, "bad unmap args");
   DeviceGuard g(c->device);
   if (c->peer[slot]) {
-    cudaIpcCloseMemHandle(c->peer[slot]);
+    if (!c->peer_local[slot]) cudaIpcCloseMemHandle(c->peer[slot]);
     c->peer[slot] = nullptr;
+    c->peer_local[slot] = false;
   }
   return FTAR_OK;
 }
@@ -967,13 +1281,23 @@ int ftar_allreduce_launch(ftar_ctx* c, const void* in, int in_dtype, float* out,
   p.nelems = n_elems;
   p.hard_timeout_ns = c->hard_timeout_ns;
   p.scale = scale;
-  p.flags = flags;
+  p.flags = flags & 0xffu;
+  {
+    // out-of-place: the reduce-scatter also writes my slice of `out` (peers
+    // still pull from the library-owned result region, so `out` is free for
+    // the caller as soon as the call returns)
+    const uint64_t o0 = reinterpret_cast<uint64_t>(out), i0 = reinterpret_cast<uint64_t>(in);
+    const bool alias = o0 < i0 + in_bytes && i0 < o0 + n_elems * 4;
+    if (!alias && n_elems && !env_int("FTAR_NO_DIRECT", 0)) p.flags |= kFlagDirect;
+  }
   p.contrib = c->contrib;
   p.dtype = (uint32_t)in_dtype;
   p.self = c->self;
   p.emulated = 0;
   p.fault_member = -1;
   p.fault_after_tiles = 0;
+  p.rs_layout = rs_layout();
+  p.diag = diag_mode();
   reset_ctl(c->ctl_h);
   c->cur_tag = tag;
   c->inflight = true;
@@ -1028,15 +1352,62 @@ int ftar_local_allreduce_launch(ftar_ctx** ctxs, int n, const void* const* ins, 
   p.nelems = n_elems;
   p.hard_timeout_ns = ctxs[0]->hard_timeout_ns;
   p.scale = scale;
-  p.flags = flags;
+  p.flags = flags & 0xffu;
+  {
+    const uint64_t ib = n_elems * (in_dtype == FTAR_DT_BF16 ? 2 : 4), ob = n_elems * 4;
+    bool alias = false;
+    for (int i = 0; i < n && !alias; ++i)
+      for (int j = 0; j < n && !alias; ++j) {
+        const uint64_t o0 = reinterpret_cast<uint64_t>(outs[i]), i0 = reinterpret_cast<uint64_t>(ins[j]);
+        alias = o0 < i0 + ib && i0 < o0 + ob;
+      }
+    if (!alias && n_elems) p.flags |= kFlagDirect;
+  }
   p.contrib = contrib_mask & ((1u << n) - 1u);
   p.dtype = (uint32_t)in_dtype;
   p.self = 0;
   p.emulated = 1;
   p.fault_member = fault_member;
   p.fault_after_tiles = fault_after_tiles;
+  p.rs_layout = rs_layout();
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (!(flags & FTAR_F_PROTOCOL) && fault_member < 0) {
+    LocalParams lp{};
+    for (int i = 0; i < n; ++i) {
+      lp.in[i] = ins[i];
+      lp.out[i] = outs[i];
+      lp.ctl[i] = ctxs[i]->ctl_d;
+      lp.tag[i] = ctxs[i]->cur_tag;
+    }
+    ArenaHdr* h0 = reinterpret_cast<ArenaHdr*>(ctxs[0]->arena);
+    // direct mode unless some output overlaps some input (in-place calls):
+    // then stage so that a non-finite sum leaves every buffer untouched
+    const uint64_t ib = n_elems * (in_dtype == FTAR_DT_BF16 ? 2 : 4), ob = n_elems * 4;
+    bool alias = false;
+    for (int i = 0; i < n && !alias; ++i)
+      for (int j = 0; j < n && !alias; ++j) {
+        const uint64_t o0 = reinterpret_cast<uint64_t>(outs[i]), i0 = reinterpret_cast<uint64_t>(ins[j]);
+        alias = o0 < i0 + ib && i0 < o0 + ob;
+      }
+    lp.stage = alias ? reinterpret_cast<float*>(ctxs[0]->arena + ctxs[0]->res_off) : nullptr;
+    lp.flags = &h0->nonfinite;
+    lp.nelems = n_elems;
+    lp.p_base = p.p_base;
+    lp.p_rem = p.p_rem;
+    lp.scale = scale;
+    lp.flags_in = flags;
+    lp.contrib = p.contrib;
+    const int bps = in_dtype == FTAR_DT_BF16 ? oneshot_blocks_per_sm<BF16In>(n) : oneshot_blocks_per_sm<F32In>(n);
+    const dim3 grid(std::max(1, sms * std::max(bps, 1)));
+    cudaError_t e = in_dtype == FTAR_DT_BF16 ? oneshot_dispatch<BF16In>(n, lp, grid, st)
+                                              : oneshot_dispatch<F32In>(n, lp, grid, st);
+    if (e != cudaSuccess) {
+      for (int i = 0; i < n; ++i) ctxs[i]->inflight = false;
+      return cuda_fail(e, "local one-shot cooperative launch");
+    }
+    return FTAR_OK;
+  }
   const int per_sm = in_dtype == FTAR_DT_BF16 ? max_coop_blocks_per_sm<BF16In>(n) : max_coop_blocks_per_sm<F32In>(n);
   int G = std::max(1, (sms * std::max(per_sm, 1)) / n);
   const int want = g_local_ctas > 0 ? g_local_ctas : env_int("FTAR_LOCAL_CTAS", 32);
@@ -1168,6 +1539,61 @@ int ftar_wait_local(ftar_ctx** ctxs, int n, double progress_timeout_s, int* stat
       std::this_thread::sleep_for(std::chrono::microseconds(it < 20000 ? 5 : 100));
     }
   }
+}
+
+int ftar_phase_times(ftar_ctx* c, uint64_t* out, int n) {
+  if (!c || !out) return fail(FTAR_ST_INVARIANT, "bad args");
+  for (int i = 0; i < n && i < 6; ++i) out[i] = c->ctl_h->tphase[i];
+  return FTAR_OK;
+}
+
+int ftar_probe_pattern(float* c, const float* a, const float* b, uint64_t n, int mode, int layout, int unroll,
+                       int ctas, int device, void* stream) {
+  DeviceGuard dg(device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int g = std::max(1, ctas);
+  switch (unroll) {
+    case 1: probe_pattern_kernel<1><<<g, kThreads, 0, st>>>(c, a, b, n, mode, layout); break;
+    case 2: probe_pattern_kernel<2><<<g, kThreads, 0, st>>>(c, a, b, n, mode, layout); break;
+    case 4: probe_pattern_kernel<4><<<g, kThreads, 0, st>>>(c, a, b, n, mode, layout); break;
+    case 8: probe_pattern_kernel<8><<<g, kThreads, 0, st>>>(c, a, b, n, mode, layout); break;
+    default: return fail(FTAR_ST_INVARIANT, "unroll must be 1, 2, 4 or 8");
+  }
+  CK(cudaGetLastError());
+  return FTAR_OK;
+}
+
+int ftar_debug_cta_times(ftar_ctx* c, uint64_t* rs_end, uint64_t* ag_end, int n) {
+  if (!c) return fail(FTAR_ST_INVARIANT, "null ctx");
+  DeviceGuard g(c->device);
+  ArenaHdr h;
+  CK(cudaMemcpy(&h, c->arena, sizeof(h), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n && i < 256; ++i) {
+    rs_end[i] = h.dbg_rs_end[i];
+    ag_end[i] = h.dbg_ag_end[i];
+  }
+  if (n >= 260) {  // caller wants the fence stamps too (rs_end[256..259])
+    for (int i = 0; i < 4; ++i) rs_end[256 + i] = h.dbg_fence[i];
+  }
+  return FTAR_OK;
+}
+
+int ftar_probe_copy(void* dst, const void* src, uint64_t bytes, int ctas, void* stream) {
+  probe_copy_kernel<<<std::max(1, ctas), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<char*>(dst), static_cast<const char*>(src), bytes);
+  CK(cudaGetLastError());
+  return FTAR_OK;
+}
+
+int ftar_peer_enable(int device, int peer) {
+  DeviceGuard g(device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return FTAR_OK;
+  }
+  CK(e);
+  return FTAR_OK;
 }
 
 // ------------------------------------------------------------------ operators

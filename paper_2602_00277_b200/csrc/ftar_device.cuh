@@ -62,6 +62,10 @@ struct alignas(128) ArenaHdr {
   int32_t err_peer;
   uint32_t pad0;
   uint64_t tiles_done;
+  alignas(128) uint64_t dbg_rs_end[256];  // per-CTA %globaltimer at end of reduce-scatter
+  uint64_t dbg_ag_end[256];               // per-CTA %globaltimer at end of all-gather
+  uint64_t dbg_t1;                        // entry barrier passed (block 0)
+  uint64_t dbg_fence[4];                  // last CTA: before/after the sys fence (RS, end)
 };
 static_assert(sizeof(ArenaHdr) <= kHdrBytes, "header too large");
 
@@ -76,6 +80,9 @@ struct alignas(64) HostCtl {
   volatile uint64_t done;          // device -> host: mk_flag(tag, status)
   volatile int64_t detail;         // device -> host: ring index blamed (-1 none)
   volatile int64_t available;      // device -> host: snapshot step available
+  volatile uint64_t tphase[6];     // device -> host: %globaltimer at phase ends
+                                   // [0] start [1] entry passed [2] RS published
+                                   // [3] AG barrier passed [4] end
 };
 
 // Snapshot arena header (retention-1 seqlock, checkpoint.py:56-80).
@@ -134,34 +141,41 @@ __device__ __forceinline__ bool nonfinite_bits(float x) {
   return (__float_as_uint(x) & 0x7f800000u) == 0x7f800000u;
 }
 
-// Element types of the bucket: the fp32 upcast of bf16 is exact.
+// Element types of the bucket: the fp32 upcast of bf16 is exact.  The unit of
+// vector work is 4 elements per lane, so that every warp-wide load (16 B/lane
+// fp32, 8 B/lane bf16) and every fp32 store (16 B/lane) is fully coalesced:
+// peer reads bypass L2, so a half-used sector is NVLink bandwidth thrown away.
+__device__ __forceinline__ uint2 ld_stream64(const void* p) {
+  uint2 r;
+  asm volatile("ld.global.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+
 struct F32In {
   using T = float;
+  using Raw = uint4;
   static constexpr int kBytes = 4;
   __device__ __forceinline__ static float scalar(const float* p, uint64_t e) { return p[e]; }
-  // 8 elements = two 16-byte loads
-  __device__ __forceinline__ static void load8(const float* p, uint64_t e, float (&v)[8]) {
-    uint4 a = ld_stream(p + e), b = ld_stream(p + e + 4);
-    v[0] = __uint_as_float(a.x); v[1] = __uint_as_float(a.y);
-    v[2] = __uint_as_float(a.z); v[3] = __uint_as_float(a.w);
-    v[4] = __uint_as_float(b.x); v[5] = __uint_as_float(b.y);
-    v[6] = __uint_as_float(b.z); v[7] = __uint_as_float(b.w);
+  __device__ __forceinline__ static Raw load4(const float* p, uint64_t e) { return ld_stream(p + e); }
+  __device__ __forceinline__ static Raw zero() { return make_uint4(0u, 0u, 0u, 0u); }
+  __device__ __forceinline__ static void cvt4(const Raw& r, float (&v)[4]) {
+    v[0] = __uint_as_float(r.x); v[1] = __uint_as_float(r.y);
+    v[2] = __uint_as_float(r.z); v[3] = __uint_as_float(r.w);
   }
 };
 struct BF16In {
   using T = __nv_bfloat16;
+  using Raw = uint2;
   static constexpr int kBytes = 2;
   __device__ __forceinline__ static float up(uint32_t h) { return __uint_as_float(h << 16); }
   __device__ __forceinline__ static float scalar(const __nv_bfloat16* p, uint64_t e) {
     return up(reinterpret_cast<const uint16_t*>(p)[e]);
   }
-  // 8 elements = one 16-byte load
-  __device__ __forceinline__ static void load8(const __nv_bfloat16* p, uint64_t e, float (&v)[8]) {
-    uint4 a = ld_stream(p + e);
-    v[0] = up(a.x & 0xffffu); v[1] = up(a.x >> 16);
-    v[2] = up(a.y & 0xffffu); v[3] = up(a.y >> 16);
-    v[4] = up(a.z & 0xffffu); v[5] = up(a.z >> 16);
-    v[6] = up(a.w & 0xffffu); v[7] = up(a.w >> 16);
+  __device__ __forceinline__ static Raw load4(const __nv_bfloat16* p, uint64_t e) { return ld_stream64(p + e); }
+  __device__ __forceinline__ static Raw zero() { return make_uint2(0u, 0u); }
+  __device__ __forceinline__ static void cvt4(const Raw& r, float (&v)[4]) {
+    v[0] = __uint_as_float(r.x << 16); v[1] = __uint_as_float(r.x & 0xffff0000u);
+    v[2] = __uint_as_float(r.y << 16); v[3] = __uint_as_float(r.y & 0xffff0000u);
   }
 };
 

@@ -472,8 +472,9 @@ def _local_all_reduce(group, buf, dst, code, cfg, f_scale, flags):
         ins = (C.c_void_p * n)(*[call.deposits[i]["buf"].data_ptr() for i in range(n)])
         outs = (C.c_void_p * n)(*[call.deposits[i]["out"].data_ptr() for i in range(n)])
         contrib = groups[0]._contrib_mask if n > 1 else 1
+        lflags = flags | (_lib.F_PROTOCOL if _local_protocol() else 0)
         rc = _lib.lib.ftar_local_allreduce_launch(ctxs, n, ins, code, outs, buf.numel(), cfg.chunk_bytes,
-                                                  cfg.max_in_flight, f_scale, flags, contrib, fault_member,
+                                                  cfg.max_in_flight, f_scale, lflags, contrib, fault_member,
                                                   fault_after, stream.cuda_stream)
         _lib.check(rc, "ftar_local_allreduce_launch")
         sts = (C.c_int * n)()
@@ -488,14 +489,24 @@ def _local_all_reduce(group, buf, dst, code, cfg, f_scale, flags):
         raise from_status(st, f"peer replica {blame}" if blame is not None else "")
 
 
+def _local_protocol() -> bool:
+    """In-process rings run the one-shot kernel unless FTAR_LOCAL_MODE=protocol
+    asks for the two-shot flag protocol (what one GPU per member runs)."""
+    return os.environ.get("FTAR_LOCAL_MODE", "oneshot") == "protocol"
+
+
 class LocalRing:
     """n single-rank members of one ring in this process, on one device —
     the B200 counterpart of ``bench._LoopbackRing`` (bench.py:53-96).
     ``all_reduce`` issues the members' calls without threads (one cooperative
-    launch), which is what the benchmark times."""
+    launch), which is what the benchmark times.  ``protocol=True`` runs the
+    two-shot flag-protocol kernel (the multi-GPU kernel, members as CTA
+    groups); the default one-shot kernel needs no inter-member waits."""
 
-    def __init__(self, n: int, device=None, max_bucket_bytes: int = 64 * MIB, rank: int = 0):
+    def __init__(self, n: int, device=None, max_bucket_bytes: int = 64 * MIB, rank: int = 0,
+                 protocol: bool | None = None):
         self.n = n
+        self.protocol = _local_protocol() if protocol is None else protocol
         self.fabric = LocalFabric()
         self.groups = [RingGroup(rid, rank, self.fabric, device=device, max_bucket_bytes=max_bucket_bytes)
                        for rid in range(n)]
@@ -540,6 +551,8 @@ class LocalRing:
         ins = (C.c_void_p * n)(*[bufs[i].data_ptr() for i in range(n)])
         ous = (C.c_void_p * n)(*[outs[i].data_ptr() for i in range(n)])
         fm, fa = (-1, 0) if fault is None else fault
+        if self.protocol or fault is not None:
+            flags |= _lib.F_PROTOCOL
         rc = _lib.lib.ftar_local_allreduce_launch(ctxs, n, ins, code, ous, bufs[0].numel(), cfg.chunk_bytes,
                                                   cfg.max_in_flight, f_scale, flags, groups[0]._contrib_mask,
                                                   fm, fa, _stream_ptr(groups[0].device))
@@ -564,3 +577,73 @@ class LocalRing:
     def close(self):
         for g in self.groups:
             g.close()
+
+
+class DeviceRing:
+    """n members of one ring on n GPUs driven by ONE process (peer access
+    instead of CUDA IPC): member i lives on devices[i].  Same kernel and flag
+    protocol as one process per GPU; the members' kernels run concurrently
+    on their own GPUs.  Used for single-process multi-GPU jobs and tuning."""
+
+    def __init__(self, devices, max_bucket_bytes: int = 64 * MIB, generation: int = 1):
+        self.devices = [torch.device("cuda", d) if isinstance(d, int) else torch.device(d) for d in devices]
+        self.n = len(self.devices)
+        self.ctxs = []
+        for d in self.devices:
+            ctx = C.c_void_p()
+            _lib.check(_lib.lib.ftar_ctx_create(d.index, max_bucket_bytes, 0, 0, C.byref(ctx)), "ftar_ctx_create")
+            self.ctxs.append(ctx)
+        for i, c in enumerate(self.ctxs):
+            for j, o in enumerate(self.ctxs):
+                if i != j:
+                    _lib.check(_lib.lib.ftar_ctx_link_local(c, j, o), "ftar_ctx_link_local")
+        self.generation = 0
+        self.reconfig(generation)
+
+    def reconfig(self, generation: int, contributors=None):
+        if generation <= self.generation:
+            raise Fatal(INTERNAL_INVARIANT, "generation must increase")
+        self.generation = generation
+        contrib = sum(1 << i for i in range(self.n) if contributors is None or i in contributors)
+        for i, c in enumerate(self.ctxs):
+            slots = (C.c_int * self.n)(*[-1 if j == i else j for j in range(self.n)])
+            _lib.check(_lib.lib.ftar_set_membership(c, slots, self.n, i, contrib, generation),
+                       "ftar_set_membership")
+
+    def launch(self, bufs, cfg: PipelineConfig | None = None, outs=None, scale=None):
+        cfg = cfg or PipelineConfig()
+        outs = outs if outs is not None else bufs
+        flags = _lib.F_SCALE if scale is not None else 0
+        f_scale = float(torch.tensor(scale if scale is not None else 1.0, dtype=torch.float32))
+        for i, c in enumerate(self.ctxs):
+            rc = _lib.lib.ftar_allreduce_launch(c, bufs[i].data_ptr(), _dtype_code(bufs[i]), outs[i].data_ptr(),
+                                                bufs[i].numel(), cfg.chunk_bytes, cfg.max_in_flight, f_scale, flags,
+                                                _stream_ptr(self.devices[i]))
+            _lib.check(rc, "ftar_allreduce_launch")
+
+    def wait(self, cfg: PipelineConfig | None = None) -> list[int]:
+        cfg = cfg or PipelineConfig()
+        out = []
+        for c in self.ctxs:
+            det = C.c_int(-1)
+            out.append(_lib.lib.ftar_wait(c, cfg.per_chunk_timeout_s, C.byref(det)))
+        return out
+
+    def all_reduce(self, bufs, cfg: PipelineConfig | None = None, outs=None, scale=None):
+        self.launch(bufs, cfg, outs, scale)
+        for st in self.wait(cfg):
+            if st:
+                raise from_status(st)
+        return outs if outs is not None else bufs
+
+    def phase_us(self, i: int = 0):
+        t = (C.c_uint64 * 6)()
+        _lib.lib.ftar_phase_times(self.ctxs[i], t, 6)
+        t = list(t)
+        names = ["entry_wait", "reduce_scatter", "rs_to_ag_barrier", "all_gather"]
+        return {k: round((t[j + 1] - t[j]) / 1e3, 1) for j, k in enumerate(names) if t[j + 1] >= t[j] > 0}
+
+    def close(self):
+        for c in self.ctxs:
+            _lib.lib.ftar_ctx_destroy(c)
+        self.ctxs = []

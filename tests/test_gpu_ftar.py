@@ -45,10 +45,11 @@ def ftar():
 def rings(ftar):
     made = {}
 
-    def get(n):
-        if n not in made:
-            made[n] = ftar.LocalRing(n, device=DEV, max_bucket_bytes=32 * 1024 * 1024)
-        return made[n]
+    def get(n, protocol=True):
+        if (n, protocol) not in made:
+            made[(n, protocol)] = ftar.LocalRing(n, device=DEV, max_bucket_bytes=32 * 1024 * 1024,
+                                                 protocol=protocol)
+        return made[(n, protocol)]
 
     yield get
     for r in made.values():
@@ -59,9 +60,10 @@ def to_dev(a, dtype=torch.float32):
     return torch.from_numpy(np.ascontiguousarray(a)).to(DEV).to(dtype)
 
 
+@pytest.mark.parametrize("mode", ["protocol", "oneshot"])
 @pytest.mark.parametrize("case", cases(), ids=lambda c: f"{c['idx']}-{c['kind']}-n{c['n']}-e{c['elems']}")
-def test_golden_cases_bit_exact(ftar, rings, case):
-    ring = rings(case["n"])
+def test_golden_cases_bit_exact(ftar, rings, case, mode):
+    ring = rings(case["n"], protocol=(mode == "protocol"))
     cfg = ftar.PipelineConfig(chunk_bytes=case["chunk_bytes"], max_in_flight=case["max_in_flight"],
                               per_chunk_timeout_s=10.0)
     behind = behind_set(case)
@@ -80,11 +82,12 @@ def test_golden_cases_bit_exact(ftar, rings, case):
         assert sha(o.cpu().numpy()) == case["sha256"]
 
 
-def test_config1_digest_and_scale(ftar, rings):
+@pytest.mark.parametrize("mode", ["protocol", "oneshot"])
+def test_config1_digest_and_scale(ftar, rings, mode):
     with open(os.path.join(GOLD, "config1.json")) as f:
         g = json.load(f)
     arrays = member_inputs(g["n"], g["elems"], seed=g["seed"])
-    ring = rings(4)
+    ring = rings(4, protocol=(mode == "protocol"))
     ring.reconfig()
     bufs = [to_dev(a) for a in arrays]
     ring.all_reduce(bufs)
@@ -101,10 +104,11 @@ def test_config1_digest_and_scale(ftar, rings):
         np.testing.assert_array_equal(b.cpu().numpy(), a)
 
 
+@pytest.mark.parametrize("mode", ["protocol", "oneshot"])
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 8])
-def test_bf16_bucket_default_geometry(ftar, rings, n):
+def test_bf16_bucket_default_geometry(ftar, rings, n, mode):
     arrays = member_inputs(n, 1_000_003, seed=5, dtype="bf16")
-    ring = rings(n)
+    ring = rings(n, protocol=(mode == "protocol"))
     ring.reconfig()
     bufs = [to_dev(a, torch.bfloat16) for a in arrays]
     outs = [torch.empty(a.size, device=DEV) for a in arrays]
@@ -114,11 +118,12 @@ def test_bf16_bucket_default_geometry(ftar, rings, n):
         np.testing.assert_array_equal(o.cpu().numpy(), want)
 
 
-def test_nonfinite_is_fatal_everywhere_and_nothing_committed(ftar, rings):
+@pytest.mark.parametrize("mode", ["protocol", "oneshot"])
+def test_nonfinite_is_fatal_everywhere_and_nothing_committed(ftar, rings, mode):
     for poison in (np.nan, np.inf):
         arrays = [np.ones(4099, dtype=np.float32) for _ in range(3)]
         arrays[1][3000] = poison
-        ring = rings(3)
+        ring = rings(3, protocol=(mode == "protocol"))
         ring.reconfig()
         bufs = [to_dev(a) for a in arrays]
         with pytest.raises(Exception) as ei:
@@ -165,7 +170,8 @@ def test_fault_injection_mid_reduce_scatter_then_requorum(ftar, rings):
     ring.reconfig()  # restore full membership for other tests
 
 
-def test_replay_reference_replica_run(ftar, rings):
+@pytest.mark.parametrize("mode", ["protocol", "oneshot"])
+def test_replay_reference_replica_run(ftar, rings, mode):
     """Every successful ftar_all_reduce of the reference's 8-replica
     kill/rejoin run (tests/golden/replica_ftar.npz): same members, same
     inputs (behind replicas' zeros), same outputs bit for bit."""
@@ -180,7 +186,7 @@ def test_replay_reference_replica_run(ftar, rings):
         by_rep = {meta[i]["replica"]: i for i in idxs}
         assert sorted(by_rep) == list(members)
         n = len(members)
-        ring = rings(8)
+        ring = rings(8, protocol=(mode == "protocol"))
         ring.reconfig(members=list(range(n)))
         chunk, C = meta[idxs[0]]["cfg"]
         cfg = ftar.PipelineConfig(chunk_bytes=chunk, max_in_flight=C)

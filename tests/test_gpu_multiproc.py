@@ -1,0 +1,198 @@
+"""One process per GPU over NVLink (the production topology): CUDA-IPC arena
+mapping through a TCPStore rendezvous, the two-shot pull kernel, failure of a
+member mid-collective, quorum re-agreement and retry.  Needs >= 2 GPUs (run
+with `gpurun --gpus 2` / `--gpus 4`); skipped otherwise."""
+
+import json
+import os
+import socket
+import sys
+import tempfile
+
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, scenario, outdir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    import hashlib
+
+    import numpy as np
+    import torch.distributed as dist
+    from datetime import timedelta
+
+    from gen import behind_set, case_inputs, member_inputs
+    from oracle import ftar_oracle as orc
+    from paper_2602_00277_b200 import errors, ftar
+    from paper_2602_00277_b200.fabric import StoreFabric
+    from paper_2602_00277_b200.quorum import Report, StoreQuorum
+
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    store = dist.TCPStore("127.0.0.1", port, world, rank == 0, timeout=timedelta(seconds=60))
+    fabric = StoreFabric(dist.PrefixStore(scenario, store))
+    res = {"rank": rank, "ok": [], "errors": []}
+
+    def sha(a):
+        return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float32).tobytes()).hexdigest()
+
+    group = ftar.RingGroup(rank, 0, fabric, device=dev, max_bucket_bytes=64 << 20, pool_bytes=16 << 20)
+    try:
+        if scenario == "golden":
+            with open(os.path.join(ROOT, "tests", "golden", "ftar_cases.json")) as f:
+                cases = [c for c in json.load(f) if c["n"] == world]
+            gen = 0
+            for case in cases:
+                gen += 1
+                behind = behind_set(case)
+                group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, gen, deadline_s=30,
+                               contributors=[r for r in range(world) if r not in behind])
+                arrays = case_inputs(case, garbage_behind=bool(behind))
+                cfg = ftar.PipelineConfig(chunk_bytes=case["chunk_bytes"], max_in_flight=case["max_in_flight"],
+                                          per_chunk_timeout_s=10)
+                if case["kind"] == "bf16":
+                    buf = torch.from_numpy(arrays[rank]).to(dev).to(torch.bfloat16)
+                    out = torch.empty(case["elems"], device=dev)
+                    ftar.ftar_all_reduce(group, buf, 1, cfg, out=out)
+                else:
+                    out = torch.from_numpy(arrays[rank]).to(dev)
+                    assert ftar.ftar_all_reduce(group, out, 1, cfg) is out
+                got = sha(out.cpu().numpy())
+                (res["ok"] if got == case["sha256"] else res["errors"]).append(case["idx"])
+            # big bucket: registered (zero-copy) bf16 with fused scale, default geometry
+            gen += 1
+            group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, gen, deadline_s=30)
+            arrays = member_inputs(world, 1_500_001, seed=4, dtype="bf16")
+            b = group.alloc_bucket(arrays[0].size, torch.bfloat16)
+            b.copy_(torch.from_numpy(arrays[rank]).to(dev).to(torch.bfloat16))
+            o = group.alloc_bucket(arrays[0].size, torch.float32)
+            for _ in range(3):
+                ftar.ftar_all_reduce(group, b, 2, ftar.PipelineConfig(), out=o, scale=1.0 / world)
+            want = orc.normalize(orc.oracle_reduce(arrays, 8 << 20, 4), world)
+            (res["ok"] if np.array_equal(o.cpu().numpy(), want) else res["errors"]).append("big_bf16")
+        elif scenario == "failure":
+            # config 2 in miniature: the highest rank stalls mid-collective
+            # (it never calls); survivors must get Recoverable within 2x the
+            # timeout, regroup through the quorum (generation+1) and retry.
+            victim = world - 1
+            q = StoreQuorum(fabric.store, list(range(world)))
+            d = q.exchange(1, rank, Report(1, 0))
+            group.reconfig({r: ftar.PeerAddress(r) for r in d.members}, d.generation, deadline_s=30)
+            arrays = member_inputs(world, 2_000_003, seed=8)
+            cfg = ftar.PipelineConfig(per_chunk_timeout_s=1.0)
+            buf = torch.from_numpy(arrays[rank]).to(dev)
+            if rank == victim:
+                import time
+                time.sleep(6.0)  # a hung replica: misses this round and the next quorum round
+                res["ok"].append("victim")
+            else:
+                import time
+                t0 = time.monotonic()
+                try:
+                    ftar.ftar_all_reduce(group, buf, 1, cfg)
+                    res["errors"].append("no error")
+                except errors.Recoverable as exc:
+                    took = time.monotonic() - t0
+                    res["ok"].append(f"recoverable:{exc.reason}:{took:.2f}")
+                    if took > 2 * cfg.per_chunk_timeout_s + 0.5:
+                        res["errors"].append(f"slow abort {took:.2f}")
+                if not np.array_equal(buf.cpu().numpy(), arrays[rank]):
+                    res["errors"].append("buffer modified")
+                d2 = q.exchange(2, rank, Report(1, 0), round_deadline_s=2.0)
+                res["decision"] = d2.to_json()
+                if victim in d2.members or d2.generation != d.generation + 1:
+                    res["errors"].append(f"bad decision {d2}")
+                group.reconfig({r: ftar.PeerAddress(r) for r in d2.members}, d2.generation, deadline_s=30)
+                out = torch.empty_like(buf)
+                ftar.ftar_all_reduce(group, buf, 1, cfg, out=out, scale=d2.scale())
+                want = orc.normalize(orc.oracle_reduce([arrays[r] for r in d2.members], cfg.chunk_bytes,
+                                                       cfg.max_in_flight), len(d2.healthy))
+                (res["ok"] if np.array_equal(out.cpu().numpy(), want) else res["errors"]).append("retry")
+        elif scenario == "catchup":
+            from paper_2602_00277_b200 import checkpoint as ck
+            snap = ck.SnapshotStore(capacity_bytes=64 << 20, device=dev, fabric=fabric, rank=0, replica_id=rank)
+            g = torch.Generator(device=dev).manual_seed(3)
+            p = torch.randn(8 << 20 >> 2, device=dev, generator=g)
+            m = torch.randn(8 << 20 >> 2, device=dev, generator=g)
+            if rank == 0:
+                snap.capture(5, p, m)
+                torch.cuda.synchronize()
+            store.set("captured", b"1")
+            store.wait(["captured"])
+            if rank == 1:
+                po, mo = torch.empty_like(p), torch.empty_like(m)
+                ck.fetch_shard(0, 5, 0, local=snap, out=(po, mo), timeout_s=10)
+                g0 = torch.Generator(device=dev).manual_seed(3)
+                wp = torch.randn(8 << 20 >> 2, device=dev, generator=g0)
+                wm = torch.randn(8 << 20 >> 2, device=dev, generator=g0)
+                (res["ok"] if torch.equal(po, wp) and torch.equal(mo, wm) else res["errors"]).append("pull")
+                try:
+                    ck.fetch_shard(0, 4, 0, local=snap, out=(po, mo), timeout_s=10)
+                    res["errors"].append("stale step served")
+                except ck.SnapshotUnavailable as exc:
+                    (res["ok"] if exc.available == 5 else res["errors"]).append("unavailable")
+            store.set(f"done{rank}", b"1")
+            store.wait([f"done{r}" for r in range(world)])
+    except Exception as exc:  # noqa: BLE001
+        import traceback
+        res["errors"].append(f"exception: {exc!r}\n{traceback.format_exc()}")
+    finally:
+        store.set(f"fin{rank}", b"1")
+        try:
+            store.wait([f"fin{r}" for r in range(world)], timedelta(seconds=60))
+        except Exception:  # noqa: BLE001
+            pass
+        group.close()
+        with open(os.path.join(outdir, f"r{rank}.json"), "w") as f:
+            json.dump(res, f)
+
+
+def run(scenario, world):
+    port = free_port()
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_worker, args=(world, port, scenario, d), nprocs=world, join=True, start_method="spawn")
+        out = []
+        for r in range(world):
+            with open(os.path.join(d, f"r{r}.json")) as f:
+                out.append(json.load(f))
+    return out
+
+
+def world_size():
+    return min(torch.cuda.device_count(), 8)
+
+
+def test_golden_cases_over_nvlink():
+    res = run("golden", world_size())
+    for r in res:
+        assert not r["errors"], r["errors"]
+        assert "big_bf16" in r["ok"]
+
+
+def test_member_failure_requorum_and_retry():
+    res = run("failure", world_size())
+    for r in res:
+        assert not r["errors"], r["errors"]
+    survivors = [r for r in res if "victim" not in r["ok"]]
+    assert all(any(x.startswith("recoverable") for x in r["ok"]) for r in survivors)
+    assert all("retry" in r["ok"] for r in survivors)
+
+
+def test_catchup_pull_over_nvlink():
+    res = run("catchup", 2)
+    assert not res[1]["errors"], res[1]["errors"]
+    assert "pull" in res[1]["ok"] and "unavailable" in res[1]["ok"]
