@@ -189,6 +189,10 @@ int ftar_phase_times(ftar_ctx* ctx, uint64_t* out, int n);
 /* Per-CTA %globaltimer at the end of reduce-scatter / all-gather (last call). */
 int ftar_debug_cta_times(ftar_ctx* ctx, uint64_t* rs_end, uint64_t* ag_end, int n);
 int ftar_peer_enable(int device, int peer);
+/* Fence-cost probe: c = a + b (b remote), load flavour `kind`, per-CTA
+ * %globaltimer stamps (loop end, bar.sync, gpu fence, sys fence). */
+int ftar_probe_fence(float* c, const float* a, const float* b, uint64_t n, int kind, int ctas,
+                     uint64_t* stamps, int device, void* stream);
 /* Access-pattern probe: mode 0 c=a+b, 1 c=b, 2 loads only, 3 all-local;
  * layout 0 grid-stride, 1 contiguous span per CTA. */
 int ftar_probe_pattern(float* c, const float* a, const float* b, uint64_t n, int mode, int layout,

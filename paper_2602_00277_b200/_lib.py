@@ -60,6 +60,7 @@ SIGNATURES = {
     "ftar_snap_wait": (i32, [c_snap_p, dbl, C.POINTER(i64)]),
     "ftar_probe_copy": (i32, [vp, vp, u64, i32, vp]),
     "ftar_peer_enable": (i32, [i32, i32]),
+    "ftar_probe_fence": (i32, [vp, vp, vp, u64, i32, i32, vp, i32, vp]),
     "ftar_phase_times": (i32, [c_ctx_p, C.POINTER(u64), i32]),
     "ftar_debug_cta_times": (i32, [c_ctx_p, C.POINTER(u64), C.POINTER(u64), i32]),
     "ftar_probe_pattern": (i32, [vp, vp, vp, u64, i32, i32, i32, i32, i32, vp]),

@@ -84,21 +84,41 @@ __device__ __forceinline__ uint32_t severity_code(uint32_t st) {
 __device__ uint32_t wait_flag(const uint64_t* flag, uint64_t tag, const uint64_t* poison,
                               const HostCtl* ctl, const uint32_t* own_err, uint64_t t0,
                               uint64_t limit_ns, uint32_t* bits) {
+  // Relaxed polls (no fence per poll: acquire loads from many spinning CTAs
+  // slow down every other CTA's fences), one acquire fence on success,
+  // exponential-ish backoff so idle pollers leave NVLink and L2 alone.
   for (uint32_t it = 0;; ++it) {
-    const uint64_t f = ld_acquire_sys(flag);
+    const uint64_t f = ld_relaxed_sys(flag);
     const uint64_t ft = flag_tag(f);
     if (ft == tag) {
+      fence_acq_rel_sys();
       if (bits) *bits = (uint32_t)(f & 0xffu);
       return ST_OK;
     }
     if (ft > tag) return tag_gen(ft) > tag_gen(tag) ? ST_PEER_RESET : ST_PROTOCOL;
     if ((it & 15u) == 15u) {
-      if (poison && flag_tag(ld_acquire_sys(poison)) == tag) return ST_PEER_RESET;
+      if (poison && flag_tag(ld_relaxed_sys(poison)) == tag) return ST_PEER_RESET;
       if (ctl->abort_tag == tag) return ST_ABORTED;
       if (own_err && ld_relaxed_sys32(own_err) != 0) return ST_FOLLOW;
       if (globaltimer_ns() - t0 > limit_ns) return ST_TIMEOUT;
     }
-    if (it > 256) __nanosleep(200);
+    if (it > 4) __nanosleep(it < 64 ? 64 : 256);
+  }
+}
+
+// Local fan-out: wait for CTA 0 of this member to post `want` on hdr->go.
+// Only CTA 0 polls peers and the host; the others spin on one L2 word.
+__device__ uint32_t wait_go(const ArenaHdr* hdr, uint64_t want, uint64_t t0, uint64_t limit_ns) {
+  for (uint32_t it = 0;; ++it) {
+    if (ld_relaxed_gpu(&hdr->go) == want) {
+      fence_acq_rel_gpu();
+      return ST_OK;
+    }
+    if ((it & 15u) == 15u) {
+      if (ld_relaxed_sys32(&hdr->err) != 0) return ST_FOLLOW;
+      if (globaltimer_ns() - t0 > limit_ns) return ST_TIMEOUT;
+    }
+    if (it > 4) __nanosleep(it < 64 ? 64 : 256);
   }
 }
 
@@ -376,46 +396,56 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
   }
   __syncthreads();
 
-  // ---- 1. entry barrier -------------------------------------------------
+  // ---- 1. entry barrier (CTA 0 polls the members, then fans out) ---------
   if (tid == 0 && s_status == ST_OK) {
-    int ok = 1;
-    for (int j = 0; j < N; ++j) {
-      if (j == me) {
-        s_src[j] = reinterpret_cast<const T*>(reinterpret_cast<uint64_t>(mybase) + p.in_off[me]);
-        s_res[j] = reinterpret_cast<const float*>(reinterpret_cast<uint64_t>(mybase) + p.res_off[me]);
-        continue;
-      }
-      ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
-      uint32_t st = wait_flag(&ph->entry.flag, tag, &ph->poison, ctl, &hdr->err, s_t0,
-                              p.hard_timeout_ns, nullptr);
-      uint64_t in_off = 0, res_off = 0;
-      if (st == ST_OK) {
-        in_off = ld_relaxed_sys(&ph->entry.in_off);
-        res_off = ld_relaxed_sys(&ph->entry.res_off);
-        const uint64_t ne = ld_relaxed_sys(&ph->entry.nelems);
-        const uint64_t ge = ld_relaxed_sys(&ph->entry.geom);
-        const uint64_t dn = ld_relaxed_sys(reinterpret_cast<const uint64_t*>(&ph->entry.dtype));
-        const uint64_t want_dn = (uint64_t)p.dtype | ((uint64_t)N << 32);
-        if (ne != E || ge != p.cap || dn != want_dn) st = ST_PROTOCOL;
-      }
-      if (st != ST_OK) {
-        s_status = st;
-        s_blame = j;
-        ok = 0;
-        break;
-      }
-      s_src[j] = reinterpret_cast<const T*>(reinterpret_cast<uint64_t>(p.base[j]) + in_off);
-      s_res[j] = reinterpret_cast<const float*>(reinterpret_cast<uint64_t>(p.base[j]) + res_off);
-    }
-    if (ok) {
-      uint64_t orbits = reinterpret_cast<uint64_t>(p.out[me]);
-      for (int j = 0; j < N; ++j)
-        orbits |= reinterpret_cast<uint64_t>(s_src[j]) | reinterpret_cast<uint64_t>(s_res[j]);
-      s_vec_ok = (orbits & 15u) == 0;
-    }
     if (blockIdx.x == 0) {
+      int ok = 1;
+      for (int j = 0; j < N; ++j) {
+        if (j == me) {
+          hdr->peer_in[j] = reinterpret_cast<uint64_t>(mybase) + p.in_off[me];
+          hdr->peer_res[j] = reinterpret_cast<uint64_t>(mybase) + p.res_off[me];
+          continue;
+        }
+        ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
+        uint32_t st = wait_flag(&ph->entry.flag, tag, &ph->poison, ctl, &hdr->err, s_t0,
+                                p.hard_timeout_ns, nullptr);
+        uint64_t in_off = 0, res_off = 0;
+        if (st == ST_OK) {
+          in_off = ld_relaxed_sys(&ph->entry.in_off);
+          res_off = ld_relaxed_sys(&ph->entry.res_off);
+          const uint64_t ne = ld_relaxed_sys(&ph->entry.nelems);
+          const uint64_t ge = ld_relaxed_sys(&ph->entry.geom);
+          const uint64_t dn = ld_relaxed_sys(reinterpret_cast<const uint64_t*>(&ph->entry.dtype));
+          const uint64_t want_dn = (uint64_t)p.dtype | ((uint64_t)N << 32);
+          if (ne != E || ge != p.cap || dn != want_dn) st = ST_PROTOCOL;
+        }
+        if (st != ST_OK) {
+          s_status = st;
+          s_blame = j;
+          ok = 0;
+          break;
+        }
+        hdr->peer_in[j] = reinterpret_cast<uint64_t>(p.base[j]) + in_off;
+        hdr->peer_res[j] = reinterpret_cast<uint64_t>(p.base[j]) + res_off;
+      }
+      if (ok) {
+        uint64_t orbits = reinterpret_cast<uint64_t>(p.out[me]);
+        for (int j = 0; j < N; ++j) orbits |= hdr->peer_in[j] | hdr->peer_res[j];
+        hdr->vec_ok = (orbits & 15u) == 0;
+        st_release_gpu(&hdr->go, mk_flag(tag, 1));
+      }
       ctl->tphase[1] = globaltimer_ns();
       hdr->dbg_t1 = ctl->tphase[1];
+    } else {
+      const uint32_t st = wait_go(hdr, mk_flag(tag, 1), s_t0, p.hard_timeout_ns);
+      if (st != ST_OK) s_status = st;
+    }
+    if (s_status == ST_OK) {
+      for (int j = 0; j < N; ++j) {
+        s_src[j] = reinterpret_cast<const T*>(ld_relaxed_gpu(&hdr->peer_in[j]));
+        s_res[j] = reinterpret_cast<const float*>(ld_relaxed_gpu(&hdr->peer_res[j]));
+      }
+      s_vec_ok = (int)ld_relaxed_sys32(&hdr->vec_ok);
     }
   }
   __syncthreads();
@@ -474,24 +504,33 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
     }
   }
 
-  // ---- 3. reduce-scatter -> all-gather barrier ----------------------------
+  // ---- 3. reduce-scatter -> all-gather barrier (CTA 0 polls, fans out) ---
   if (tid == 0 && s_status == ST_OK) {
-    uint32_t bits = 0;
-    for (int jj = 0; jj < N; ++jj) {
-      const int j = (me + jj) % N;
-      ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
-      uint32_t b = 0;
-      uint32_t st = wait_flag(&ph->rs_done, tag, j == me ? nullptr : &ph->poison, ctl,
-                              &hdr->err, s_t0, p.hard_timeout_ns, &b);
-      if (st != ST_OK) {
-        s_status = st;
-        s_blame = j;
-        break;
+    if (blockIdx.x == 0) {
+      uint32_t bits = 0;
+      for (int jj = 0; jj < N; ++jj) {
+        const int j = (me + jj) % N;
+        ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
+        uint32_t b = 0;
+        uint32_t st = wait_flag(&ph->rs_done, tag, j == me ? nullptr : &ph->poison, ctl,
+                                &hdr->err, s_t0, p.hard_timeout_ns, &b);
+        if (st != ST_OK) {
+          s_status = st;
+          s_blame = j;
+          break;
+        }
+        bits |= b;
       }
-      bits |= b;
+      if (s_status == ST_OK) {
+        hdr->peer_bits = bits;
+        st_release_gpu(&hdr->go, mk_flag(tag, 2));
+      }
+      ctl->tphase[3] = globaltimer_ns();
+    } else {
+      const uint32_t st = wait_go(hdr, mk_flag(tag, 2), s_t0, p.hard_timeout_ns);
+      if (st != ST_OK) s_status = st;
     }
-    if (s_status == ST_OK && (bits & kBitNonFinite)) s_status = ST_NUMERICAL;
-    if (blockIdx.x == 0) ctl->tphase[3] = globaltimer_ns();
+    if (s_status == ST_OK && (ld_relaxed_sys32(&hdr->peer_bits) & kBitNonFinite)) s_status = ST_NUMERICAL;
   }
   __syncthreads();
 
@@ -864,6 +903,59 @@ __global__ void __launch_bounds__(kThreads, 1) probe_pattern_kernel(float* c, co
   if (mode == 2 && acc == 123456.f) c[0] = acc;
 }
 
+// Fence-cost probe (diagnostic): c = a + b with remote b, load flavour LK
+// (0 L1::no_allocate, 1 default ld.global, 2 ld.global.nc), then per-CTA
+// stamps: [0] loop end (warp 0), [1] after bar.sync, [2] after gpu fence,
+// [3] after sys fence.
+template <int LK>
+__device__ __forceinline__ uint4 ld_kind(const float* p) {
+  if (LK == 0) return ld_stream(p);
+  if (LK == 1) return *reinterpret_cast<const uint4*>(p);
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+template <int LK>
+__global__ void __launch_bounds__(kThreads, 1) probe_fence_kernel(float* c, const float* a, const float* b,
+                                                                  uint64_t n, uint64_t* stamps) {
+  const uint64_t nv = n >> 2;
+  const uint64_t per = (nv + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = umin((uint64_t)blockIdx.x * per, nv), hi = umin(lo + per, nv);
+  constexpr int U = 8;
+  for (uint64_t v = lo + threadIdx.x; v < hi; v += (uint64_t)kThreads * U) {
+    uint4 ra[U], rb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = v + (uint64_t)u * kThreads;
+      const uint64_t ii = i < hi ? i : lo;
+      ra[u] = ld_kind<LK>(a + ii * 4);
+      rb[u] = ld_kind<LK>(b + ii * 4);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = v + (uint64_t)u * kThreads;
+      if (i < hi) {
+        uint4 r;
+        r.x = __float_as_uint(__uint_as_float(ra[u].x) + __uint_as_float(rb[u].x));
+        r.y = __float_as_uint(__uint_as_float(ra[u].y) + __uint_as_float(rb[u].y));
+        r.z = __float_as_uint(__uint_as_float(ra[u].z) + __uint_as_float(rb[u].z));
+        r.w = __float_as_uint(__uint_as_float(ra[u].w) + __uint_as_float(rb[u].w));
+        *reinterpret_cast<uint4*>(c + i * 4) = r;
+      }
+    }
+  }
+  uint64_t* st = stamps + blockIdx.x * 4;
+  if (threadIdx.x == 0) st[0] = globaltimer_ns();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st[1] = globaltimer_ns();
+    __threadfence();
+    st[2] = globaltimer_ns();
+    __threadfence_system();
+    st[3] = globaltimer_ns();
+  }
+}
+
 __global__ void snap_init_kernel(SnapHdr* h) {
   h->seq = 0;
   h->step = -1;
@@ -921,9 +1013,25 @@ int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
 }
-int real_ctas() { return g_ctas > 0 ? g_ctas : env_int("FTAR_CTAS", 32); }
+int real_ctas() { return g_ctas > 0 ? g_ctas : env_int("FTAR_CTAS", 64); }
 int rs_layout() { return env_int("FTAR_RS_LAYOUT", 0); }
 int diag_mode() { return env_int("FTAR_DIAG", 0); }
+
+// Host wait policy: pure spinning (pause) for the first 50 ms of a wait —
+// sleep_for() of a few us really sleeps ~50 us (timer slack), which would add
+// that much to every collective — then yield, then 100 us sleeps.
+inline void host_backoff(uint64_t it, double waited_s) {
+  if (waited_s < 0.05) {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  } else if (waited_s < 0.5) {
+    std::this_thread::yield();
+  } else {
+    std::this_thread::sleep_for(std::chrono::microseconds(100));
+  }
+  (void)it;
+}
 
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -1445,6 +1553,7 @@ int ftar_wait(ftar_ctx* c, double progress_timeout_s, int* detail) {
   const uint64_t tag = c->cur_tag;
   uint64_t last_prog = ~0ull;
   double last_change = now_s();
+  const double t_begin = last_change;
   bool aborted = false;
   double abort_t = 0;
   for (uint64_t it = 0;; ++it) {
@@ -1472,13 +1581,7 @@ int ftar_wait(ftar_ctx* c, double progress_timeout_s, int* detail) {
     if (aborted && t - abort_t > 60.0) {
       return fail(FTAR_ST_TIMEOUT, "kernel did not drain after abort");
     }
-    if (it < 2000) {
-#if defined(__x86_64__)
-      __builtin_ia32_pause();
-#endif
-    } else {
-      std::this_thread::sleep_for(std::chrono::microseconds(it < 20000 ? 5 : 100));
-    }
+    host_backoff(it, t - t_begin);
   }
 }
 
@@ -1491,6 +1594,7 @@ int ftar_wait_local(ftar_ctx** ctxs, int n, double progress_timeout_s, int* stat
   bool aborted[kMaxMembers] = {};
   bool fin[kMaxMembers] = {};
   double t0 = now_s();
+  const double t_begin = t0;
   for (int i = 0; i < n; ++i) {
     last_prog[i] = ~0ull;
     last_change[i] = t0;
@@ -1531,13 +1635,7 @@ int ftar_wait_local(ftar_ctx** ctxs, int n, double progress_timeout_s, int* stat
     }
     if (!left) return FTAR_OK;
     if (abort_t > 0 && t - abort_t > 60.0) return fail(FTAR_ST_TIMEOUT, "kernel did not drain after abort");
-    if (it < 2000) {
-#if defined(__x86_64__)
-      __builtin_ia32_pause();
-#endif
-    } else {
-      std::this_thread::sleep_for(std::chrono::microseconds(it < 20000 ? 5 : 100));
-    }
+    host_backoff(it, t - t_begin);
   }
 }
 
@@ -1575,6 +1673,18 @@ int ftar_debug_cta_times(ftar_ctx* c, uint64_t* rs_end, uint64_t* ag_end, int n)
   if (n >= 260) {  // caller wants the fence stamps too (rs_end[256..259])
     for (int i = 0; i < 4; ++i) rs_end[256 + i] = h.dbg_fence[i];
   }
+  return FTAR_OK;
+}
+
+int ftar_probe_fence(float* c, const float* a, const float* b, uint64_t n, int kind, int ctas, uint64_t* stamps,
+                     int device, void* stream) {
+  DeviceGuard dg(device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int g = std::max(1, ctas);
+  if (kind == 0) probe_fence_kernel<0><<<g, kThreads, 0, st>>>(c, a, b, n, stamps);
+  else if (kind == 1) probe_fence_kernel<1><<<g, kThreads, 0, st>>>(c, a, b, n, stamps);
+  else probe_fence_kernel<2><<<g, kThreads, 0, st>>>(c, a, b, n, stamps);
+  CK(cudaGetLastError());
   return FTAR_OK;
 }
 
@@ -1778,6 +1888,7 @@ int ftar_snap_wait(ftar_snap* s, double progress_timeout_s, int64_t* available) 
   const uint64_t tag = s->cur_tag;
   uint64_t last = ~0ull;
   double last_change = now_s();
+  const double t_begin = last_change;
   bool aborted = false;
   double abort_t = 0;
   for (uint64_t it = 0;; ++it) {
@@ -1802,13 +1913,7 @@ int ftar_snap_wait(ftar_snap* s, double progress_timeout_s, int64_t* available) 
       last_change = t;
     }
     if (aborted && t - abort_t > 60.0) return fail(FTAR_ST_TIMEOUT, "pull did not drain after abort");
-    if (it < 2000) {
-#if defined(__x86_64__)
-      __builtin_ia32_pause();
-#endif
-    } else {
-      std::this_thread::sleep_for(std::chrono::microseconds(it < 20000 ? 5 : 100));
-    }
+    host_backoff(it, t - t_begin);
   }
 }
 

@@ -66,6 +66,11 @@ struct alignas(128) ArenaHdr {
   uint64_t dbg_ag_end[256];               // per-CTA %globaltimer at end of all-gather
   uint64_t dbg_t1;                        // entry barrier passed (block 0)
   uint64_t dbg_fence[4];                  // last CTA: before/after the sys fence (RS, end)
+  alignas(128) uint64_t go;               // CTA 0 -> local CTAs: (tag << 8) | barrier passed
+  uint64_t peer_in[kMaxMembers];          // entry barrier result: member inputs (my VA)
+  uint64_t peer_res[kMaxMembers];         // and member result slices (my VA)
+  uint32_t peer_bits;                     // RS barrier: OR of members' rs_done bits
+  uint32_t vec_ok;
 };
 static_assert(sizeof(ArenaHdr) <= kHdrBytes, "header too large");
 
@@ -117,6 +122,16 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
 }
 __device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ uint64_t ld_relaxed_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;

@@ -26,6 +26,7 @@ from __future__ import annotations
 import ctypes as C
 import logging
 import os
+import struct
 import threading
 from dataclasses import dataclass, field
 
@@ -177,6 +178,11 @@ class _CudaView:
 
 
 _TYPESTR = {torch.float32: "<f4", torch.bfloat16: "<i2"}
+
+
+def _f32(x: float) -> float:
+    """Round to float32 (np.float32(x) semantics) without creating tensors."""
+    return struct.unpack("f", struct.pack("f", x))[0]
 
 
 def _stream_ptr(device: torch.device) -> int:
@@ -374,13 +380,18 @@ class RingGroup:
             pass
 
     def inflight_bound(self, in_dtype_bytes: int) -> tuple[int, int]:
-        """(bytes, CTAs) a single peer link can have outstanding per call."""
-        slice_e, ctas, threads = C.c_uint64(), C.c_int(), C.c_int()
-        _lib.lib.ftar_geometry(1, max(1, self.n), C.byref(slice_e), C.byref(ctas), C.byref(threads))
-        n = max(1, self.n)
-        unroll = 4 if n <= 2 else (2 if n <= 4 else 1)
-        per_thread = unroll * 8 * in_dtype_bytes
-        return ctas.value * threads.value * per_thread, ctas.value
+        """(bytes, CTAs) a single peer link can have outstanding per call:
+        CTAs x threads x one 4-element vector per unrolled load."""
+        key = (self.n, in_dtype_bytes)
+        cache = self.__dict__.setdefault("_bound_cache", {})
+        if key not in cache:
+            slice_e, ctas, threads = C.c_uint64(), C.c_int(), C.c_int()
+            _lib.lib.ftar_geometry(1, max(1, self.n), C.byref(slice_e), C.byref(ctas), C.byref(threads))
+            n = max(1, self.n)
+            vec_bytes = 4 * in_dtype_bytes
+            unroll = max(1, min(16, (16 * 16 // vec_bytes) // n))
+            cache[key] = (ctas.value * threads.value * unroll * vec_bytes, ctas.value)
+        return cache[key]
 
 
 # --------------------------------------------------------------- all-reduce
@@ -416,9 +427,8 @@ def ftar_all_reduce(group: RingGroup, buf: torch.Tensor, step: int, cfg: Pipelin
     if group.n > 1 and not group.links_ready():
         raise Recoverable(PEER_RESET, "ring links not established")
     flags = _lib.F_SCALE if scale is not None else 0
-    f_scale = float(torch.tensor(scale if scale is not None else 1.0, dtype=torch.float32))
-    nbytes_in = buf.element_size()
-    bound, ctas = group.inflight_bound(nbytes_in)
+    f_scale = _f32(scale) if scale is not None else 1.0
+    bound, ctas = group.inflight_bound(buf.element_size())
     try:
         if group._local:
             _local_all_reduce(group, buf, dst, code, cfg, f_scale, flags)
@@ -544,7 +554,7 @@ class LocalRing:
         code = _dtype_code(bufs[0])
         outs = outs if outs is not None else bufs
         flags = _lib.F_SCALE if scale is not None else 0
-        f_scale = float(torch.tensor(scale if scale is not None else 1.0, dtype=torch.float32))
+        f_scale = _f32(scale) if scale is not None else 1.0
         for g in groups:
             g._seq += 1
         ctxs = (C.c_void_p * n)(*[g.ctx for g in groups])
@@ -614,7 +624,7 @@ class DeviceRing:
         cfg = cfg or PipelineConfig()
         outs = outs if outs is not None else bufs
         flags = _lib.F_SCALE if scale is not None else 0
-        f_scale = float(torch.tensor(scale if scale is not None else 1.0, dtype=torch.float32))
+        f_scale = _f32(scale) if scale is not None else 1.0
         for i, c in enumerate(self.ctxs):
             rc = _lib.lib.ftar_allreduce_launch(c, bufs[i].data_ptr(), _dtype_code(bufs[i]), outs[i].data_ptr(),
                                                 bufs[i].numel(), cfg.chunk_bytes, cfg.max_in_flight, f_scale, flags,
