@@ -239,18 +239,17 @@ def run_single(args):
             "definition": "n*E*(in_bytes+4): every replica's bucket read once, every replica's fp32 result "
                           "written once; peak = MEASURED_PEAKS.json hbm_gbs (measured copy)",
             "avg_launch_ms": round(per_launch * 1e3, 4)}
-    # e2e through the public API with host buffers
+    # e2e through the public API with HOST buffers (the reference's call
+    # shape): LocalRing.all_reduce_host pipelines chunked H2D, the range
+    # all-reduce and D2H; every step moves the replicas' buckets in and the
+    # reduced buckets out over PCIe inside the timed region
     e2e = None
     if not args.no_e2e:
         hosts = [b.cpu().pin_memory() for b in bufs]
         hout = [torch.empty(elems, dtype=torch.float32).pin_memory() for _ in range(n)]
 
         def e2e_step():
-            for h, b in zip(hosts, bufs):
-                b.copy_(h, non_blocking=True)
-            ring.all_reduce(bufs, cfg, outs=outs, scale=scale)
-            for o, h in zip(outs, hout):
-                h.copy_(o, non_blocking=True)
+            ring.all_reduce_host(hosts, cfg, outs=hout, scale=scale, chunk_elems=args.host_chunk_elems)
 
         for _ in range(2):
             e2e_step()
@@ -258,7 +257,8 @@ def run_single(args):
         tot, _ = timed_loop(e2e_step, ke, stream, torch)
         e2e = {"value": round(busbw(elems * in_bytes, tot / ke, n), 3), "unit": "GB/s",
                "h2d_bytes_per_step": n * elems * in_bytes, "d2h_bytes_per_step": n * elems * 4,
-               "ms_per_step": round(tot / ke * 1e3, 3), "steps": ke}
+               "ms_per_step": round(tot / ke * 1e3, 3), "steps": ke,
+               "api": "LocalRing.all_reduce_host (pinned host buffers; chunked H2D/reduce/D2H pipeline)"}
     cpu = None if args.no_cpu_baseline else cpu_ring_rate(n, elems, seconds=args.cpu_seconds)
     line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4), "higher_is_better": True,
@@ -328,9 +328,7 @@ def run_multi(args, rank, world, local_rank):
         hout = torch.empty(elems, dtype=torch.float32).pin_memory()
 
         def e2e_step():
-            buf.copy_(host, non_blocking=True)
-            step()
-            hout.copy_(out, non_blocking=True)
+            ftar.ftar_all_reduce(group, host, 0, cfg, out=hout, scale=scale)
 
         for _ in range(2):
             e2e_step()
@@ -342,7 +340,9 @@ def run_multi(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = {"value": round(busbw(elems * in_bytes, t.item() / ke, n), 3), "unit": "GB/s",
                "h2d_bytes_per_step": elems * in_bytes, "d2h_bytes_per_step": elems * 4,
-               "ms_per_step": round(t.item() / ke * 1e3, 3), "steps": ke, "per": "rank (each GPU its own PCIe)"}
+               "ms_per_step": round(t.item() / ke * 1e3, 3), "steps": ke,
+               "per": "rank (each GPU its own PCIe)",
+               "api": "ftar_all_reduce(group, pinned host tensor, out=host tensor): chunked H2D/reduce/D2H"}
     nccl = None
     if not args.no_nccl:
         nccl = nccl_busbw(args, n, elems, tdtype, dev, stream)
@@ -408,6 +408,7 @@ def main():
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch, if captured")
     ap.add_argument("--inplace", action="store_true", help="reduce fp32 buckets in place (reference API shape)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--host-chunk-elems", type=int, default=8 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     args = ap.parse_args()

@@ -110,6 +110,15 @@ int ftar_allreduce_launch(ftar_ctx* ctx, const void* in, int in_dtype, float* ou
                           uint64_t n_elems, uint64_t chunk_bytes, int max_in_flight,
                           float scale, uint32_t flags, void* stream);
 
+/* Range form: reduce elements [base_elem, base_elem + n_elems) of a bucket of
+ * `total_elems` elements, folding with the WHOLE bucket's partition geometry
+ * (so a bucket reduced chunk by chunk — e.g. pipelined with host copies — is
+ * bit-identical to one call).  in/out point at element base_elem. */
+int ftar_allreduce_launch_range(ftar_ctx* ctx, const void* in, int in_dtype, float* out,
+                                uint64_t n_elems, uint64_t base_elem, uint64_t total_elems,
+                                uint64_t chunk_bytes, int max_in_flight, float scale,
+                                uint32_t flags, void* stream);
+
 /* In-process ring: all `n` members live on ONE device and are driven by one
  * cooperative launch (the members' kernels wait on one another, so they
  * must be co-resident).  ctxs[i] is the member at ring index i.
@@ -121,6 +130,13 @@ int ftar_local_allreduce_launch(ftar_ctx** ctxs, int n, const void* const* ins,
                                 uint64_t chunk_bytes, int max_in_flight, float scale,
                                 uint32_t flags, uint32_t contrib_mask,
                                 int fault_member, int fault_after_tiles, void* stream);
+
+int ftar_local_allreduce_launch_range(ftar_ctx** ctxs, int n, const void* const* ins,
+                                      int in_dtype, float* const* outs, uint64_t n_elems,
+                                      uint64_t base_elem, uint64_t total_elems,
+                                      uint64_t chunk_bytes, int max_in_flight, float scale,
+                                      uint32_t flags, uint32_t contrib_mask, int fault_member,
+                                      int fault_after_tiles, void* stream);
 
 /* Poll the op in flight: *status = FTAR_ST_PENDING while running, else the
  * final code; *progress = work tiles completed (the per-chunk completion

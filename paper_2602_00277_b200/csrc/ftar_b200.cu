@@ -57,6 +57,8 @@ struct LaunchParams {
   uint64_t slice;                // elements reduced per ring index (multiple of 8)
   uint64_t p_base, p_rem;        // partition lengths: p_rem of p_base+1, rest p_base
   uint64_t cap;                  // partition cap (elements), validated across members
+  uint64_t ebase;                // element index of this call's element 0 in the bucket
+  uint64_t total;                // bucket length (geometry)
   uint64_t hard_timeout_ns;
   float scale;
   uint32_t flags;
@@ -125,8 +127,10 @@ __device__ uint32_t wait_go(const ArenaHdr* hdr, uint64_t want, uint64_t t0, uin
 // Owner (segment index) of element e under the reference geometry
 // (build_partition_plan ftar.py:80-99 + segment_bounds ftar.py:102-112), and
 // the element index where that segment ends.
-__device__ __forceinline__ void owner_of(uint64_t e, const LaunchParams& p, int n,
-                                         int& owner, uint64_t& seg_end) {
+__device__ __forceinline__ void owner_of(uint64_t e_local, const LaunchParams& p, int n,
+                                         int& owner, uint64_t& seg_end_local) {
+  const uint64_t e = e_local + p.ebase;  // range calls fold with the whole bucket's geometry
+  uint64_t seg_end;
   const uint64_t big = p.p_rem * (p.p_base + 1);
   uint64_t poff, L;
   if (e < big) {
@@ -151,6 +155,7 @@ __device__ __forceinline__ void owner_of(uint64_t e, const LaunchParams& p, int 
   }
   owner = (int)j;
   seg_end = poff + send;
+  seg_end_local = seg_end - p.ebase;
 }
 
 // Where folded values go: one fp32 array (result region or output), two
@@ -389,6 +394,8 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         en->geom = p.cap;
         en->dtype = p.dtype;
         en->n = (uint32_t)N;
+        en->ebase = p.ebase;
+        en->total = p.total;
         __threadfence_system();
         st_release_sys(&en->flag, mk_flag(tag, 0));
       }
@@ -417,7 +424,8 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
           const uint64_t ge = ld_relaxed_sys(&ph->entry.geom);
           const uint64_t dn = ld_relaxed_sys(reinterpret_cast<const uint64_t*>(&ph->entry.dtype));
           const uint64_t want_dn = (uint64_t)p.dtype | ((uint64_t)N << 32);
-          if (ne != E || ge != p.cap || dn != want_dn) st = ST_PROTOCOL;
+          const uint64_t eb = ld_relaxed_sys(&ph->entry.ebase), et = ld_relaxed_sys(&ph->entry.total);
+          if (ne != E || ge != p.cap || dn != want_dn || eb != p.ebase || et != p.total) st = ST_PROTOCOL;
         }
         if (st != ST_OK) {
           s_status = st;
@@ -745,6 +753,7 @@ struct LocalParams {
   uint64_t tag[kMaxMembers];
   uint64_t nelems;
   uint64_t p_base, p_rem;
+  uint64_t ebase;
   float scale;
   uint32_t flags_in;
   uint32_t contrib;
@@ -769,6 +778,7 @@ __global__ void __launch_bounds__(kThreads, 1) local_oneshot_kernel(const __grid
   LaunchParams g{};
   g.p_base = p.p_base;
   g.p_rem = p.p_rem;
+  g.ebase = p.ebase;
   uint64_t orbits = reinterpret_cast<uint64_t>(p.stage);
   for (int j = 0; j < N; ++j) orbits |= reinterpret_cast<uint64_t>(p.in[j]) | reinterpret_cast<uint64_t>(p.out[j]);
   const bool vec_ok = (orbits & 15u) == 0;
@@ -1137,18 +1147,23 @@ int oneshot_blocks_per_sm(int n) {
   return e == cudaSuccess ? nb : 0;
 }
 
-// Reference geometry (elements; ELEM = 4 bytes of the fp32 view).
-void fill_geometry(LaunchParams& p, uint64_t E, uint64_t chunk_bytes, int C, int n) {
+// Reference geometry (elements; ELEM = 4 bytes of the fp32 view), built on
+// the whole bucket (`total`); this call covers [ebase, ebase + E).
+void fill_geometry(LaunchParams& p, uint64_t E, uint64_t chunk_bytes, int C, int n, uint64_t ebase = 0,
+                   uint64_t total = ~0ull) {
+  if (total == ~0ull) total = E;
   uint64_t cap = (chunk_bytes * (uint64_t)C * (uint64_t)n) / 4;
   if (cap < 1) cap = 1;
   p.cap = cap;
-  if (E == 0) {
+  p.ebase = ebase;
+  p.total = total;
+  if (total == 0) {
     p.p_base = 1;
     p.p_rem = 0;
   } else {
-    const uint64_t nparts = (E + cap - 1) / cap;
-    p.p_base = E / nparts;
-    p.p_rem = E % nparts;
+    const uint64_t nparts = (total + cap - 1) / cap;
+    p.p_base = total / nparts;
+    p.p_rem = total % nparts;
   }
   const uint64_t per = (E + (uint64_t)n - 1) / (uint64_t)n;
   p.slice = (per + 7) & ~7ull;
@@ -1349,9 +1364,10 @@ int ftar_geometry(uint64_t n_elems, int n, uint64_t* slice_elems, int* ctas, int
   return FTAR_OK;
 }
 
-int ftar_allreduce_launch(ftar_ctx* c, const void* in, int in_dtype, float* out, uint64_t n_elems,
-                          uint64_t chunk_bytes, int max_in_flight, float scale, uint32_t flags,
-                          void* stream) {
+int ftar_allreduce_launch_range(ftar_ctx* c, const void* in, int in_dtype, float* out, uint64_t n_elems,
+                                uint64_t base_elem, uint64_t total_elems, uint64_t chunk_bytes,
+                                int max_in_flight, float scale, uint32_t flags, void* stream) {
+  if (base_elem + n_elems > total_elems) return fail(FTAR_ST_INVARIANT, "range exceeds the bucket");
   if (!c) return fail(FTAR_ST_INVARIANT, "null ctx");
   int v = validate_common(in_dtype, c->n, chunk_bytes, max_in_flight);
   if (v) return v;
@@ -1379,7 +1395,7 @@ int ftar_allreduce_launch(ftar_ctx* c, const void* in, int in_dtype, float* out,
     in_off = so;
   }
   LaunchParams p{};
-  fill_geometry(p, n_elems, chunk_bytes, max_in_flight, c->n);
+  fill_geometry(p, n_elems, chunk_bytes, max_in_flight, c->n, base_elem, total_elems);
   for (int i = 0; i < c->n; ++i) p.base[i] = (i == c->self) ? c->arena : c->peer[c->ring_slots[i]];
   p.ctl[c->self] = c->ctl_d;
   p.out[c->self] = out;
@@ -1419,10 +1435,12 @@ int ftar_allreduce_launch(ftar_ctx* c, const void* in, int in_dtype, float* out,
   return FTAR_OK;
 }
 
-int ftar_local_allreduce_launch(ftar_ctx** ctxs, int n, const void* const* ins, int in_dtype,
-                                float* const* outs, uint64_t n_elems, uint64_t chunk_bytes,
-                                int max_in_flight, float scale, uint32_t flags, uint32_t contrib_mask,
-                                int fault_member, int fault_after_tiles, void* stream) {
+int ftar_local_allreduce_launch_range(ftar_ctx** ctxs, int n, const void* const* ins, int in_dtype,
+                                      float* const* outs, uint64_t n_elems, uint64_t base_elem,
+                                      uint64_t total_elems, uint64_t chunk_bytes, int max_in_flight,
+                                      float scale, uint32_t flags, uint32_t contrib_mask, int fault_member,
+                                      int fault_after_tiles, void* stream) {
+  if (base_elem + n_elems > total_elems) return fail(FTAR_ST_INVARIANT, "range exceeds the bucket");
   int v = validate_common(in_dtype, n, chunk_bytes, max_in_flight);
   if (v) return v;
   if (!ctxs || !ins || !outs) return fail(FTAR_ST_INVARIANT, "null arrays");
@@ -1440,7 +1458,7 @@ int ftar_local_allreduce_launch(ftar_ctx** ctxs, int n, const void* const* ins, 
   DeviceGuard g(dev);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   LaunchParams p{};
-  fill_geometry(p, n_elems, chunk_bytes, max_in_flight, n);
+  fill_geometry(p, n_elems, chunk_bytes, max_in_flight, n, base_elem, total_elems);
   uint64_t tag = 0;
   for (int i = 0; i < n; ++i) {
     ftar_ctx* c = ctxs[i];
@@ -1503,6 +1521,7 @@ int ftar_local_allreduce_launch(ftar_ctx** ctxs, int n, const void* const* ins, 
     lp.nelems = n_elems;
     lp.p_base = p.p_base;
     lp.p_rem = p.p_rem;
+    lp.ebase = p.ebase;
     lp.scale = scale;
     lp.flags_in = flags;
     lp.contrib = p.contrib;
@@ -1528,6 +1547,22 @@ int ftar_local_allreduce_launch(ftar_ctx** ctxs, int n, const void* const* ins, 
     return cuda_fail(e, "local allreduce cooperative launch");
   }
   return FTAR_OK;
+}
+
+int ftar_allreduce_launch(ftar_ctx* c, const void* in, int in_dtype, float* out, uint64_t n_elems,
+                          uint64_t chunk_bytes, int max_in_flight, float scale, uint32_t flags,
+                          void* stream) {
+  return ftar_allreduce_launch_range(c, in, in_dtype, out, n_elems, 0, n_elems, chunk_bytes, max_in_flight,
+                                     scale, flags, stream);
+}
+
+int ftar_local_allreduce_launch(ftar_ctx** ctxs, int n, const void* const* ins, int in_dtype,
+                                float* const* outs, uint64_t n_elems, uint64_t chunk_bytes,
+                                int max_in_flight, float scale, uint32_t flags, uint32_t contrib_mask,
+                                int fault_member, int fault_after_tiles, void* stream) {
+  return ftar_local_allreduce_launch_range(ctxs, n, ins, in_dtype, outs, n_elems, 0, n_elems, chunk_bytes,
+                                           max_in_flight, scale, flags, contrib_mask, fault_member,
+                                           fault_after_tiles, stream);
 }
 
 int ftar_poll(ftar_ctx* c, int* status, uint64_t* progress) {

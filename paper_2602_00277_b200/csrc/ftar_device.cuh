@@ -49,6 +49,8 @@ struct alignas(128) EntryRec {
   uint64_t geom;       // partition cap (elements) the member folds with
   uint32_t dtype;
   uint32_t n;
+  uint64_t ebase;      // range calls: first element of this call in the bucket
+  uint64_t total;      // range calls: bucket length the geometry is built on
 };
 
 struct alignas(128) ArenaHdr {

@@ -423,6 +423,8 @@ def ftar_all_reduce(group: RingGroup, buf: torch.Tensor, step: int, cfg: Pipelin
     ``scale`` multiplies the fp32 sum by f32(scale) in the same pass.  On a
     Recoverable error the links are closed and nothing has been written."""
     cfg = cfg or PipelineConfig()
+    if not (isinstance(buf, torch.Tensor) and buf.is_cuda):
+        return _host_all_reduce(group, buf, step, cfg, out, scale)
     code, dst = _check_buffers(buf, out)
     if group.n > 1 and not group.links_ready():
         raise Recoverable(PEER_RESET, "ring links not established")
@@ -440,6 +442,52 @@ def ftar_all_reduce(group: RingGroup, buf: torch.Tensor, step: int, cfg: Pipelin
     group.meter.sent(bound, ctas)
     group.meter.acked(bound, ctas)
     return dst
+
+
+def _host_all_reduce(group, buf, step, cfg, out, scale):
+    """Host (numpy / CPU tensor) buffers: the reference's exact call shape.
+    One process per GPU: chunked H2D / range all-reduce / D2H pipeline.
+    In-process (threaded) rings: stage through the device whole."""
+    host = _as_host_tensor(buf)
+    if host.dtype not in (torch.float32, torch.bfloat16):
+        raise Fatal(INTERNAL_INVARIANT, "all-reduce buffer must be contiguous float32")
+    if out is None and host.dtype != torch.float32:
+        raise Fatal(INTERNAL_INVARIANT, "all-reduce buffer must be contiguous float32 (pass out= for bf16)")
+    hout = _as_host_tensor(out) if out is not None else None
+    if group.n > 1 and not group.links_ready():
+        raise Recoverable(PEER_RESET, "ring links not established")
+    if group._local:
+        dev = host.to(group.device)
+        dres = torch.empty(host.numel(), device=group.device) if out is not None else None
+        ftar_all_reduce(group, dev, step, cfg, out=dres, scale=scale)
+        (hout if hout is not None else host).copy_((dres if dres is not None else dev).cpu())
+        return out if out is not None else buf
+    pipe = group.__dict__.get("_pipe")
+    if pipe is None or pipe.key != (1, host.dtype, 8 << 20):
+        pipe = group._pipe = _HostPipeline(group.device, 1, host.dtype, 8 << 20)
+    flags = _lib.F_SCALE if scale is not None else 0
+    f_scale = _f32(scale) if scale is not None else 1.0
+    code = _dtype_code(host)
+
+    def launch(dins, douts, base, total):
+        rc = _lib.lib.ftar_allreduce_launch_range(group.ctx, dins[0].data_ptr(), code, douts[0].data_ptr(),
+                                                  dins[0].numel(), base, total, cfg.chunk_bytes, cfg.max_in_flight,
+                                                  f_scale, flags, _stream_ptr(group.device))
+        _lib.check(rc, "ftar_allreduce_launch_range")
+        return None
+
+    def wait(_tok):
+        det = C.c_int(-1)
+        st = _lib.lib.ftar_wait(group.ctx, cfg.per_chunk_timeout_s, C.byref(det))
+        if st:
+            raise from_status(st, _lib.last_error() if st == 10 else "")
+
+    try:
+        pipe.run([host], [hout] if hout is not None else None, launch, wait)
+    except FtdpError:
+        group.close_links()
+        raise
+    return out if out is not None else buf
 
 
 def _remote_all_reduce(group, buf, dst, code, cfg, f_scale, flags):
@@ -499,6 +547,86 @@ def _local_all_reduce(group, buf, dst, code, cfg, f_scale, flags):
         raise from_status(st, f"peer replica {blame}" if blame is not None else "")
 
 
+def _as_host_tensor(b) -> torch.Tensor:
+    if isinstance(b, torch.Tensor):
+        if b.is_cuda:
+            raise Fatal(INTERNAL_INVARIANT, "expected a host buffer")
+        return b
+    import numpy as np
+    if isinstance(b, np.ndarray):
+        if not b.flags.c_contiguous:
+            raise Fatal(INTERNAL_INVARIANT, "all-reduce buffer must be contiguous float32")
+        return torch.from_numpy(b)
+    raise Fatal(INTERNAL_INVARIANT, "all-reduce buffer must be a tensor or numpy array")
+
+
+class _HostPipeline:
+    """Double-buffered device staging for host-buffer all-reduces: chunk c+1
+    is copied in while chunk c is reduced and chunk c-1 is copied out."""
+
+    def __init__(self, device: torch.device, n: int, dtype: torch.dtype, chunk_elems: int):
+        self.key = (n, dtype, chunk_elems)
+        self.device = device
+        self.chunk = chunk_elems
+        self.din = [[torch.empty(chunk_elems, dtype=dtype, device=device) for _ in range(n)] for _ in range(2)]
+        self.dout = [[torch.empty(chunk_elems, dtype=torch.float32, device=device) for _ in range(n)]
+                     for _ in range(2)]
+        self.h2d = torch.cuda.Stream(device=device)
+        self.d2h = torch.cuda.Stream(device=device)
+        self.staging = None
+
+    def run(self, hosts, outs, launch, wait):
+        n = len(hosts)
+        total = hosts[0].numel()
+        inplace = outs is None
+        if inplace:
+            if hosts[0].dtype != torch.float32:
+                raise Fatal(INTERNAL_INVARIANT, "in-place host all-reduce needs float32 (pass outs=)")
+            if self.staging is None or self.staging[0].numel() < total or len(self.staging) != n:
+                self.staging = [torch.empty(total, dtype=torch.float32).pin_memory() for _ in range(n)]
+            dsts = [t[:total] for t in self.staging]
+        else:
+            dsts = outs
+        comp = torch.cuda.current_stream(self.device)
+        nchunks = max(1, -(-total // self.chunk))
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_comp = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [None, None]
+
+        def stage_in(c):
+            slot, off = c % 2, c * self.chunk
+            ln = min(self.chunk, total - off)
+            with torch.cuda.stream(self.h2d):
+                for i in range(n):
+                    self.din[slot][i][:ln].copy_(hosts[i][off:off + ln], non_blocking=True)
+                ev_in[slot].record(self.h2d)
+
+        stage_in(0)
+        for c in range(nchunks):
+            slot, off = c % 2, c * self.chunk
+            ln = min(self.chunk, total - off)
+            comp.wait_event(ev_in[slot])
+            if ev_out[slot] is not None:
+                comp.wait_event(ev_out[slot])
+            tok = launch([t[:ln] for t in self.din[slot]], [t[:ln] for t in self.dout[slot]], off, total)
+            ev_comp[slot].record(comp)
+            if c + 1 < nchunks:
+                stage_in(c + 1)  # overlaps the reduction of chunk c
+            wait(tok)            # one collective in flight per ring group
+            with torch.cuda.stream(self.d2h):
+                self.d2h.wait_event(ev_comp[slot])
+                for i in range(n):
+                    dsts[i][off:off + ln].copy_(self.dout[slot][i][:ln], non_blocking=True)
+                ev_out[slot] = torch.cuda.Event()
+                ev_out[slot].record(self.d2h)
+        self.d2h.synchronize()
+        if inplace:
+            for h, st in zip(hosts, dsts):
+                h.copy_(st)
+            return hosts
+        return outs
+
+
 def _local_protocol() -> bool:
     """In-process rings run the one-shot kernel unless FTAR_LOCAL_MODE=protocol
     asks for the two-shot flag protocol (what one GPU per member runs)."""
@@ -545,8 +673,10 @@ class LocalRing:
             errs.append(exc)
 
     def launch(self, bufs, cfg: PipelineConfig | None = None, outs=None, scale=None, members=None,
-               fault=None):
-        """Launch one all-reduce over `members` (default all) without waiting."""
+               fault=None, base: int = 0, total: int | None = None):
+        """Launch one all-reduce over `members` (default all) without waiting.
+        With base/total the buffers hold elements [base, base+len) of a bucket
+        of `total` elements and fold with that bucket's geometry."""
         cfg = cfg or PipelineConfig()
         members = sorted(members if members is not None else range(self.n))
         groups = [self.groups[m] for m in members]
@@ -563,9 +693,11 @@ class LocalRing:
         fm, fa = (-1, 0) if fault is None else fault
         if self.protocol or fault is not None:
             flags |= _lib.F_PROTOCOL
-        rc = _lib.lib.ftar_local_allreduce_launch(ctxs, n, ins, code, ous, bufs[0].numel(), cfg.chunk_bytes,
-                                                  cfg.max_in_flight, f_scale, flags, groups[0]._contrib_mask,
-                                                  fm, fa, _stream_ptr(groups[0].device))
+        ln = bufs[0].numel()
+        rc = _lib.lib.ftar_local_allreduce_launch_range(ctxs, n, ins, code, ous, ln, base,
+                                                        ln + base if total is None else total, cfg.chunk_bytes,
+                                                        cfg.max_in_flight, f_scale, flags, groups[0]._contrib_mask,
+                                                        fm, fa, _stream_ptr(groups[0].device))
         _lib.check(rc, "ftar_local_allreduce_launch")
         return ctxs
 
@@ -583,6 +715,30 @@ class LocalRing:
             if st:
                 raise from_status(st)
         return outs if outs is not None else bufs
+
+    def all_reduce_host(self, host_bufs, cfg: PipelineConfig | None = None, outs=None, scale=None,
+                        chunk_elems: int = 8 << 20):
+        """The reference call shape with HOST buffers (bench._LoopbackRing
+        .timed_all_reduce on numpy arrays): chunked H2D -> range all-reduce ->
+        D2H, pipelined on three streams so both PCIe directions and the
+        kernel overlap.  outs (fp32 host) default to the inputs (in place:
+        results are committed only once every chunk succeeded)."""
+        cfg = cfg or PipelineConfig()
+        hosts = [_as_host_tensor(b) for b in host_bufs]
+        n = len(hosts)
+        pipe = self.__dict__.get("_pipe")
+        if pipe is None or pipe.key != (n, hosts[0].dtype, chunk_elems):
+            pipe = self._pipe = _HostPipeline(self.groups[0].device, n, hosts[0].dtype, chunk_elems)
+
+        def launch(dins, douts, base, total):
+            return self.launch(dins, cfg, outs=douts, scale=scale, base=base, total=total)
+
+        def wait(tok):
+            for st in self.wait(tok, cfg):
+                if st:
+                    raise from_status(st)
+
+        return pipe.run(hosts, [_as_host_tensor(o) for o in outs] if outs is not None else None, launch, wait)
 
     def close(self):
         for g in self.groups:

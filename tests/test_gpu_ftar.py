@@ -415,3 +415,61 @@ def test_registered_pool_zero_copy(ftar):
     finally:
         for g in gs:
             g.close()
+
+
+# ---------------------------------------------------------------------------
+# Host buffers (the reference's numpy call shape) and range launches.
+
+
+@pytest.mark.parametrize("mode", ["protocol", "oneshot"])
+def test_host_pipeline_chunks_fold_with_whole_bucket_geometry(ftar, rings, mode):
+    """Chunked H2D/reduce/D2H: chunk boundaries cut partitions and segments,
+    yet every element folds as in one whole-bucket call."""
+    n, e = 3, 1_000_003
+    arrays = member_inputs(n, e, seed=21)
+    ring = rings(n, protocol=(mode == "protocol"))
+    ring.reconfig()
+    cfg = ftar.PipelineConfig(chunk_bytes=40_000, max_in_flight=3)  # 90k-element partitions
+    want = orc.oracle_reduce(arrays, cfg.chunk_bytes, cfg.max_in_flight)
+    hosts = [torch.from_numpy(a.copy()).pin_memory() for a in arrays]
+    outs = [torch.empty(e).pin_memory() for _ in range(n)]
+    ring.all_reduce_host(hosts, cfg, outs=outs, chunk_elems=77_777)
+    for o in outs:
+        np.testing.assert_array_equal(o.numpy(), want)
+    # in place, numpy arrays, fused scale
+    bufs = [a.copy() for a in arrays]
+    ring.all_reduce_host(bufs, cfg, scale=1.0 / n, chunk_elems=300_000)
+    for b in bufs:
+        np.testing.assert_array_equal(b, orc.normalize(want, n))
+
+
+def test_host_pipeline_bf16_to_f32(ftar, rings):
+    n, e = 4, 2_000_001
+    arrays = member_inputs(n, e, seed=22, dtype="bf16")
+    ring = rings(n, protocol=False)
+    ring.reconfig()
+    hosts = [torch.from_numpy(a).to(torch.bfloat16).pin_memory() for a in arrays]
+    outs = [torch.empty(e).pin_memory() for _ in range(n)]
+    ring.all_reduce_host(hosts, outs=outs, chunk_elems=1 << 19)
+    want = orc.oracle_reduce(arrays, 8 << 20, 4)
+    for o in outs:
+        np.testing.assert_array_equal(o.numpy(), want)
+
+
+def test_dropin_numpy_buffers_threaded(ftar):
+    """ftar_all_reduce on numpy arrays, members on threads: the reference's
+    tests/test_ftar.py run_case shape, unchanged."""
+    ring = Ring(ftar, 3)
+    try:
+        ring.reconfig()
+        cfg = ftar.PipelineConfig(chunk_bytes=28, max_in_flight=2)
+        rng = np.random.default_rng(42)
+        arrays = [rng.standard_normal(2049).astype(np.float32) for _ in range(3)]
+        bufs = {r: arrays[r].copy() for r in range(3)}
+        res = ring.all_reduce(bufs, 1, cfg, [0, 1, 2])
+        want = orc.oracle_reduce(arrays, cfg.chunk_bytes, cfg.max_in_flight)
+        for r in range(3):
+            assert res[r] is bufs[r]
+            np.testing.assert_array_equal(bufs[r], want)
+    finally:
+        ring.close()

@@ -122,6 +122,23 @@ def _worker(rank, world, port, scenario, outdir):
                 want = orc.normalize(orc.oracle_reduce([arrays[r] for r in d2.members], cfg.chunk_bytes,
                                                        cfg.max_in_flight), len(d2.healthy))
                 (res["ok"] if np.array_equal(out.cpu().numpy(), want) else res["errors"]).append("retry")
+        elif scenario == "host":
+            # the reference's call shape: numpy buffers in, reduced in place;
+            # chunked H2D / range all-reduce / D2H pipeline (bit-exact)
+            group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, 1, deadline_s=30)
+            e = 20_000_003
+            arrays = member_inputs(world, e, seed=31)
+            cfg = ftar.PipelineConfig(chunk_bytes=1 << 20, max_in_flight=3)
+            want = orc.oracle_reduce(arrays, cfg.chunk_bytes, cfg.max_in_flight)
+            buf = arrays[rank].copy()
+            assert ftar.ftar_all_reduce(group, buf, 1, cfg) is buf
+            (res["ok"] if np.array_equal(buf, want) else res["errors"]).append("host_inplace")
+            hb = torch.from_numpy(arrays[rank]).to(torch.bfloat16).pin_memory()
+            ho = torch.empty(e).pin_memory()
+            arrays16 = [torch.from_numpy(a).to(torch.bfloat16).float().numpy() for a in arrays]
+            ftar.ftar_all_reduce(group, hb, 2, cfg, out=ho, scale=1.0 / world)
+            want16 = orc.normalize(orc.oracle_reduce(arrays16, cfg.chunk_bytes, cfg.max_in_flight), world)
+            (res["ok"] if np.array_equal(ho.numpy(), want16) else res["errors"]).append("host_bf16")
         elif scenario == "catchup":
             from paper_2602_00277_b200 import checkpoint as ck
             snap = ck.SnapshotStore(capacity_bytes=64 << 20, device=dev, fabric=fabric, rank=0, replica_id=rank)
@@ -190,6 +207,13 @@ def test_member_failure_requorum_and_retry():
     survivors = [r for r in res if "victim" not in r["ok"]]
     assert all(any(x.startswith("recoverable") for x in r["ok"]) for r in survivors)
     assert all("retry" in r["ok"] for r in survivors)
+
+
+def test_host_buffers_over_nvlink():
+    res = run("host", world_size())
+    for r in res:
+        assert not r["errors"], r["errors"]
+        assert "host_inplace" in r["ok"] and "host_bf16" in r["ok"]
 
 
 def test_catchup_pull_over_nvlink():
