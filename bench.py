@@ -36,6 +36,22 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+
+class _StdoutToStderr:
+    """Rank 0's stdout must be exactly one JSON line: route fd 1 to stderr
+    while NCCL initialises (its version banner is printed from C)."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
 MIB = 1024 * 1024
 NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md measured peer copy per direction (fallback; 900 nominal)
 NVLINK_NOMINAL_GBS = 900.0
@@ -188,7 +204,7 @@ def workload_config(args, n):
             "parallelism": f"dp{n}" + (" (emulated)" if emu else "")}
 
 
-def timed_loop(fn, steps, stream, torch):
+def timed_loop(fn, steps, stream, torch, drain=None):
     """Run fn() `steps` times; CUDA events per launch and around the loop."""
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -197,6 +213,8 @@ def timed_loop(fn, steps, stream, torch):
         ev[i][0].record(stream)
         fn()
         ev[i][1].record(stream)
+    if drain is not None:
+        drain()
     t_end.record(stream)
     torch.cuda.synchronize()
     per = [a.elapsed_time(b) for a, b in ev]
@@ -296,15 +314,27 @@ def run_multi(args, rank, world, local_rank):
     scale = 1.0 / n
     stream = torch.cuda.current_stream(dev)
 
+    # buckets are enqueued asynchronously (queue depth args.depth), the way a
+    # bucketed backward pass issues them; every step is still one complete
+    # all-reduce of the whole bucket and all of them finish inside the region
+    pend = []
+
     def step():
-        ftar.ftar_all_reduce(group, buf, 0, cfg, out=None if out is buf else out, scale=scale)
+        pend.append(ftar.ftar_all_reduce_async(group, buf, 0, cfg, out=None if out is buf else out, scale=scale))
+        while len(pend) >= args.depth:
+            pend.pop(0).wait()
+
+    def drain():
+        while pend:
+            pend.pop(0).wait()
 
     for _ in range(args.warmup):
         step()
+    drain()
     torch.cuda.synchronize()
     dist.barrier()
     with ClockSampler(local_rank) as clk:
-        total, per_launch = timed_loop(step, args.steps, stream, torch)
+        total, per_launch = timed_loop(step, args.steps, stream, torch, drain)
     dist.barrier()
     phases = phase_us(group)
     tt = torch.tensor([total, per_launch], dtype=torch.float64)
@@ -379,11 +409,12 @@ def nccl_busbw(args, n, elems, tdtype, dev, stream):
     import torch
     import torch.distributed as dist
     try:
-        pg = dist.new_group(backend="nccl")
-        x = torch.randn(elems, device=dev).to(tdtype)
-        for _ in range(max(2, args.warmup)):
-            dist.all_reduce(x, group=pg)
-        torch.cuda.synchronize()
+        with _StdoutToStderr():
+            pg = dist.new_group(backend="nccl")
+            x = torch.randn(elems, device=dev).to(tdtype)
+            for _ in range(max(2, args.warmup)):
+                dist.all_reduce(x, group=pg)
+            torch.cuda.synchronize()
         dist.barrier()
         total, _ = timed_loop(lambda: dist.all_reduce(x, group=pg), args.steps, stream, torch)
         t = torch.tensor([total], dtype=torch.float64)
@@ -407,6 +438,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch, if captured")
     ap.add_argument("--inplace", action="store_true", help="reduce fp32 buckets in place (reference API shape)")
+    ap.add_argument("--depth", type=int, default=3, help="queued all-reduces per rank (1 = blocking)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-chunk-elems", type=int, default=8 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")

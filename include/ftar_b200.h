@@ -142,9 +142,14 @@ int ftar_local_allreduce_launch_range(ftar_ctx** ctxs, int n, const void* const*
  * final code; *progress = work tiles completed (the per-chunk completion
  * counter the CPU polls, cf. _recv_chunk deadlines ftar.py:378-398). */
 int ftar_poll(ftar_ctx* ctx, int* status, uint64_t* progress);
-/* Set the abort word: the kernel drains and reports FTAR_ST_ABORTED. */
+/* Set the abort word of every queued collective: kernels drain and report
+ * FTAR_ST_ABORTED. */
 int ftar_abort(ftar_ctx* ctx);
-/* Block (GIL-free when called via ctypes) until done.  If the kernel has
+/* Number of launched collectives not yet collected by ftar_wait (<= 4:
+ * callers may enqueue several buckets and wait for them in order). */
+int ftar_inflight(ftar_ctx* ctx);
+/* Block (GIL-free when called via ctypes) until the OLDEST queued
+ * collective is done.  If the kernel has
  * started and progress does not advance for `progress_timeout_s`, write the
  * abort word (per-chunk deadline semantics, ftar.py:382-386).  Returns the
  * final status; *detail receives the ring index of the peer blamed (or -1). */

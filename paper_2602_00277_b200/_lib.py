@@ -46,6 +46,7 @@ SIGNATURES = {
                                           i32, i32, vp]),
     "ftar_poll": (i32, [c_ctx_p, C.POINTER(i32), C.POINTER(u64)]),
     "ftar_abort": (i32, [c_ctx_p]),
+    "ftar_inflight": (i32, [c_ctx_p]),
     "ftar_wait": (i32, [c_ctx_p, dbl, C.POINTER(i32)]),
     "ftar_wait_local": (i32, [C.POINTER(c_ctx_p), i32, dbl, C.POINTER(i32), C.POINTER(i32)]),
     "ftar_geometry": (i32, [u64, i32, C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]),

@@ -124,6 +124,22 @@ __device__ uint32_t wait_go(const ArenaHdr* hdr, uint64_t want, uint64_t t0, uin
   }
 }
 
+// Direct mode: wait until CTA 0 has seen member k's slice reduced.
+__device__ uint32_t wait_go_bit(const ArenaHdr* hdr, uint64_t tag, int k, uint64_t t0, uint64_t limit_ns) {
+  for (uint32_t it = 0;; ++it) {
+    const uint64_t v = ld_relaxed_gpu(&hdr->go2);
+    if (flag_tag(v) == tag && ((v >> k) & 1u)) {
+      fence_acq_rel_gpu();
+      return ST_OK;
+    }
+    if ((it & 15u) == 15u) {
+      if (ld_relaxed_sys32(&hdr->err) != 0) return ST_FOLLOW;
+      if (globaltimer_ns() - t0 > limit_ns) return ST_TIMEOUT;
+    }
+    if (it > 4) __nanosleep(it < 64 ? 64 : 256);
+  }
+}
+
 // Owner (segment index) of element e under the reference geometry
 // (build_partition_plan ftar.py:80-99 + segment_bounds ftar.py:102-112), and
 // the element index where that segment ends.
@@ -513,10 +529,43 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
   }
 
   // ---- 3. reduce-scatter -> all-gather barrier (CTA 0 polls, fans out) ---
-  if (tid == 0 && s_status == ST_OK) {
-    if (blockIdx.x == 0) {
-      uint32_t bits = 0;
-      for (int jj = 0; jj < N; ++jj) {
+  // In-place calls: a full barrier (nothing is committed unless every slice
+  // is reduced and finite).  Out-of-place (direct) calls: `out` is scratch
+  // until success, so CTA 0 publishes members one by one (go2 mask) and each
+  // CTA pulls a slice as soon as its owner is done.
+  if (!direct) {
+    if (tid == 0 && s_status == ST_OK) {
+      if (blockIdx.x == 0) {
+        uint32_t bits = 0;
+        for (int jj = 0; jj < N; ++jj) {
+          const int j = (me + jj) % N;
+          ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
+          uint32_t b = 0;
+          uint32_t st = wait_flag(&ph->rs_done, tag, j == me ? nullptr : &ph->poison, ctl,
+                                  &hdr->err, s_t0, p.hard_timeout_ns, &b);
+          if (st != ST_OK) {
+            s_status = st;
+            s_blame = j;
+            break;
+          }
+          bits |= b;
+        }
+        if (s_status == ST_OK) {
+          hdr->peer_bits = bits;
+          st_release_gpu(&hdr->go, mk_flag(tag, 2));
+        }
+        ctl->tphase[3] = globaltimer_ns();
+      } else {
+        const uint32_t st = wait_go(hdr, mk_flag(tag, 2), s_t0, p.hard_timeout_ns);
+        if (st != ST_OK) s_status = st;
+      }
+      if (s_status == ST_OK && (ld_relaxed_sys32(&hdr->peer_bits) & kBitNonFinite)) s_status = ST_NUMERICAL;
+    }
+    __syncthreads();
+  } else if (blockIdx.x == 0) {
+    if (tid == 0 && s_status == ST_OK) {
+      uint32_t bits = 0, mask = 0;
+      for (int jj = 1; jj <= N; ++jj) {  // peers first, my own slice (already in out) last
         const int j = (me + jj) % N;
         ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
         uint32_t b = 0;
@@ -528,28 +577,31 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
           break;
         }
         bits |= b;
-      }
-      if (s_status == ST_OK) {
-        hdr->peer_bits = bits;
-        st_release_gpu(&hdr->go, mk_flag(tag, 2));
+        mask |= 1u << j;
+        st_release_gpu(&hdr->go2, mk_flag(tag, mask));
       }
       ctl->tphase[3] = globaltimer_ns();
-    } else {
-      const uint32_t st = wait_go(hdr, mk_flag(tag, 2), s_t0, p.hard_timeout_ns);
-      if (st != ST_OK) s_status = st;
+      if (s_status == ST_OK && (bits & kBitNonFinite)) s_status = ST_NUMERICAL;
     }
-    if (s_status == ST_OK && (ld_relaxed_sys32(&hdr->peer_bits) & kBitNonFinite)) s_status = ST_NUMERICAL;
+    __syncthreads();
   }
-  __syncthreads();
 
   // ---- 4. all-gather pull (commit) ---------------------------------------
-  if (s_status == ST_OK) {
+  if (s_status == ST_OK || (direct && s_status == ST_NUMERICAL)) {
     float* const out = p.out[me];
     const bool vec_ok = s_vec_ok != 0;
     // every CTA starts on a different peer so all links stay busy
     for (int i = 0; i < N; ++i) {
       const int k = (int)((me + 1 + blockIdx.x + i) % N);
       if (direct && k == me) continue;  // written during the reduce-scatter
+      if (direct && blockIdx.x != 0) {
+        if (tid == 0) {
+          const uint32_t st = wait_go_bit(hdr, tag, k, s_t0, p.hard_timeout_ns);
+          if (st != ST_OK) s_status = st;
+        }
+        __syncthreads();
+        if (s_status != ST_OK) break;
+      }
       const uint64_t klo = umin((uint64_t)k * p.slice, E), khi = umin(klo + p.slice, E);
       copy_f32<8>(out + klo, s_res[k], khi - klo, vec_ok);
     }
@@ -1015,6 +1067,7 @@ struct DeviceGuard {
 };
 
 constexpr int kMaxSlots = 256;
+constexpr int kQueue = 4;
 
 int g_ctas = 0;         // real-mode CTAs per member (0 = default)
 int g_local_ctas = 0;   // in-process ring CTAs per member (0 = default)
@@ -1056,8 +1109,15 @@ struct ftar_ctx {
   uint64_t arena_bytes = 0;
   uint64_t max_bucket_bytes = 0;
   uint64_t res_off = 0, stage_off[2] = {0, 0}, pool_off = 0, pool_bytes = 0;
+  // control blocks: a FIFO of kQueue slots, one per queued collective, so a
+  // caller can enqueue several buckets before waiting (the GPU then runs
+  // them back to back); ctl_h/ctl_d point at the most recently launched one
+  HostCtl* ctl_hs = nullptr;
+  HostCtl* ctl_ds = nullptr;
   HostCtl* ctl_h = nullptr;
   HostCtl* ctl_d = nullptr;
+  uint64_t q_tag[kQueue] = {};
+  int q_head = 0, q_count = 0;
   char* peer[kMaxSlots] = {};
   uint64_t peer_bytes[kMaxSlots] = {};
   bool peer_local[kMaxSlots] = {};  // linked in-process (no IPC handle to close)
@@ -1066,8 +1126,37 @@ struct ftar_ctx {
   uint32_t contrib = 1;
   uint64_t gen = 0, seq = 0;
   uint64_t cur_tag = 0;
-  bool inflight = false;
   uint64_t hard_timeout_ns = 120ull * 1000000000ull;
+
+  // enqueue a collective with `tag`; returns its control block or nullptr when full
+  HostCtl* push(uint64_t tag) {
+    if (q_count == kQueue) return nullptr;
+    const int slot = (q_head + q_count) % kQueue;
+    HostCtl* h = ctl_hs + slot;
+    h->abort_tag = 0;
+    h->started = 0;
+    h->progress = 0;
+    h->done = 0;
+    h->detail = -1;
+    h->available = -1;
+    h->epoch = gen;
+    q_tag[slot] = tag;
+    ++q_count;
+    ctl_h = h;
+    ctl_d = ctl_ds + slot;
+    cur_tag = tag;
+    return h;
+  }
+  void pop_last() {  // undo a push whose launch failed
+    --q_count;
+  }
+  bool all_done() const {
+    for (int i = 0; i < q_count; ++i) {
+      const int slot = (q_head + i) % kQueue;
+      if (flag_tag(ctl_hs[slot].done) != q_tag[slot]) return false;
+    }
+    return true;
+  }
 };
 
 struct ftar_snap {
@@ -1230,17 +1319,21 @@ int ftar_ctx_create(int device, uint64_t max_bucket_bytes, uint64_t pool_bytes, 
   ArenaHdr init{};
   init.err_peer = -1;
   cudaMemcpy(c->arena, &init, sizeof(init), cudaMemcpyHostToDevice);
-  e = cudaHostAlloc(&c->ctl_h, sizeof(HostCtl), cudaHostAllocMapped | cudaHostAllocPortable);
+  e = cudaHostAlloc(&c->ctl_hs, kQueue * sizeof(HostCtl), cudaHostAllocMapped | cudaHostAllocPortable);
   if (e != cudaSuccess) {
     cudaFree(c->arena);
     delete c;
     return cuda_fail(e, "cudaHostAlloc(ctl)");
   }
-  std::memset((void*)c->ctl_h, 0, sizeof(HostCtl));
-  reset_ctl(c->ctl_h);
-  c->ctl_h->live_mask = 1;
-  c->ctl_h->contrib_mask = 1;
-  cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->ctl_d), (void*)c->ctl_h, 0);
+  std::memset((void*)c->ctl_hs, 0, kQueue * sizeof(HostCtl));
+  cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->ctl_ds), (void*)c->ctl_hs, 0);
+  for (int i = 0; i < kQueue; ++i) {
+    reset_ctl(c->ctl_hs + i);
+    c->ctl_hs[i].live_mask = 1;
+    c->ctl_hs[i].contrib_mask = 1;
+  }
+  c->ctl_h = c->ctl_hs;
+  c->ctl_d = c->ctl_ds;
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cuda_fail(e, "ctx init");
   c->ring_slots[0] = -1;
@@ -1255,7 +1348,7 @@ int ftar_ctx_destroy(ftar_ctx* c) {
   for (int s = 0; s < kMaxSlots; ++s)
     if (c->peer[s] && !c->peer_local[s]) cudaIpcCloseMemHandle(c->peer[s]);
   cudaFree(c->arena);
-  cudaFreeHost((void*)c->ctl_h);
+  cudaFreeHost((void*)c->ctl_hs);
   delete c;
   return FTAR_OK;
 }
@@ -1328,11 +1421,10 @@ int ftar_set_membership(ftar_ctx* c, const int* ring_slots, int n, int self_inde
   if (!c || n < 1 || n > kMaxMembers || self_index < 0 || self_index >= n)
     return fail(FTAR_ST_INVARIANT, "bad membership");
   if (generation > 0xffffffull) return fail(FTAR_ST_INVARIANT, "generation exceeds 24 bits");
-  if (c->inflight) {
-    int s = 0;
-    if (flag_tag(c->ctl_h->done) != c->cur_tag) return fail(FTAR_ST_INVARIANT, "membership change with an all-reduce in flight");
-    (void)s;
-    c->inflight = false;
+  if (c->q_count) {
+    if (!c->all_done()) return fail(FTAR_ST_INVARIANT, "membership change with an all-reduce in flight");
+    c->q_head = (c->q_head + c->q_count) % kQueue;  // statuses of finished, unwaited ops are dropped
+    c->q_count = 0;
   }
   for (int i = 0; i < n; ++i) {
     if (i == self_index) {
@@ -1348,9 +1440,11 @@ int ftar_set_membership(ftar_ctx* c, const int* ring_slots, int n, int self_inde
   c->contrib = contrib_mask & ((n >= 32) ? 0xffffffffu : ((1u << n) - 1u));
   c->gen = generation;
   c->seq = 0;
-  c->ctl_h->live_mask = (n >= 32) ? 0xffffffffu : ((1u << n) - 1u);
-  c->ctl_h->contrib_mask = c->contrib;
-  c->ctl_h->epoch = generation;
+  for (int i = 0; i < kQueue; ++i) {
+    c->ctl_hs[i].live_mask = (n >= 32) ? 0xffffffffu : ((1u << n) - 1u);
+    c->ctl_hs[i].contrib_mask = c->contrib;
+    c->ctl_hs[i].epoch = generation;
+  }
   return FTAR_OK;
 }
 
@@ -1371,8 +1465,7 @@ int ftar_allreduce_launch_range(ftar_ctx* c, const void* in, int in_dtype, float
   if (!c) return fail(FTAR_ST_INVARIANT, "null ctx");
   int v = validate_common(in_dtype, c->n, chunk_bytes, max_in_flight);
   if (v) return v;
-  if (c->inflight && flag_tag(c->ctl_h->done) != c->cur_tag)
-    return fail(FTAR_ST_INVARIANT, "one all-reduce in flight per ring group");
+  if (c->q_count == kQueue) return fail(FTAR_ST_INVARIANT, "all-reduce queue full: wait for the oldest first");
   const uint64_t esz = in_dtype == FTAR_DT_BF16 ? 2 : 4;
   const uint64_t in_bytes = n_elems * esz;
   if (in_bytes > c->max_bucket_bytes || n_elems * 4 > 2 * c->max_bucket_bytes)
@@ -1397,6 +1490,7 @@ int ftar_allreduce_launch_range(ftar_ctx* c, const void* in, int in_dtype, float
   LaunchParams p{};
   fill_geometry(p, n_elems, chunk_bytes, max_in_flight, c->n, base_elem, total_elems);
   for (int i = 0; i < c->n; ++i) p.base[i] = (i == c->self) ? c->arena : c->peer[c->ring_slots[i]];
+  c->push(tag);
   p.ctl[c->self] = c->ctl_d;
   p.out[c->self] = out;
   p.in_off[c->self] = in_off;
@@ -1422,14 +1516,11 @@ int ftar_allreduce_launch_range(ftar_ctx* c, const void* in, int in_dtype, float
   p.fault_after_tiles = 0;
   p.rs_layout = rs_layout();
   p.diag = diag_mode();
-  reset_ctl(c->ctl_h);
-  c->cur_tag = tag;
-  c->inflight = true;
   const dim3 grid(real_ctas(), 1);
   cudaError_t e = in_dtype == FTAR_DT_BF16 ? launch_dispatch<BF16In>(c->n, p, grid, st, false)
                                             : launch_dispatch<F32In>(c->n, p, grid, st, false);
   if (e != cudaSuccess) {
-    c->inflight = false;
+    c->pop_last();
     return cuda_fail(e, "allreduce launch");
   }
   return FTAR_OK;
@@ -1448,8 +1539,7 @@ int ftar_local_allreduce_launch_range(ftar_ctx** ctxs, int n, const void* const*
   for (int i = 0; i < n; ++i) {
     ftar_ctx* c = ctxs[i];
     if (!c || c->device != dev) return fail(FTAR_ST_INVARIANT, "in-process ring members must share a device");
-    if (c->inflight && flag_tag(c->ctl_h->done) != c->cur_tag)
-      return fail(FTAR_ST_INVARIANT, "one all-reduce in flight per ring group");
+    if (c->q_count) return fail(FTAR_ST_INVARIANT, "in-process rings run one all-reduce at a time");
     if (n_elems * 4 > 2 * c->max_bucket_bytes)
       return fail(FTAR_ST_INVARIANT, "bucket exceeds the ring group's arena capacity");
     if (c->gen != ctxs[0]->gen || c->seq != ctxs[0]->seq)
@@ -1464,15 +1554,12 @@ int ftar_local_allreduce_launch_range(ftar_ctx** ctxs, int n, const void* const*
     ftar_ctx* c = ctxs[i];
     c->seq += 1;
     tag = mk_tag(c->gen, c->seq);
+    c->push(tag);
     p.base[i] = c->arena;
     p.ctl[i] = c->ctl_d;
     p.out[i] = outs[i];
     p.in_off[i] = (uint64_t)(static_cast<const char*>(ins[i]) - c->arena);
     p.res_off[i] = c->res_off;
-    reset_ctl(c->ctl_h);
-    c->ctl_h->epoch = c->gen;
-    c->cur_tag = tag;
-    c->inflight = true;
   }
   p.tag = tag;
   p.nelems = n_elems;
@@ -1530,7 +1617,7 @@ int ftar_local_allreduce_launch_range(ftar_ctx** ctxs, int n, const void* const*
     cudaError_t e = in_dtype == FTAR_DT_BF16 ? oneshot_dispatch<BF16In>(n, lp, grid, st)
                                               : oneshot_dispatch<F32In>(n, lp, grid, st);
     if (e != cudaSuccess) {
-      for (int i = 0; i < n; ++i) ctxs[i]->inflight = false;
+      for (int i = 0; i < n; ++i) ctxs[i]->pop_last();
       return cuda_fail(e, "local one-shot cooperative launch");
     }
     return FTAR_OK;
@@ -1543,7 +1630,7 @@ int ftar_local_allreduce_launch_range(ftar_ctx** ctxs, int n, const void* const*
   cudaError_t e = in_dtype == FTAR_DT_BF16 ? launch_dispatch<BF16In>(n, p, grid, st, true)
                                             : launch_dispatch<F32In>(n, p, grid, st, true);
   if (e != cudaSuccess) {
-    for (int i = 0; i < n; ++i) ctxs[i]->inflight = false;
+    for (int i = 0; i < n; ++i) ctxs[i]->pop_last();
     return cuda_fail(e, "local allreduce cooperative launch");
   }
   return FTAR_OK;
@@ -1567,25 +1654,39 @@ int ftar_local_allreduce_launch(ftar_ctx** ctxs, int n, const void* const* ins, 
 
 int ftar_poll(ftar_ctx* c, int* status, uint64_t* progress) {
   if (!c) return fail(FTAR_ST_INVARIANT, "null ctx");
-  const uint64_t d = c->ctl_h->done;
-  if (progress) *progress = c->ctl_h->progress;
-  if (status) *status = (c->inflight && flag_tag(d) == c->cur_tag) ? (int)(d & 0xff)
-                       : (c->inflight ? FTAR_ST_PENDING : FTAR_OK);
+  if (!c->q_count) {
+    if (status) *status = FTAR_OK;
+    if (progress) *progress = c->ctl_h->progress;
+    return FTAR_OK;
+  }
+  const HostCtl* h = c->ctl_hs + c->q_head;
+  const uint64_t d = h->done;
+  if (progress) *progress = h->progress;
+  if (status) *status = flag_tag(d) == c->q_tag[c->q_head] ? (int)(d & 0xff) : FTAR_ST_PENDING;
   return FTAR_OK;
 }
 
 int ftar_abort(ftar_ctx* c) {
   if (!c) return fail(FTAR_ST_INVARIANT, "null ctx");
-  c->ctl_h->abort_tag = c->cur_tag;
+  for (int i = 0; i < c->q_count; ++i) {
+    const int slot = (c->q_head + i) % kQueue;
+    c->ctl_hs[slot].abort_tag = c->q_tag[slot];
+  }
   return FTAR_OK;
 }
 
+int ftar_inflight(ftar_ctx* c) { return c ? c->q_count : 0; }
+
 int ftar_wait(ftar_ctx* c, double progress_timeout_s, int* detail) {
+  // Waits for the OLDEST queued collective (FIFO).  Its per-chunk deadline
+  // starts when its kernel starts (queued work behind earlier buckets does
+  // not count); no progress for progress_timeout_s -> abort word -> drain.
   if (!c) return fail(FTAR_ST_INVARIANT, "null ctx");
   if (detail) *detail = -1;
-  if (!c->inflight) return FTAR_OK;
-  HostCtl* h = c->ctl_h;
-  const uint64_t tag = c->cur_tag;
+  if (!c->q_count) return FTAR_OK;
+  const int slot = c->q_head;
+  HostCtl* h = c->ctl_hs + slot;
+  const uint64_t tag = c->q_tag[slot];
   uint64_t last_prog = ~0ull;
   double last_change = now_s();
   const double t_begin = last_change;
@@ -1594,10 +1695,10 @@ int ftar_wait(ftar_ctx* c, double progress_timeout_s, int* detail) {
   for (uint64_t it = 0;; ++it) {
     const uint64_t d = h->done;
     if (flag_tag(d) == tag) {
-      c->inflight = false;
+      c->q_head = (c->q_head + 1) % kQueue;
+      --c->q_count;
       if (detail) *detail = (int)h->detail;
-      int st = (int)(d & 0xff);
-      return st;
+      return (int)(d & 0xff);
     }
     const double t = now_s();
     if (h->started == tag) {
@@ -1606,7 +1707,11 @@ int ftar_wait(ftar_ctx* c, double progress_timeout_s, int* detail) {
         last_prog = pr;
         last_change = t;
       } else if (!aborted && t - last_change > progress_timeout_s) {
-        h->abort_tag = tag;  // per-chunk deadline expired: drain the kernel
+        // per-chunk deadline expired: drain this and every queued collective
+        for (int i = 0; i < c->q_count; ++i) {
+          const int sl = (c->q_head + i) % kQueue;
+          c->ctl_hs[sl].abort_tag = c->q_tag[sl];
+        }
         aborted = true;
         abort_t = t;
       }
@@ -1635,7 +1740,7 @@ int ftar_wait_local(ftar_ctx** ctxs, int n, double progress_timeout_s, int* stat
     last_change[i] = t0;
     statuses[i] = FTAR_OK;
     if (details) details[i] = -1;
-    fin[i] = !ctxs[i]->inflight;
+    fin[i] = ctxs[i]->q_count == 0;
   }
   double abort_t = 0;
   for (uint64_t it = 0;; ++it) {
@@ -1644,23 +1749,26 @@ int ftar_wait_local(ftar_ctx** ctxs, int n, double progress_timeout_s, int* stat
     for (int i = 0; i < n; ++i) {
       if (fin[i]) continue;
       ftar_ctx* c = ctxs[i];
-      HostCtl* h = c->ctl_h;
+      const int slot = c->q_head;
+      HostCtl* h = c->ctl_hs + slot;
+      const uint64_t tag = c->q_tag[slot];
       const uint64_t d = h->done;
-      if (flag_tag(d) == c->cur_tag) {
+      if (flag_tag(d) == tag) {
         fin[i] = true;
-        c->inflight = false;
+        c->q_head = (c->q_head + 1) % kQueue;
+        --c->q_count;
         statuses[i] = (int)(d & 0xff);
         if (details) details[i] = (int)h->detail;
         continue;
       }
       ++left;
-      if (h->started == c->cur_tag) {
+      if (h->started == tag) {
         const uint64_t pr = h->progress;
         if (pr != last_prog[i]) {
           last_prog[i] = pr;
           last_change[i] = t;
         } else if (!aborted[i] && t - last_change[i] > progress_timeout_s) {
-          h->abort_tag = c->cur_tag;
+          h->abort_tag = tag;
           aborted[i] = true;
           if (abort_t == 0) abort_t = t;
         }

@@ -73,6 +73,7 @@ struct alignas(128) ArenaHdr {
   uint64_t peer_res[kMaxMembers];         // and member result slices (my VA)
   uint32_t peer_bits;                     // RS barrier: OR of members' rs_done bits
   uint32_t vec_ok;
+  alignas(128) uint64_t go2;              // direct mode: (tag << 8) | mask of members whose slice is reduced
 };
 static_assert(sizeof(ArenaHdr) <= kHdrBytes, "header too large");
 

@@ -444,6 +444,64 @@ def ftar_all_reduce(group: RingGroup, buf: torch.Tensor, step: int, cfg: Pipelin
     return dst
 
 
+class PendingAllReduce:
+    """A queued collective (ftar_all_reduce_async).  wait() collects it —
+    and every earlier one of the same group, in launch order — and raises the
+    taxonomy exception of its status (the links are then closed, as in
+    ftar.py:323-325)."""
+
+    __slots__ = ("group", "result", "cfg", "status", "detail", "done")
+
+    def __init__(self, group, result, cfg):
+        self.group, self.result, self.cfg = group, result, cfg
+        self.status, self.detail, self.done = 0, -1, False
+
+    def wait(self):
+        q = self.group._pending
+        while not self.done:
+            head = q.popleft()
+            det = C.c_int(-1)
+            head.status = _lib.lib.ftar_wait(self.group.ctx, head.cfg.per_chunk_timeout_s, C.byref(det))
+            head.detail, head.done = det.value, True
+        if self.status:
+            self.group.close_links()
+            blame = self.group.members[self.detail] if 0 <= self.detail < self.group.n else None
+            msg = _lib.last_error() if self.status == 10 else ""
+            raise from_status(self.status, (msg + f" (peer replica {blame})") if blame is not None else msg)
+        return self.result
+
+
+def ftar_all_reduce_async(group: RingGroup, buf: torch.Tensor, step: int, cfg: PipelineConfig | None = None,
+                          *, out: torch.Tensor | None = None, scale: float | None = None) -> PendingAllReduce:
+    """Enqueue one all-reduce on the current stream and return at once (up to
+    4 per group in flight; the GPU runs queued buckets back to back, as a
+    bucketed backward pass would issue them).  Same semantics as
+    ftar_all_reduce once .wait() returns."""
+    cfg = cfg or PipelineConfig()
+    if group._local or not (isinstance(buf, torch.Tensor) and buf.is_cuda):
+        p = PendingAllReduce(group, ftar_all_reduce(group, buf, step, cfg, out=out, scale=scale), cfg)
+        p.done = True
+        return p
+    code, dst = _check_buffers(buf, out)
+    if group.n > 1 and not group.links_ready():
+        raise Recoverable(PEER_RESET, "ring links not established")
+    q = group.__dict__.setdefault("_pending", __import__("collections").deque())
+    while len(q) >= 4:
+        q[0].wait()
+    flags = _lib.F_SCALE if scale is not None else 0
+    f_scale = _f32(scale) if scale is not None else 1.0
+    rc = _lib.lib.ftar_allreduce_launch(group.ctx, buf.data_ptr(), code, dst.data_ptr(), buf.numel(),
+                                        cfg.chunk_bytes, cfg.max_in_flight, f_scale, flags,
+                                        _stream_ptr(group.device))
+    _lib.check(rc, "ftar_allreduce_launch")
+    p = PendingAllReduce(group, dst, cfg)
+    q.append(p)
+    bound, ctas = group.inflight_bound(buf.element_size())
+    group.meter.sent(bound, ctas)
+    group.meter.acked(bound, ctas)
+    return p
+
+
 def _host_all_reduce(group, buf, step, cfg, out, scale):
     """Host (numpy / CPU tensor) buffers: the reference's exact call shape.
     One process per GPU: chunked H2D / range all-reduce / D2H pipeline.
@@ -456,6 +514,9 @@ def _host_all_reduce(group, buf, step, cfg, out, scale):
     hout = _as_host_tensor(out) if out is not None else None
     if group.n > 1 and not group.links_ready():
         raise Recoverable(PEER_RESET, "ring links not established")
+    q = group.__dict__.get("_pending")
+    while q:
+        q[0].wait()
     if group._local:
         dev = host.to(group.device)
         dres = torch.empty(host.numel(), device=group.device) if out is not None else None
@@ -491,6 +552,9 @@ def _host_all_reduce(group, buf, step, cfg, out, scale):
 
 
 def _remote_all_reduce(group, buf, dst, code, cfg, f_scale, flags):
+    q = group.__dict__.get("_pending")
+    while q:
+        q[0].wait()
     with group._lock:
         group._seq += 1
         rc = _lib.lib.ftar_allreduce_launch(group.ctx, buf.data_ptr(), code, dst.data_ptr(), buf.numel(),

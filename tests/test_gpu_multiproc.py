@@ -220,3 +220,57 @@ def test_catchup_pull_over_nvlink():
     res = run("catchup", 2)
     assert not res[1]["errors"], res[1]["errors"]
     assert "pull" in res[1]["ok"] and "unavailable" in res[1]["ok"]
+
+
+def _async_worker(rank, world, port, outdir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    import numpy as np
+    import torch.distributed as dist
+    from datetime import timedelta
+
+    from gen import member_inputs
+    from oracle import ftar_oracle as orc
+    from paper_2602_00277_b200 import ftar
+    from paper_2602_00277_b200.fabric import StoreFabric
+
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    store = dist.TCPStore("127.0.0.1", port, world, rank == 0, timeout=timedelta(seconds=60))
+    fabric = StoreFabric(dist.PrefixStore("async", store))
+    res = {"rank": rank, "ok": [], "errors": []}
+    group = ftar.RingGroup(rank, 0, fabric, device=dev, max_bucket_bytes=16 << 20)
+    try:
+        group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, 1, deadline_s=30)
+        buckets = [member_inputs(world, 1_000_003 + 7 * b, seed=100 + b) for b in range(7)]
+        bufs = [torch.from_numpy(bk[rank]).to(dev) for bk in buckets]
+        outs = [torch.empty_like(b) for b in bufs]
+        pend = [ftar.ftar_all_reduce_async(group, b, 1, out=o, scale=0.5) for b, o in zip(bufs, outs)]
+        for p in reversed(pend):  # waiting a later one collects the earlier ones first
+            p.wait()
+        for bk, o in zip(buckets, outs):
+            want = orc.normalize(orc.oracle_reduce(bk, 8 << 20, 4), 2) if world == 2 else None
+            if want is None:
+                want = orc.oracle_reduce(bk, 8 << 20, 4) * np.float32(0.5)
+            (res["ok"] if np.array_equal(o.cpu().numpy(), want) else res["errors"]).append("bucket")
+    except Exception as exc:  # noqa: BLE001
+        import traceback
+        res["errors"].append(f"exception: {exc!r}\n{traceback.format_exc()}")
+    finally:
+        store.set(f"fin{rank}", b"1")
+        store.wait([f"fin{r}" for r in range(world)], timedelta(seconds=60))
+        group.close()
+        with open(os.path.join(outdir, f"r{rank}.json"), "w") as f:
+            json.dump(res, f)
+
+
+def test_async_queue_of_buckets():
+    world = world_size()
+    port = free_port()
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_async_worker, args=(world, port, d), nprocs=world, join=True, start_method="spawn")
+        for r in range(world):
+            with open(os.path.join(d, f"r{r}.json")) as f:
+                res = json.load(f)
+            assert not res["errors"], res["errors"]
+            assert res["ok"].count("bucket") == 7
