@@ -45,6 +45,7 @@ __host__ __device__ __forceinline__ uint64_t umax(uint64_t a, uint64_t b) { retu
 
 constexpr uint32_t ST_FOLLOW = 254;  // stop because another CTA of mine failed
 constexpr uint32_t kFlagDirect = 1u << 8;  // internal launch flag: RS writes my slice of out
+constexpr uint32_t kFlagPush = 1u << 9;    // internal: all-gather by posted writes into peers' outs
 
 struct LaunchParams {
   char* base[kMaxMembers];       // arena base of ring member i, as mapped here
@@ -52,6 +53,7 @@ struct LaunchParams {
   float* out[kMaxMembers];       // fp32 output of member i
   uint64_t in_off[kMaxMembers];  // member i's input address - its arena base
   uint64_t res_off[kMaxMembers]; // member i's result region offset
+  uint64_t out_off[kMaxMembers]; // member i's out - arena base (push mode), ~0 = none
   uint64_t tag;
   uint64_t nelems;
   uint64_t slice;                // elements reduced per ring index (multiple of 8)
@@ -70,6 +72,7 @@ struct LaunchParams {
   int fault_after_tiles;
   int rs_layout;                 // 0: contiguous span per CTA, 1: grid-strided tiles
   int diag;                      // timing diagnostics: 1 = RS stores skipped, 2 = RS reads local only
+  int rs_ctas;                   // CTAs that reduce (the rest only all-gather); <= gridDim.x
 };
 
 __device__ __forceinline__ uint32_t severity_code(uint32_t st) {
@@ -191,6 +194,20 @@ struct SinkNone {  // diagnostics: results computed, never stored
     if (v.x == 0x7fc00001u && v.y == 0x7fc00001u) *reinterpret_cast<uint4*>(p + e) = v;
   }
 };
+// Push mode: my folded slice goes to my `out` and, by posted NVLink writes,
+// straight into every peer's `out` (the all-gather fused into the reduce).
+template <int N>
+struct SinkPush {
+  float* const* outs;  // members' out (element 0), my VA; outs[me] local
+  __device__ __forceinline__ void put1(uint64_t e, float x) const {
+#pragma unroll
+    for (int j = 0; j < N; ++j) outs[j][e] = x;
+  }
+  __device__ __forceinline__ void put4(uint64_t e, const uint4& v) const {
+#pragma unroll
+    for (int j = 0; j < N; ++j) st_stream(outs[j] + e, v);
+  }
+};
 struct SinkTwo {
   float* p;
   float* q;
@@ -307,9 +324,11 @@ __device__ __forceinline__ int fold_tiles(const LaunchParams& p, const typename 
   int done = 0;
   int s = 0;
   uint64_t sbeg = 1, send = 0;  // cached run [sbeg, send) with owner s
-  uint64_t first = lo + (uint64_t)blockIdx.x * TL, step = (uint64_t)gridDim.x * TL;
+  const uint64_t G = (p.rs_ctas > 0 && p.rs_ctas < (int)gridDim.x) ? (uint64_t)p.rs_ctas : gridDim.x;
+  if (blockIdx.x >= G) return 0;  // all-gather-only CTA
+  uint64_t first = lo + (uint64_t)blockIdx.x * TL, step = G * TL;
   if (p.rs_layout == 0) {  // one contiguous span per CTA
-    const uint64_t per = ((hi - lo + gridDim.x - 1) / gridDim.x + 7) & ~7ull;
+    const uint64_t per = ((hi - lo + G - 1) / G + 7) & ~7ull;
     first = umin(lo + (uint64_t)blockIdx.x * per, hi);
     hi = umin(first + per, hi);
     step = TL;
@@ -382,6 +401,8 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
 
   __shared__ const T* s_src[N];
   __shared__ const float* s_res[N];
+  __shared__ float* s_out[N];
+  __shared__ int s_push;
   __shared__ uint32_t s_status;
   __shared__ int s_blame;
   __shared__ uint32_t s_nf;
@@ -392,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
     s_status = ST_OK;
     s_blame = -1;
     s_nf = 0;
+    s_push = 0;
     s_t0 = globaltimer_ns();
     if (blockIdx.x == 0) {
       // Epoch fence: an op queued under an older decision must not run
@@ -412,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         en->n = (uint32_t)N;
         en->ebase = p.ebase;
         en->total = p.total;
+        en->out_off = (p.flags & kFlagPush) ? p.out_off[me] : ~0ull;
         __threadfence_system();
         st_release_sys(&en->flag, mk_flag(tag, 0));
       }
@@ -423,10 +446,12 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
   if (tid == 0 && s_status == ST_OK) {
     if (blockIdx.x == 0) {
       int ok = 1;
+      uint32_t push_ok = (p.flags & kFlagPush) ? 1u : 0u;
       for (int j = 0; j < N; ++j) {
         if (j == me) {
           hdr->peer_in[j] = reinterpret_cast<uint64_t>(mybase) + p.in_off[me];
           hdr->peer_res[j] = reinterpret_cast<uint64_t>(mybase) + p.res_off[me];
+          hdr->peer_out[j] = reinterpret_cast<uint64_t>(p.out[me]);
           continue;
         }
         ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
@@ -451,10 +476,16 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         }
         hdr->peer_in[j] = reinterpret_cast<uint64_t>(p.base[j]) + in_off;
         hdr->peer_res[j] = reinterpret_cast<uint64_t>(p.base[j]) + res_off;
+        const uint64_t oo = ld_relaxed_sys(&ph->entry.out_off);
+        if (oo == ~0ull) push_ok = 0;  // every member must accept pushes, or nobody pushes
+        hdr->peer_out[j] = reinterpret_cast<uint64_t>(p.base[j]) + oo;
       }
+      hdr->push_ok = push_ok;
       if (ok) {
         uint64_t orbits = reinterpret_cast<uint64_t>(p.out[me]);
         for (int j = 0; j < N; ++j) orbits |= hdr->peer_in[j] | hdr->peer_res[j];
+        if (push_ok)
+          for (int j = 0; j < N; ++j) orbits |= hdr->peer_out[j];
         hdr->vec_ok = (orbits & 15u) == 0;
         st_release_gpu(&hdr->go, mk_flag(tag, 1));
       }
@@ -468,8 +499,10 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
       for (int j = 0; j < N; ++j) {
         s_src[j] = reinterpret_cast<const T*>(ld_relaxed_gpu(&hdr->peer_in[j]));
         s_res[j] = reinterpret_cast<const float*>(ld_relaxed_gpu(&hdr->peer_res[j]));
+        s_out[j] = reinterpret_cast<float*>(ld_relaxed_gpu(&hdr->peer_out[j]));
       }
       s_vec_ok = (int)ld_relaxed_sys32(&hdr->vec_ok);
+      s_push = direct && N > 1 && ld_relaxed_sys32(&hdr->push_ok) != 0;
     }
   }
   __syncthreads();
@@ -489,6 +522,8 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
       if (tid < N) s_loc[tid] = s_src[me];
       __syncthreads();
       done = fold_tiles<N, In>(p, s_loc, SinkOne{res}, lo, hi, vec_ok, do_scale, nf, ctl, max_tiles);
+    } else if (s_push) {
+      done = fold_tiles<N, In>(p, s_src, SinkPush<N>{s_out}, lo, hi, vec_ok, do_scale, nf, ctl, max_tiles);
     } else if (direct && res != p.out[me]) {
       done = fold_tiles<N, In>(p, s_src, SinkTwo{res, p.out[me]}, lo, hi, vec_ok, do_scale, nf, ctl, max_tiles);
     } else {
@@ -522,6 +557,15 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
       if (ld_relaxed_sys32(&hdr->err) == 0) {
         const uint32_t bits = ld_relaxed_sys32(&hdr->nonfinite) ? kBitNonFinite : 0u;
         st_release_sys(&hdr->rs_done, mk_flag(tag, bits));
+        if (s_push) {
+          // my whole slice is in every peer's out: tell them (the sys fence
+          // above made all my CTAs' posted writes visible first)
+          for (int j = 0; j < N; ++j) {
+            if (j == me) continue;
+            ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
+            st_release_sys(&ph->ag_in[me], mk_flag(tag, bits));
+          }
+        }
         ctl->tphase[2] = globaltimer_ns();
       }
       ctl->progress = hdr->tiles_done;
@@ -533,7 +577,29 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
   // is reduced and finite).  Out-of-place (direct) calls: `out` is scratch
   // until success, so CTA 0 publishes members one by one (go2 mask) and each
   // CTA pulls a slice as soon as its owner is done.
-  if (!direct) {
+  if (s_push) {
+    // push mode: peers wrote their slices into my out; CTA 0 waits for
+    // every peer's ag_in flag (local polls; their poison words remote)
+    if (blockIdx.x == 0 && tid == 0 && s_status == ST_OK) {
+      uint32_t bits = ld_relaxed_sys32(&hdr->nonfinite) ? kBitNonFinite : 0u;
+      for (int jj = 1; jj < N; ++jj) {
+        const int j = (me + jj) % N;
+        ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
+        uint32_t b = 0;
+        const uint32_t st = wait_flag(&hdr->ag_in[j], tag, &ph->poison, ctl, &hdr->err, s_t0,
+                                      p.hard_timeout_ns, &b);
+        if (st != ST_OK) {
+          s_status = st;
+          s_blame = j;
+          break;
+        }
+        bits |= b;
+      }
+      ctl->tphase[3] = globaltimer_ns();
+      if (s_status == ST_OK && (bits & kBitNonFinite)) s_status = ST_NUMERICAL;
+    }
+    __syncthreads();
+  } else if (!direct) {
     if (tid == 0 && s_status == ST_OK) {
       if (blockIdx.x == 0) {
         uint32_t bits = 0;
@@ -587,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
   }
 
   // ---- 4. all-gather pull (commit) ---------------------------------------
-  if (s_status == ST_OK || (direct && s_status == ST_NUMERICAL)) {
+  if (!s_push && (s_status == ST_OK || (direct && s_status == ST_NUMERICAL))) {
     float* const out = p.out[me];
     const bool vec_ok = s_vec_ok != 0;
     // every CTA starts on a different peer so all links stay busy
@@ -1076,7 +1142,13 @@ int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
 }
-int real_ctas() { return g_ctas > 0 ? g_ctas : env_int("FTAR_CTAS", 64); }
+// Launch shape (tuned on 2x/4x B200, tools/tune_allreduce.py + bench.py):
+// pull mode 64 CTAs that all reduce; push mode 128 CTAs.
+int real_ctas(bool push = false) {
+  if (g_ctas > 0) return g_ctas;
+  return push ? env_int("FTAR_CTAS_PUSH", 128) : env_int("FTAR_CTAS", 64);
+}
+int rs_ctas_knob() { return env_int("FTAR_RS_CTAS", 0); }
 int rs_layout() { return env_int("FTAR_RS_LAYOUT", 0); }
 int diag_mode() { return env_int("FTAR_DIAG", 0); }
 
@@ -1507,6 +1579,13 @@ int ftar_allreduce_launch_range(ftar_ctx* c, const void* in, int in_dtype, float
     const uint64_t o0 = reinterpret_cast<uint64_t>(out), i0 = reinterpret_cast<uint64_t>(in);
     const bool alias = o0 < i0 + in_bytes && i0 < o0 + n_elems * 4;
     if (!alias && n_elems && !env_int("FTAR_NO_DIRECT", 0)) p.flags |= kFlagDirect;
+    // push mode needs `out` inside my exported arena (peers write into it)
+    const char* op = reinterpret_cast<const char*>(out);
+    const bool out_reg = op >= c->arena + c->pool_off && op + n_elems * 4 <= c->arena + c->arena_bytes;
+    if ((p.flags & kFlagDirect) && out_reg && !env_int("FTAR_NO_PUSH", 0)) {
+      p.flags |= kFlagPush;
+      p.out_off[c->self] = (uint64_t)(op - c->arena);
+    }
   }
   p.contrib = c->contrib;
   p.dtype = (uint32_t)in_dtype;
@@ -1516,7 +1595,8 @@ int ftar_allreduce_launch_range(ftar_ctx* c, const void* in, int in_dtype, float
   p.fault_after_tiles = 0;
   p.rs_layout = rs_layout();
   p.diag = diag_mode();
-  const dim3 grid(real_ctas(), 1);
+  p.rs_ctas = rs_ctas_knob();
+  const dim3 grid(real_ctas((p.flags & kFlagPush) != 0), 1);
   cudaError_t e = in_dtype == FTAR_DT_BF16 ? launch_dispatch<BF16In>(c->n, p, grid, st, false)
                                             : launch_dispatch<F32In>(c->n, p, grid, st, false);
   if (e != cudaSuccess) {
@@ -1575,6 +1655,11 @@ int ftar_local_allreduce_launch_range(ftar_ctx** ctxs, int n, const void* const*
         alias = o0 < i0 + ib && i0 < o0 + ob;
       }
     if (!alias && n_elems) p.flags |= kFlagDirect;
+    if ((p.flags & kFlagDirect) && !env_int("FTAR_NO_PUSH", 0)) {
+      p.flags |= kFlagPush;  // in-process: every member's out is addressable
+      for (int i = 0; i < n; ++i)
+        p.out_off[i] = (uint64_t)(reinterpret_cast<const char*>(outs[i]) - ctxs[i]->arena);
+    }
   }
   p.contrib = contrib_mask & ((1u << n) - 1u);
   p.dtype = (uint32_t)in_dtype;

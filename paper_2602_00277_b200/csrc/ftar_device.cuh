@@ -51,6 +51,7 @@ struct alignas(128) EntryRec {
   uint32_t n;
   uint64_t ebase;      // range calls: first element of this call in the bucket
   uint64_t total;      // range calls: bucket length the geometry is built on
+  uint64_t out_off;    // push mode: my `out` (element 0) - arena base; ~0 = not addressable
 };
 
 struct alignas(128) ArenaHdr {
@@ -74,6 +75,9 @@ struct alignas(128) ArenaHdr {
   uint32_t peer_bits;                     // RS barrier: OR of members' rs_done bits
   uint32_t vec_ok;
   alignas(128) uint64_t go2;              // direct mode: (tag << 8) | mask of members whose slice is reduced
+  uint64_t peer_out[kMaxMembers];         // push mode: members' `out` element 0 (my VA)
+  uint32_t push_ok;                       // push mode agreed for this call
+  alignas(128) uint64_t ag_in[kMaxMembers];  // push mode: member k finished writing its slice into my out
 };
 static_assert(sizeof(ArenaHdr) <= kHdrBytes, "header too large");
 
