@@ -119,6 +119,18 @@ int ftar_allreduce_launch_range(ftar_ctx* ctx, const void* in, int in_dtype, flo
                                 uint64_t chunk_bytes, int max_in_flight, float scale,
                                 uint32_t flags, void* stream);
 
+/* §8f: the all-reduce with the SGD-momentum step fused in (model.py:146-155,
+ * replica.py:622-633): g = sum x f32(scale); m' = f32(m*beta) + g;
+ * p' = p - f32(lr*m'), every op separately rounded (bit-exact with the
+ * reference).  Out of place (params_out/momentum_out) so that, as in the
+ * reference, nothing is applied before the caller's commit vote; grad_out
+ * (nullable) optionally receives g.  Each member updates its own copy. */
+int ftar_allreduce_sgd_launch(ftar_ctx* ctx, const void* in, int in_dtype, float* grad_out,
+                              uint64_t n_elems, uint64_t chunk_bytes, int max_in_flight, float scale,
+                              uint32_t flags, const float* params, const float* momentum,
+                              float* params_out, float* momentum_out, float lr, float beta,
+                              void* stream);
+
 /* In-process ring: all `n` members live on ONE device and are driven by one
  * cooperative launch (the members' kernels wait on one another, so they
  * must be co-resident).  ctxs[i] is the member at ring index i.
@@ -137,6 +149,14 @@ int ftar_local_allreduce_launch_range(ftar_ctx** ctxs, int n, const void* const*
                                       uint64_t chunk_bytes, int max_in_flight, float scale,
                                       uint32_t flags, uint32_t contrib_mask, int fault_member,
                                       int fault_after_tiles, void* stream);
+
+/* In-process form of ftar_allreduce_sgd_launch (protocol kernel, one device). */
+int ftar_local_allreduce_sgd_launch(ftar_ctx** ctxs, int n, const void* const* ins, int in_dtype,
+                                    float* const* grad_outs, uint64_t n_elems, uint64_t chunk_bytes,
+                                    int max_in_flight, float scale, uint32_t flags,
+                                    uint32_t contrib_mask, const float* const* params,
+                                    const float* const* momentum, float* const* params_out,
+                                    float* const* momentum_out, float lr, float beta, void* stream);
 
 /* Poll the op in flight: *status = FTAR_ST_PENDING while running, else the
  * final code; *progress = work tiles completed (the per-chunk completion

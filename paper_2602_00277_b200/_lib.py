@@ -38,6 +38,11 @@ SIGNATURES = {
     "ftar_ctx_link_local": (i32, [c_ctx_p, i32, c_ctx_p]),
     "ftar_set_membership": (i32, [c_ctx_p, C.POINTER(i32), i32, i32, u32, u64]),
     "ftar_allreduce_launch": (i32, [c_ctx_p, vp, i32, vp, u64, u64, i32, C.c_float, u32, vp]),
+    "ftar_allreduce_sgd_launch": (i32, [c_ctx_p, vp, i32, vp, u64, u64, i32, C.c_float, u32, vp, vp, vp, vp,
+                                        C.c_float, C.c_float, vp]),
+    "ftar_local_allreduce_sgd_launch": (i32, [C.POINTER(c_ctx_p), i32, C.POINTER(vp), i32, C.POINTER(vp), u64, u64,
+                                              i32, C.c_float, u32, u32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                                              C.POINTER(vp), C.c_float, C.c_float, vp]),
     "ftar_allreduce_launch_range": (i32, [c_ctx_p, vp, i32, vp, u64, u64, u64, u64, i32, C.c_float, u32, vp]),
     "ftar_local_allreduce_launch_range": (i32, [C.POINTER(c_ctx_p), i32, C.POINTER(vp), i32, C.POINTER(vp), u64,
                                                 u64, u64, u64, i32, C.c_float, u32, u32, i32, i32, vp]),

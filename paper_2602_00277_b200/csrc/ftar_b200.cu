@@ -46,6 +46,7 @@ __host__ __device__ __forceinline__ uint64_t umax(uint64_t a, uint64_t b) { retu
 constexpr uint32_t ST_FOLLOW = 254;  // stop because another CTA of mine failed
 constexpr uint32_t kFlagDirect = 1u << 8;  // internal launch flag: RS writes my slice of out
 constexpr uint32_t kFlagPush = 1u << 9;    // internal: all-gather by posted writes into peers' outs
+constexpr uint32_t kFlagSGD = 1u << 10;    // internal: apply SGD-momentum to the reduced gradient
 
 struct LaunchParams {
   char* base[kMaxMembers];       // arena base of ring member i, as mapped here
@@ -62,6 +63,11 @@ struct LaunchParams {
   uint64_t ebase;                // element index of this call's element 0 in the bucket
   uint64_t total;                // bucket length (geometry)
   uint64_t hard_timeout_ns;
+  const float* sgd_p[kMaxMembers];  // fused optimizer (§8f): member i's params / momentum in
+  const float* sgd_m[kMaxMembers];
+  float* sgd_po[kMaxMembers];        // updated params / momentum out (the caller swaps on commit,
+  float* sgd_mo[kMaxMembers];        // as replica.py applies the optimizer only after the 2PC vote)
+  float sgd_lr, sgd_beta;
   float scale;
   uint32_t flags;
   uint32_t contrib;              // bit i: ring index i contributes data (healthy)
@@ -206,6 +212,53 @@ struct SinkPush {
   __device__ __forceinline__ void put4(uint64_t e, const uint4& v) const {
 #pragma unroll
     for (int j = 0; j < N; ++j) st_stream(outs[j] + e, v);
+  }
+};
+// SGD-momentum on the reduced gradient g, exactly model.optimizer_step
+// (model.py:146-155): m = f32(m*beta); m = f32(m + g); p = f32(p - f32(lr*m)).
+// Optionally the gradient itself goes to `g_out` too.
+struct SgdRefs {
+  const float* p;
+  const float* m;
+  float* po;
+  float* mo;
+  __device__ __forceinline__ SgdRefs at(uint64_t off) const { return {p + off, m + off, po + off, mo + off}; }
+};
+__device__ __forceinline__ void sgd4(const SgdRefs& r, uint64_t e, const uint4& gv, float lr, float beta) {
+  const uint4 mv = ld_stream(r.m + e), pv = ld_stream(r.p + e);
+  float gg[4] = {__uint_as_float(gv.x), __uint_as_float(gv.y), __uint_as_float(gv.z), __uint_as_float(gv.w)};
+  float mm[4] = {__uint_as_float(mv.x), __uint_as_float(mv.y), __uint_as_float(mv.z), __uint_as_float(mv.w)};
+  float pp[4] = {__uint_as_float(pv.x), __uint_as_float(pv.y), __uint_as_float(pv.z), __uint_as_float(pv.w)};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    mm[i] = __fadd_rn(__fmul_rn(mm[i], beta), gg[i]);
+    pp[i] = __fsub_rn(pp[i], __fmul_rn(lr, mm[i]));
+  }
+  st_stream(r.mo + e, make_uint4(__float_as_uint(mm[0]), __float_as_uint(mm[1]), __float_as_uint(mm[2]),
+                                 __float_as_uint(mm[3])));
+  st_stream(r.po + e, make_uint4(__float_as_uint(pp[0]), __float_as_uint(pp[1]), __float_as_uint(pp[2]),
+                                 __float_as_uint(pp[3])));
+}
+__device__ __forceinline__ void sgd1(const SgdRefs& r, uint64_t e, float g, float lr, float beta) {
+  const float mm = __fadd_rn(__fmul_rn(r.m[e], beta), g);
+  const float pe = r.p[e];
+  r.mo[e] = mm;
+  r.po[e] = __fsub_rn(pe, __fmul_rn(lr, mm));
+}
+struct SinkSGD {  // my slice: result region (peers pull g) + fused update + optional g out
+  float* res;
+  float* gout;
+  SgdRefs r;
+  float lr, beta;
+  __device__ __forceinline__ void put1(uint64_t e, float x) const {
+    res[e] = x;
+    if (gout) gout[e] = x;
+    sgd1(r, e, x, lr, beta);
+  }
+  __device__ __forceinline__ void put4(uint64_t e, const uint4& v) const {
+    *reinterpret_cast<uint4*>(res + e) = v;
+    if (gout) st_stream(gout + e, v);
+    sgd4(r, e, v, lr, beta);
   }
 };
 struct SinkTwo {
@@ -354,6 +407,48 @@ __device__ __forceinline__ int fold_tiles(const LaunchParams& p, const typename 
 
 // Grid-stride fp32 copy (the all-gather pull), 16-byte vectors, UA loads in
 // flight per thread before the stores.
+// All-gather pull of a reduced slice straight into the optimizer update
+// (gradient never stored unless dst != nullptr).
+template <int UA>
+__device__ __forceinline__ void pull_sgd(float* dst, const float* src, const SgdRefs& r, uint64_t cnt,
+                                         bool vec_ok, float lr, float beta) {
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  const uint64_t first = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (!vec_ok) {
+    for (uint64_t e = first; e < cnt; e += stride) {
+      const float g = src[e];
+      if (dst) dst[e] = g;
+      sgd1(r, e, g, lr, beta);
+    }
+    return;
+  }
+  const uint64_t nv = cnt >> 2;
+  if (nv) {
+    for (uint64_t v = first; v < nv; v += stride * UA) {
+      uint4 rv[UA];
+#pragma unroll
+      for (int u = 0; u < UA; ++u) {
+        const uint64_t i = v + (uint64_t)u * stride;
+        rv[u] = ld_stream(src + (i < nv ? i : 0) * 4);
+      }
+#pragma unroll
+      for (int u = 0; u < UA; ++u) {
+        const uint64_t i = v + (uint64_t)u * stride;
+        if (i < nv) {
+          if (dst) *reinterpret_cast<uint4*>(dst + i * 4) = rv[u];
+          sgd4(r, i * 4, rv[u], lr, beta);
+        }
+      }
+    }
+  }
+  const uint64_t t = (nv << 2) + first;
+  if (t < cnt && first < 4) {
+    const float g = src[t];
+    if (dst) dst[t] = g;
+    sgd1(r, t, g, lr, beta);
+  }
+}
+
 template <int UA>
 __device__ __forceinline__ void copy_f32(float* dst, const float* src, uint64_t cnt, bool vec_ok) {
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
@@ -486,6 +581,9 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         for (int j = 0; j < N; ++j) orbits |= hdr->peer_in[j] | hdr->peer_res[j];
         if (push_ok)
           for (int j = 0; j < N; ++j) orbits |= hdr->peer_out[j];
+        if (p.flags & kFlagSGD)
+          orbits |= reinterpret_cast<uint64_t>(p.sgd_p[me]) | reinterpret_cast<uint64_t>(p.sgd_m[me]) |
+                    reinterpret_cast<uint64_t>(p.sgd_po[me]) | reinterpret_cast<uint64_t>(p.sgd_mo[me]);
         hdr->vec_ok = (orbits & 15u) == 0;
         st_release_gpu(&hdr->go, mk_flag(tag, 1));
       }
@@ -522,6 +620,11 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
       if (tid < N) s_loc[tid] = s_src[me];
       __syncthreads();
       done = fold_tiles<N, In>(p, s_loc, SinkOne{res}, lo, hi, vec_ok, do_scale, nf, ctl, max_tiles);
+    } else if (p.flags & kFlagSGD) {
+      done = fold_tiles<N, In>(p, s_src,
+                               SinkSGD{res, direct ? p.out[me] : nullptr, SgdRefs{p.sgd_p[me], p.sgd_m[me], p.sgd_po[me], p.sgd_mo[me]},
+                                       p.sgd_lr, p.sgd_beta},
+                               lo, hi, vec_ok, do_scale, nf, ctl, max_tiles);
     } else if (s_push) {
       done = fold_tiles<N, In>(p, s_src, SinkPush<N>{s_out}, lo, hi, vec_ok, do_scale, nf, ctl, max_tiles);
     } else if (direct && res != p.out[me]) {
@@ -659,7 +762,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
     // every CTA starts on a different peer so all links stay busy
     for (int i = 0; i < N; ++i) {
       const int k = (int)((me + 1 + blockIdx.x + i) % N);
-      if (direct && k == me) continue;  // written during the reduce-scatter
+      if ((direct || (p.flags & kFlagSGD)) && k == me) continue;  // done during the reduce-scatter
       if (direct && blockIdx.x != 0) {
         if (tid == 0) {
           const uint32_t st = wait_go_bit(hdr, tag, k, s_t0, p.hard_timeout_ns);
@@ -669,7 +772,11 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         if (s_status != ST_OK) break;
       }
       const uint64_t klo = umin((uint64_t)k * p.slice, E), khi = umin(klo + p.slice, E);
-      copy_f32<8>(out + klo, s_res[k], khi - klo, vec_ok);
+      if (p.flags & kFlagSGD)
+        pull_sgd<8>(direct ? out + klo : nullptr, s_res[k], SgdRefs{p.sgd_p[me], p.sgd_m[me], p.sgd_po[me], p.sgd_mo[me]}.at(klo),
+                    khi - klo, vec_ok, p.sgd_lr, p.sgd_beta);
+      else
+        copy_f32<8>(out + klo, s_res[k], khi - klo, vec_ok);
     }
   }
   __syncthreads();
@@ -1530,9 +1637,44 @@ int ftar_geometry(uint64_t n_elems, int n, uint64_t* slice_elems, int* ctas, int
   return FTAR_OK;
 }
 
+struct SgdArgs {
+  const float* p = nullptr;
+  const float* m = nullptr;
+  float* po = nullptr;
+  float* mo = nullptr;
+  float lr = 0.f, beta = 0.f;
+};
+
+static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, uint64_t n_elems,
+                       uint64_t base_elem, uint64_t total_elems, uint64_t chunk_bytes, int max_in_flight,
+                       float scale, uint32_t flags, void* stream, const SgdArgs* sgd);
+
 int ftar_allreduce_launch_range(ftar_ctx* c, const void* in, int in_dtype, float* out, uint64_t n_elems,
                                 uint64_t base_elem, uint64_t total_elems, uint64_t chunk_bytes,
                                 int max_in_flight, float scale, uint32_t flags, void* stream) {
+  return launch_real(c, in, in_dtype, out, n_elems, base_elem, total_elems, chunk_bytes, max_in_flight, scale,
+                     flags, stream, nullptr);
+}
+
+int ftar_allreduce_sgd_launch(ftar_ctx* c, const void* in, int in_dtype, float* grad_out, uint64_t n_elems,
+                              uint64_t chunk_bytes, int max_in_flight, float scale, uint32_t flags,
+                              const float* params, const float* momentum, float* params_out, float* momentum_out,
+                              float lr, float beta, void* stream) {
+  if (!params || !momentum || !params_out || !momentum_out) return fail(FTAR_ST_INVARIANT, "null optimizer state");
+  SgdArgs a;
+  a.p = params;
+  a.m = momentum;
+  a.po = params_out;
+  a.mo = momentum_out;
+  a.lr = lr;
+  a.beta = beta;
+  return launch_real(c, in, in_dtype, grad_out, n_elems, 0, n_elems, chunk_bytes, max_in_flight, scale, flags,
+                     stream, &a);
+}
+
+static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, uint64_t n_elems,
+                       uint64_t base_elem, uint64_t total_elems, uint64_t chunk_bytes, int max_in_flight,
+                       float scale, uint32_t flags, void* stream, const SgdArgs* sgd) {
   if (base_elem + n_elems > total_elems) return fail(FTAR_ST_INVARIANT, "range exceeds the bucket");
   if (!c) return fail(FTAR_ST_INVARIANT, "null ctx");
   int v = validate_common(in_dtype, c->n, chunk_bytes, max_in_flight);
@@ -1542,7 +1684,7 @@ int ftar_allreduce_launch_range(ftar_ctx* c, const void* in, int in_dtype, float
   const uint64_t in_bytes = n_elems * esz;
   if (in_bytes > c->max_bucket_bytes || n_elems * 4 > 2 * c->max_bucket_bytes)
     return fail(FTAR_ST_INVARIANT, "bucket exceeds the ring group's arena capacity");
-  if (n_elems && (!in || !out)) return fail(FTAR_ST_INVARIANT, "null buffer");
+  if (n_elems && (!in || (!out && !sgd))) return fail(FTAR_ST_INVARIANT, "null buffer");
   DeviceGuard g(c->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   c->seq += 1;
@@ -1578,11 +1720,20 @@ int ftar_allreduce_launch_range(ftar_ctx* c, const void* in, int in_dtype, float
     // the caller as soon as the call returns)
     const uint64_t o0 = reinterpret_cast<uint64_t>(out), i0 = reinterpret_cast<uint64_t>(in);
     const bool alias = o0 < i0 + in_bytes && i0 < o0 + n_elems * 4;
-    if (!alias && n_elems && !env_int("FTAR_NO_DIRECT", 0)) p.flags |= kFlagDirect;
+    if (out && !alias && n_elems && !env_int("FTAR_NO_DIRECT", 0)) p.flags |= kFlagDirect;
+    if (sgd) {
+      p.flags |= kFlagSGD;
+      p.sgd_p[c->self] = sgd->p;
+      p.sgd_m[c->self] = sgd->m;
+      p.sgd_po[c->self] = sgd->po;
+      p.sgd_mo[c->self] = sgd->mo;
+      p.sgd_lr = sgd->lr;
+      p.sgd_beta = sgd->beta;
+    }
     // push mode needs `out` inside my exported arena (peers write into it)
     const char* op = reinterpret_cast<const char*>(out);
     const bool out_reg = op >= c->arena + c->pool_off && op + n_elems * 4 <= c->arena + c->arena_bytes;
-    if ((p.flags & kFlagDirect) && out_reg && !env_int("FTAR_NO_PUSH", 0)) {
+    if (!sgd && (p.flags & kFlagDirect) && out_reg && !env_int("FTAR_NO_PUSH", 0)) {
       p.flags |= kFlagPush;
       p.out_off[c->self] = (uint64_t)(op - c->arena);
     }
@@ -1606,11 +1757,39 @@ int ftar_allreduce_launch_range(ftar_ctx* c, const void* in, int in_dtype, float
   return FTAR_OK;
 }
 
+static int launch_local(ftar_ctx** ctxs, int n, const void* const* ins, int in_dtype, float* const* outs,
+                        uint64_t n_elems, uint64_t base_elem, uint64_t total_elems, uint64_t chunk_bytes,
+                        int max_in_flight, float scale, uint32_t flags, uint32_t contrib_mask, int fault_member,
+                        int fault_after_tiles, void* stream, const float* const* sgd_p, const float* const* sgd_m,
+                        float* const* sgd_po, float* const* sgd_mo, float lr, float beta);
+
 int ftar_local_allreduce_launch_range(ftar_ctx** ctxs, int n, const void* const* ins, int in_dtype,
                                       float* const* outs, uint64_t n_elems, uint64_t base_elem,
                                       uint64_t total_elems, uint64_t chunk_bytes, int max_in_flight,
                                       float scale, uint32_t flags, uint32_t contrib_mask, int fault_member,
                                       int fault_after_tiles, void* stream) {
+  return launch_local(ctxs, n, ins, in_dtype, outs, n_elems, base_elem, total_elems, chunk_bytes, max_in_flight,
+                      scale, flags, contrib_mask, fault_member, fault_after_tiles, stream, nullptr, nullptr, nullptr,
+                      nullptr, 0.f, 0.f);
+}
+
+int ftar_local_allreduce_sgd_launch(ftar_ctx** ctxs, int n, const void* const* ins, int in_dtype,
+                                    float* const* grad_outs, uint64_t n_elems, uint64_t chunk_bytes,
+                                    int max_in_flight, float scale, uint32_t flags, uint32_t contrib_mask,
+                                    const float* const* params, const float* const* momentum,
+                                    float* const* params_out, float* const* momentum_out, float lr, float beta,
+                                    void* stream) {
+  if (!params || !momentum || !params_out || !momentum_out) return fail(FTAR_ST_INVARIANT, "null optimizer state");
+  return launch_local(ctxs, n, ins, in_dtype, grad_outs, n_elems, 0, n_elems, chunk_bytes, max_in_flight, scale,
+                      flags | FTAR_F_PROTOCOL, contrib_mask, -1, 0, stream, params, momentum, params_out,
+                      momentum_out, lr, beta);
+}
+
+static int launch_local(ftar_ctx** ctxs, int n, const void* const* ins, int in_dtype, float* const* outs,
+                        uint64_t n_elems, uint64_t base_elem, uint64_t total_elems, uint64_t chunk_bytes,
+                        int max_in_flight, float scale, uint32_t flags, uint32_t contrib_mask, int fault_member,
+                        int fault_after_tiles, void* stream, const float* const* sgd_p, const float* const* sgd_m,
+                        float* const* sgd_po, float* const* sgd_mo, float lr, float beta) {
   if (base_elem + n_elems > total_elems) return fail(FTAR_ST_INVARIANT, "range exceeds the bucket");
   int v = validate_common(in_dtype, n, chunk_bytes, max_in_flight);
   if (v) return v;
@@ -1648,14 +1827,27 @@ int ftar_local_allreduce_launch_range(ftar_ctx** ctxs, int n, const void* const*
   p.flags = flags & 0xffu;
   {
     const uint64_t ib = n_elems * (in_dtype == FTAR_DT_BF16 ? 2 : 4), ob = n_elems * 4;
-    bool alias = false;
-    for (int i = 0; i < n && !alias; ++i)
+    bool alias = false, null_out = false;
+    for (int i = 0; i < n && !alias; ++i) {
+      null_out |= outs[i] == nullptr;
       for (int j = 0; j < n && !alias; ++j) {
         const uint64_t o0 = reinterpret_cast<uint64_t>(outs[i]), i0 = reinterpret_cast<uint64_t>(ins[j]);
         alias = o0 < i0 + ib && i0 < o0 + ob;
       }
-    if (!alias && n_elems) p.flags |= kFlagDirect;
-    if ((p.flags & kFlagDirect) && !env_int("FTAR_NO_PUSH", 0)) {
+    }
+    if (!alias && !null_out && n_elems) p.flags |= kFlagDirect;
+    if (sgd_p) {
+      p.flags |= kFlagSGD;
+      for (int i = 0; i < n; ++i) {
+        p.sgd_p[i] = sgd_p[i];
+        p.sgd_m[i] = sgd_m[i];
+        p.sgd_po[i] = sgd_po[i];
+        p.sgd_mo[i] = sgd_mo[i];
+      }
+      p.sgd_lr = lr;
+      p.sgd_beta = beta;
+    }
+    if (!sgd_p && (p.flags & kFlagDirect) && !env_int("FTAR_NO_PUSH", 0)) {
       p.flags |= kFlagPush;  // in-process: every member's out is addressable
       for (int i = 0; i < n; ++i)
         p.out_off[i] = (uint64_t)(reinterpret_cast<const char*>(outs[i]) - ctxs[i]->arena);

@@ -502,6 +502,53 @@ def ftar_all_reduce_async(group: RingGroup, buf: torch.Tensor, step: int, cfg: P
     return p
 
 
+def ftar_all_reduce_sgd(group: RingGroup, grad: torch.Tensor, step: int, cfg: PipelineConfig | None = None, *,
+                        params: torch.Tensor, momentum: torch.Tensor, lr: float, beta: float,
+                        scale: float | None = None, params_out: torch.Tensor | None = None,
+                        momentum_out: torch.Tensor | None = None, grad_out: torch.Tensor | None = None):
+    """the all-reduce with normalisation and the
+    SGD-momentum step fused in.  g = sum x f32(scale) (replica.py:622-626);
+    m' = f32(m * f32(beta)) + g; p' = p - f32(f32(lr) * m') (model.py:146-155),
+    every fp32 op separately rounded.  Out of place: params/momentum are
+    never modified (the reference applies the optimizer only after its commit
+    vote, replica.py:616-633); returns (params_out, momentum_out).  grad_out
+    (optional, must not alias grad) receives g."""
+    cfg = cfg or PipelineConfig()
+    if group._local:
+        raise Fatal(INTERNAL_INVARIANT, "in-process groups: use LocalRing.all_reduce_sgd")
+    if not (isinstance(grad, torch.Tensor) and grad.is_cuda and grad.is_contiguous()):
+        raise Fatal(INTERNAL_INVARIANT, "gradient bucket must be a contiguous CUDA tensor")
+    code = _dtype_code(grad)
+    if grad_out is not None:
+        _check_buffers(grad, grad_out)
+    for t in (params, momentum):
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.numel() == grad.numel()):
+            raise Fatal(INTERNAL_INVARIANT, "params/momentum must be contiguous fp32 CUDA tensors shaped like grad")
+    params_out = torch.empty_like(params) if params_out is None else params_out
+    momentum_out = torch.empty_like(momentum) if momentum_out is None else momentum_out
+    if group.n > 1 and not group.links_ready():
+        raise Recoverable(PEER_RESET, "ring links not established")
+    q = group.__dict__.get("_pending")
+    while q:
+        q[0].wait()
+    flags = _lib.F_SCALE if scale is not None else 0
+    f_scale = _f32(scale) if scale is not None else 1.0
+    try:
+        rc = _lib.lib.ftar_allreduce_sgd_launch(
+            group.ctx, grad.data_ptr(), code, grad_out.data_ptr() if grad_out is not None else None, grad.numel(),
+            cfg.chunk_bytes, cfg.max_in_flight, f_scale, flags, params.data_ptr(), momentum.data_ptr(),
+            params_out.data_ptr(), momentum_out.data_ptr(), _f32(lr), _f32(beta), _stream_ptr(group.device))
+        _lib.check(rc, "ftar_allreduce_sgd_launch")
+        det = C.c_int(-1)
+        st = _lib.lib.ftar_wait(group.ctx, cfg.per_chunk_timeout_s, C.byref(det))
+        if st:
+            raise from_status(st, _lib.last_error() if st == 10 else "")
+    except FtdpError:
+        group.close_links()
+        raise
+    return params_out, momentum_out
+
+
 def _host_all_reduce(group, buf, step, cfg, out, scale):
     """Host (numpy / CPU tensor) buffers: the reference's exact call shape.
     One process per GPU: chunked H2D / range all-reduce / D2H pipeline.
@@ -803,6 +850,33 @@ class LocalRing:
                     raise from_status(st)
 
         return pipe.run(hosts, [_as_host_tensor(o) for o in outs] if outs is not None else None, launch, wait)
+
+    def all_reduce_sgd(self, bufs, cfg: PipelineConfig | None = None, *, params, momenta, lr: float, beta: float,
+                       scale=None, params_out=None, momenta_out=None, grad_outs=None):
+        """In-process form of ftar_all_reduce_sgd (protocol kernel): every
+        member's (params, momentum) updated out of place with its reduced,
+        scaled gradient."""
+        cfg = cfg or PipelineConfig()
+        n = len(bufs)
+        groups = self.groups[:n]
+        code = _dtype_code(bufs[0])
+        params_out = params_out if params_out is not None else [torch.empty_like(t) for t in params]
+        momenta_out = momenta_out if momenta_out is not None else [torch.empty_like(t) for t in momenta]
+        flags = _lib.F_SCALE if scale is not None else 0
+        f_scale = _f32(scale) if scale is not None else 1.0
+        for g in groups:
+            g._seq += 1
+        arr = lambda ts: (C.c_void_p * n)(*[t.data_ptr() if t is not None else None for t in ts])  # noqa: E731
+        ctxs = (C.c_void_p * n)(*[g.ctx for g in groups])
+        rc = _lib.lib.ftar_local_allreduce_sgd_launch(
+            ctxs, n, arr(bufs), code, arr(grad_outs if grad_outs is not None else [None] * n), bufs[0].numel(),
+            cfg.chunk_bytes, cfg.max_in_flight, f_scale, flags, groups[0]._contrib_mask, arr(params), arr(momenta),
+            arr(params_out), arr(momenta_out), _f32(lr), _f32(beta), _stream_ptr(groups[0].device))
+        _lib.check(rc, "ftar_local_allreduce_sgd_launch")
+        for st in self.wait(ctxs, cfg):
+            if st:
+                raise from_status(st)
+        return params_out, momenta_out
 
     def close(self):
         for g in self.groups:

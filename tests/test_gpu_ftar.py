@@ -473,3 +473,36 @@ def test_dropin_numpy_buffers_threaded(ftar):
             np.testing.assert_array_equal(bufs[r], want)
     finally:
         ring.close()
+
+
+# ---------------------------------------------------------------------------
+# §8f rank 1: normalisation + SGD-momentum fused into the collective.
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_fused_sgd_momentum_bit_exact(ftar, rings, dtype):
+    """model.optimizer_step(grad * f32(1/(h*R))) (model.py:146-155,
+    replica.py:622-633) on every member, bit for bit, out of place."""
+    n, e = 4, 1_000_003
+    arrays = member_inputs(n, e, seed=41, dtype=dtype)
+    ring = rings(n, protocol=True)
+    ring.reconfig()
+    rng = np.random.default_rng(42)
+    p0 = rng.standard_normal(e).astype(np.float32)
+    m0 = (rng.standard_normal(e) * 0.1).astype(np.float32)
+    lr, beta, denom = 0.05, 0.9, n * 2
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    bufs = [to_dev(a, tdt) for a in arrays]
+    params = [to_dev(p0) for _ in range(n)]
+    moms = [to_dev(m0) for _ in range(n)]
+    gouts = [torch.empty(e, device=DEV) for _ in range(n)]
+    pout, mout = ring.all_reduce_sgd(bufs, params=params, momenta=moms, lr=lr, beta=beta, scale=1.0 / denom,
+                                     grad_outs=gouts)
+    g = orc.normalize(orc.oracle_reduce(arrays, 8 << 20, 4), denom)
+    pw, mw = orc.sgd_momentum(p0.copy(), m0.copy(), g, beta, lr)
+    for i in range(n):
+        np.testing.assert_array_equal(gouts[i].cpu().numpy(), g)
+        np.testing.assert_array_equal(pout[i].cpu().numpy(), pw)
+        np.testing.assert_array_equal(mout[i].cpu().numpy(), mw)
+        np.testing.assert_array_equal(params[i].cpu().numpy(), p0)  # inputs untouched (commit is the caller's)
+        np.testing.assert_array_equal(moms[i].cpu().numpy(), m0)

@@ -139,6 +139,22 @@ def _worker(rank, world, port, scenario, outdir):
             ftar.ftar_all_reduce(group, hb, 2, cfg, out=ho, scale=1.0 / world)
             want16 = orc.normalize(orc.oracle_reduce(arrays16, cfg.chunk_bytes, cfg.max_in_flight), world)
             (res["ok"] if np.array_equal(ho.numpy(), want16) else res["errors"]).append("host_bf16")
+        elif scenario == "sgd":
+            # §8f: all-reduce + normalisation + SGD-momentum fused, bit-exact
+            group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, 1, deadline_s=30)
+            e = 3_000_001
+            arrays = member_inputs(world, e, seed=51, dtype="bf16")
+            rng = np.random.default_rng(52)
+            p0 = rng.standard_normal(e).astype(np.float32)
+            m0 = (rng.standard_normal(e) * 0.1).astype(np.float32)
+            g = torch.from_numpy(arrays[rank]).to(dev).to(torch.bfloat16)
+            pt, mt = torch.from_numpy(p0).to(dev), torch.from_numpy(m0).to(dev)
+            po, mo = ftar.ftar_all_reduce_sgd(group, g, 1, params=pt, momentum=mt, lr=0.01, beta=0.9,
+                                              scale=1.0 / world)
+            gw = orc.normalize(orc.oracle_reduce(arrays, 8 << 20, 4), world)
+            pw, mw = orc.sgd_momentum(p0.copy(), m0.copy(), gw, 0.9, 0.01)
+            good = np.array_equal(po.cpu().numpy(), pw) and np.array_equal(mo.cpu().numpy(), mw)
+            (res["ok"] if good else res["errors"]).append("sgd")
         elif scenario == "catchup":
             from paper_2602_00277_b200 import checkpoint as ck
             snap = ck.SnapshotStore(capacity_bytes=64 << 20, device=dev, fabric=fabric, rank=0, replica_id=rank)
@@ -214,6 +230,13 @@ def test_host_buffers_over_nvlink():
     for r in res:
         assert not r["errors"], r["errors"]
         assert "host_inplace" in r["ok"] and "host_bf16" in r["ok"]
+
+
+def test_fused_sgd_over_nvlink():
+    res = run("sgd", world_size())
+    for r in res:
+        assert not r["errors"], r["errors"]
+        assert "sgd" in r["ok"]
 
 
 def test_catchup_pull_over_nvlink():
