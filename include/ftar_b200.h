@@ -215,6 +215,13 @@ int ftar_snap_import(ftar_snap* local, int slot, const void* handle, size_t len,
 int ftar_snap_pull_launch(ftar_snap* local, int slot, const ftar_snap* src_local,
                           uint64_t want_step, void* dst_params, uint64_t pbytes,
                           void* dst_momentum, uint64_t mbytes, int ctas, void* stream);
+/* Striped pull: chunk c comes from donor slots[c % nslots] (every healthy
+ * replica holds the same retention-1 snapshot), spreading the catch-up over
+ * all donors' NVLink egress.  nslots <= 8. */
+int ftar_snap_pull_multi_launch(ftar_snap* local, const int* slots, int nslots,
+                                const ftar_snap* src_local, uint64_t want_step, void* dst_params,
+                                uint64_t pbytes, void* dst_momentum, uint64_t mbytes, int ctas,
+                                void* stream);
 int ftar_snap_poll(ftar_snap* s, int* status, uint64_t* progress, int64_t* available);
 int ftar_snap_abort(ftar_snap* s);
 int ftar_snap_wait(ftar_snap* s, double progress_timeout_s, int64_t* available);

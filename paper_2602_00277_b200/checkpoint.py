@@ -190,22 +190,27 @@ def catchup_stream(device: torch.device) -> torch.cuda.Stream:
 def start_fetch(local: SnapshotStore, donor, step: int, rank: int, params_out: torch.Tensor,
                 momentum_out: torch.Tensor, timeout_s: float = 5.0, ctas: int = 16) -> CatchupPull:
     """Launch the pull of `donor`'s snapshot of `step` into the given tensors
-    without waiting.  `donor` is a SnapshotStore in this process (same device)
-    or a replica id resolved through ``local.fabric``."""
+    without waiting.  `donor` is a SnapshotStore in this process (same device),
+    a replica id resolved through ``local.fabric``, or a list of replica ids:
+    the pull is then striped across all of them (every healthy replica holds
+    the same retention-1 snapshot), so no single donor's NVLink egress carries
+    the whole catch-up."""
     p, m = _as_bytes_tensor(params_out), _as_bytes_tensor(momentum_out)
     pb, mb = p.numel() * p.element_size(), m.numel() * m.element_size()
     if local.handle is None:
         local._alloc(max(pb + mb, 16))
     if isinstance(donor, SnapshotStore):
-        slot, src = -1, donor.handle
+        slots, src = [], donor.handle
         if src is None:
             raise SnapshotUnavailable(None)
     else:
-        slot, src = local._map_donor(int(donor), rank, timeout_s), None
+        donors = list(donor) if isinstance(donor, (list, tuple)) else [donor]
+        slots, src = [local._map_donor(int(d), rank, timeout_s) for d in donors], None
     stream = catchup_stream(local.device)
     stream.wait_stream(torch.cuda.current_stream(local.device))
-    rc = _lib.lib.ftar_snap_pull_launch(local.handle, slot, src, step, p.data_ptr(), pb, m.data_ptr(), mb,
-                                        ctas, stream.cuda_stream)
+    arr = (C.c_int * max(1, len(slots)))(*slots)
+    rc = _lib.lib.ftar_snap_pull_multi_launch(local.handle, arr, len(slots), src, step, p.data_ptr(), pb,
+                                              m.data_ptr(), mb, ctas, stream.cuda_stream)
     _lib.check(rc, "ftar_snap_pull_launch")
     return CatchupPull(local, p, m, stream, timeout_s)
 

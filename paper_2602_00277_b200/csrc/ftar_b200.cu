@@ -881,41 +881,52 @@ __global__ void __launch_bounds__(kThreads) snap_copy_kernel(char* dst, const ch
   copy_bytes_grid(dst + pb, m, mb, first, stride);
 }
 
-// Pull a donor snapshot (over NVLink when `src` is a peer mapping) in chunks,
-// honouring the host abort word, publishing progress, and validating the
-// donor's seqlock across the whole pull.
+// Pull a snapshot (over NVLink when the sources are peer mappings) in 1 MiB
+// chunks striped across `nsrc` donors (all healthy replicas hold the same
+// retention-1 snapshot, so chunk c can come from donor c % nsrc and no single
+// donor's NVLink egress carries the whole catch-up).  Honours the host abort
+// word, publishes progress, and validates every donor's seqlock across the
+// whole pull (a re-capture mid-pull = torn = SnapshotUnavailable).
 constexpr uint64_t kPullChunk = 1ull << 20;
 
+struct PullSrcs {
+  const char* arena[kMaxMembers];
+  int n;
+};
+
 __global__ void __launch_bounds__(kThreads, 1)
-snap_pull_kernel(const char* src_arena, SnapHdr* lhdr, HostCtl* ctl, uint64_t tag, int64_t want,
+snap_pull_kernel(const __grid_constant__ PullSrcs src, SnapHdr* lhdr, HostCtl* ctl, uint64_t tag, int64_t want,
                  char* dp, uint64_t pb, char* dm, uint64_t mb) {
-  const SnapHdr* sh = reinterpret_cast<const SnapHdr*>(src_arena);
-  const char* data = src_arena + kSnapHdrBytes;
   __shared__ uint32_t s_st;
-  __shared__ uint64_t s_seq;
   const int tid = threadIdx.x;
   if (tid == 0) {
     if (blockIdx.x == 0) ctl->started = tag;
     s_st = ST_OK;
-    const uint64_t seq = ld_acquire_sys(&sh->seq);
-    const int64_t step = (int64_t)ld_relaxed_sys(reinterpret_cast<const uint64_t*>(&sh->step));
-    const uint64_t spb = ld_relaxed_sys(&sh->pbytes), smb = ld_relaxed_sys(&sh->mbytes);
-    if ((seq & 1u) || step != want || spb != pb || smb != mb) {
-      s_st = ST_UNAVAILABLE;
-      if (blockIdx.x == 0) ctl->available = (seq & 1u) ? -1 : step;
+    for (int d = 0; d < src.n; ++d) {
+      const SnapHdr* sh = reinterpret_cast<const SnapHdr*>(src.arena[d]);
+      const uint64_t seq = ld_acquire_sys(&sh->seq);
+      const int64_t step = (int64_t)ld_relaxed_sys(reinterpret_cast<const uint64_t*>(&sh->step));
+      const uint64_t spb = ld_relaxed_sys(&sh->pbytes), smb = ld_relaxed_sys(&sh->mbytes);
+      if ((seq & 1u) || step != want || spb != pb || smb != mb) {
+        s_st = ST_UNAVAILABLE;
+        if (blockIdx.x == 0) ctl->available = (seq & 1u) ? -1 : step;
+      }
+      atomicMin(reinterpret_cast<unsigned long long*>(&lhdr->seq_min[d]), (unsigned long long)seq);
+      atomicMax(reinterpret_cast<unsigned long long*>(&lhdr->seq_max[d]), (unsigned long long)seq);
     }
-    s_seq = seq;
-    atomicMin(reinterpret_cast<unsigned long long*>(&lhdr->seq_min), (unsigned long long)seq);
-    atomicMax(reinterpret_cast<unsigned long long*>(&lhdr->seq_max), (unsigned long long)seq);
   }
   __syncthreads();
   const uint64_t total = pb + mb;
   const uint64_t nchunks = (total + kPullChunk - 1) / kPullChunk;
   if (s_st == ST_OK) {
-    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-      if (tid == 0 && (ctl->abort_tag == tag || ld_relaxed_sys32(&lhdr->err) != 0)) s_st = ST_ABORTED;
-      __syncthreads();
-      if (s_st != ST_OK) break;
+    uint32_t it = 0;
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+      if ((it & 7u) == 0) {  // abort word lives in host memory: check every 8 chunks
+        if (tid == 0 && (ctl->abort_tag == tag || ld_relaxed_sys32(&lhdr->err) != 0)) s_st = ST_ABORTED;
+        __syncthreads();
+        if (s_st != ST_OK) break;
+      }
+      const char* data = src.arena[c % (uint64_t)src.n] + kSnapHdrBytes;
       const uint64_t a = c * kPullChunk, b = umin(a + kPullChunk, total);
       // a chunk may straddle params|momentum
       if (a < pb) {
@@ -926,33 +937,33 @@ snap_pull_kernel(const char* src_arena, SnapHdr* lhdr, HostCtl* ctl, uint64_t ta
         const uint64_t s = umax(a, pb);
         copy_bytes_grid(dm + (s - pb), data + s, b - s, tid, kThreads);
       }
-      __syncthreads();
-      if (tid == 0) {
-        const unsigned long long v =
-            atomicAdd(reinterpret_cast<unsigned long long*>(&lhdr->bytes_done), (unsigned long long)(b - a)) +
-            (b - a);
-        ctl->progress = v;
-      }
+      if (tid == 0 && (it & 7u) == 7u) ctl->progress = ((uint64_t)blockIdx.x << 32) | it;
     }
   }
   __syncthreads();
   if (tid == 0) {
-    const uint64_t seq2 = ld_acquire_sys(&sh->seq);
-    atomicMax(reinterpret_cast<unsigned long long*>(&lhdr->seq_max), (unsigned long long)seq2);
+    for (int d = 0; d < src.n; ++d) {
+      const SnapHdr* sh = reinterpret_cast<const SnapHdr*>(src.arena[d]);
+      const uint64_t seq2 = ld_acquire_sys(&sh->seq);
+      atomicMax(reinterpret_cast<unsigned long long*>(&lhdr->seq_max[d]), (unsigned long long)seq2);
+    }
     if (s_st != ST_OK) atomicMax(&lhdr->err, s_st);
-    __threadfence_system();
+    __threadfence();
     const uint32_t old = atomicAdd(&lhdr->done_arrive, 1u);
     if (old == gridDim.x - 1) {
       __threadfence_system();
       uint32_t err = ld_relaxed_sys32(&lhdr->err);
-      const uint64_t smin = ld_relaxed_sys(&lhdr->seq_min), smax = ld_relaxed_sys(&lhdr->seq_max);
-      if (err == ST_OK && smin != smax) {  // donor re-captured mid-pull: torn
-        err = ST_UNAVAILABLE;
-        ctl->available = (int64_t)ld_relaxed_sys(reinterpret_cast<const uint64_t*>(&sh->step));
+      for (int d = 0; d < src.n; ++d) {
+        const uint64_t smin = ld_relaxed_sys(&lhdr->seq_min[d]), smax = ld_relaxed_sys(&lhdr->seq_max[d]);
+        if (err == ST_OK && smin != smax) {  // this donor re-captured mid-pull: torn
+          err = ST_UNAVAILABLE;
+          const SnapHdr* sh = reinterpret_cast<const SnapHdr*>(src.arena[d]);
+          ctl->available = (int64_t)ld_relaxed_sys(reinterpret_cast<const uint64_t*>(&sh->step));
+        }
+        lhdr->seq_min[d] = ~0ull;
+        lhdr->seq_max[d] = 0;
       }
-      ctl->progress = lhdr->bytes_done;
-      lhdr->seq_min = ~0ull;
-      lhdr->seq_max = 0;
+      ctl->progress = total;
       lhdr->err = 0;
       lhdr->done_arrive = 0;
       lhdr->bytes_done = 0;
@@ -1195,8 +1206,10 @@ __global__ void snap_init_kernel(SnapHdr* h) {
   h->seq = 0;
   h->step = -1;
   h->pbytes = h->mbytes = 0;
-  h->seq_min = ~0ull;
-  h->seq_max = 0;
+  for (int d = 0; d < kMaxMembers; ++d) {
+    h->seq_min[d] = ~0ull;
+    h->seq_max[d] = 0;
+  }
   h->done_arrive = 0;
   h->err = 0;
   h->bytes_done = 0;
@@ -2252,19 +2265,25 @@ int ftar_snap_import(ftar_snap* s, int slot, const void* handle, size_t len, uin
   return FTAR_OK;
 }
 
-int ftar_snap_pull_launch(ftar_snap* local, int slot, const ftar_snap* src_local, uint64_t want_step,
-                          void* dst_params, uint64_t pbytes, void* dst_momentum, uint64_t mbytes,
-                          int ctas, void* stream) {
+int ftar_snap_pull_multi_launch(ftar_snap* local, const int* slots, int nslots, const ftar_snap* src_local,
+                                uint64_t want_step, void* dst_params, uint64_t pbytes, void* dst_momentum,
+                                uint64_t mbytes, int ctas, void* stream) {
   if (!local) return fail(FTAR_ST_INVARIANT, "null snapshot");
   if (local->inflight && flag_tag(local->ctl_h->done) != local->cur_tag)
     return fail(FTAR_ST_INVARIANT, "one pull in flight per snapshot context");
-  const char* src = nullptr;
-  if (slot >= 0) {
-    if (slot >= kMaxSlots || !local->peer[slot]) return fail(FTAR_ST_INVARIANT, "donor not mapped");
-    src = local->peer[slot];
+  PullSrcs src{};
+  if (nslots > 0) {
+    if (nslots > kMaxMembers) return fail(FTAR_ST_INVARIANT, "too many donors");
+    for (int i = 0; i < nslots; ++i) {
+      const int slot = slots[i];
+      if (slot < 0 || slot >= kMaxSlots || !local->peer[slot]) return fail(FTAR_ST_INVARIANT, "donor not mapped");
+      src.arena[i] = local->peer[slot];
+    }
+    src.n = nslots;
   } else {
     if (!src_local) return fail(FTAR_ST_INVARIANT, "no donor");
-    src = src_local->arena;
+    src.arena[0] = src_local->arena;
+    src.n = 1;
   }
   DeviceGuard g(local->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -2283,6 +2302,13 @@ int ftar_snap_pull_launch(ftar_snap* local, int slot, const ftar_snap* src_local
     return cuda_fail(e, "snapshot pull launch");
   }
   return FTAR_OK;
+}
+
+int ftar_snap_pull_launch(ftar_snap* local, int slot, const ftar_snap* src_local, uint64_t want_step,
+                          void* dst_params, uint64_t pbytes, void* dst_momentum, uint64_t mbytes, int ctas,
+                          void* stream) {
+  return ftar_snap_pull_multi_launch(local, &slot, slot >= 0 ? 1 : 0, src_local, want_step, dst_params, pbytes,
+                                     dst_momentum, mbytes, ctas, stream);
 }
 
 int ftar_snap_poll(ftar_snap* s, int* status, uint64_t* progress, int64_t* available) {

@@ -102,7 +102,7 @@ struct alignas(128) SnapHdr {
   uint64_t seq;        // odd while a capture is writing
   int64_t step;        // -1 = nothing captured yet
   uint64_t pbytes, mbytes;
-  alignas(128) uint64_t seq_min, seq_max;  // pull-side consistency (local)
+  alignas(128) uint64_t seq_min[kMaxMembers], seq_max[kMaxMembers];  // pull-side, per donor (local)
   uint32_t done_arrive, err;
   uint64_t bytes_done;
 };

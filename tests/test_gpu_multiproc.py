@@ -158,21 +158,27 @@ def _worker(rank, world, port, scenario, outdir):
         elif scenario == "catchup":
             from paper_2602_00277_b200 import checkpoint as ck
             snap = ck.SnapshotStore(capacity_bytes=64 << 20, device=dev, fabric=fabric, rank=0, replica_id=rank)
+            rec = world - 1
+            donors = list(range(world - 1))
             g = torch.Generator(device=dev).manual_seed(3)
             p = torch.randn(8 << 20 >> 2, device=dev, generator=g)
             m = torch.randn(8 << 20 >> 2, device=dev, generator=g)
-            if rank == 0:
+            if rank != rec:  # every healthy replica holds the same retention-1 snapshot
                 snap.capture(5, p, m)
                 torch.cuda.synchronize()
-            store.set("captured", b"1")
-            store.wait(["captured"])
-            if rank == 1:
-                po, mo = torch.empty_like(p), torch.empty_like(m)
-                ck.fetch_shard(0, 5, 0, local=snap, out=(po, mo), timeout_s=10)
+            store.set(f"captured{rank}", b"1")
+            store.wait([f"captured{r}" for r in donors])
+            if rank == rec:
                 g0 = torch.Generator(device=dev).manual_seed(3)
                 wp = torch.randn(8 << 20 >> 2, device=dev, generator=g0)
                 wm = torch.randn(8 << 20 >> 2, device=dev, generator=g0)
+                po, mo = torch.empty_like(p), torch.empty_like(m)
+                ck.fetch_shard(0, 5, 0, local=snap, out=(po, mo), timeout_s=10)
                 (res["ok"] if torch.equal(po, wp) and torch.equal(mo, wm) else res["errors"]).append("pull")
+                po.zero_()
+                mo.zero_()
+                ck.start_fetch(snap, donors, 5, 0, po, mo, timeout_s=10).wait()  # striped over all donors
+                (res["ok"] if torch.equal(po, wp) and torch.equal(mo, wm) else res["errors"]).append("striped")
                 try:
                     ck.fetch_shard(0, 4, 0, local=snap, out=(po, mo), timeout_s=10)
                     res["errors"].append("stale step served")
@@ -240,9 +246,11 @@ def test_fused_sgd_over_nvlink():
 
 
 def test_catchup_pull_over_nvlink():
-    res = run("catchup", 2)
-    assert not res[1]["errors"], res[1]["errors"]
-    assert "pull" in res[1]["ok"] and "unavailable" in res[1]["ok"]
+    world = world_size()
+    res = run("catchup", world)
+    rec = res[world - 1]
+    assert not rec["errors"], rec["errors"]
+    assert {"pull", "striped", "unavailable"} <= set(rec["ok"])
 
 
 def _async_worker(rank, world, port, outdir):

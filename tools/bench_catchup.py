@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--bucket-mib", type=int, default=256)
     ap.add_argument("--ctas", type=str, default="8,16,32")
+    ap.add_argument("--stripe", action="store_true", help="stripe the pull over every healthy donor")
     args = ap.parse_args()
 
     import torch
@@ -54,7 +55,7 @@ def main():
     elems = args.bucket_mib * (1 << 20) // 4
 
     snap = ck.SnapshotStore(capacity_bytes=nbytes, device=dev, fabric=fabric, rank=0, replica_id=rank)
-    if rank == donor:
+    if rank != rec:  # every healthy replica holds the same retention-1 snapshot
         g = torch.Generator(device=dev).manual_seed(5)
         p = torch.randn(half, device=dev, generator=g)
         m = torch.randn(half, device=dev, generator=g)
@@ -96,13 +97,13 @@ def main():
         torch.cuda.synchronize()
         return s.elapsed_time(e) / k
 
-    def pull(ctas):
+    def pull(ctas, donors=None):
         s = torch.cuda.Event(enable_timing=True)
         e = torch.cuda.Event(enable_timing=True)
         side = ck.catchup_stream(dev)
         t0 = time.perf_counter()
         s.record(side)
-        h = ck.start_fetch(snap, donor, 41, 0, p_out, m_out, timeout_s=30, ctas=ctas)
+        h = ck.start_fetch(snap, donor if donors is None else donors, 41, 0, p_out, m_out, timeout_s=30, ctas=ctas)
         e.record(side)
         h.wait()
         torch.cuda.synchronize()
@@ -115,18 +116,22 @@ def main():
 
     if rank != rec:
         healthy_steps(5)
-    if rank == rec:
-        pull(16)  # warm-up: lazy peer mapping of the donor's snapshot arena
+    if rank == rec:  # warm-up: lazy peer mapping of the donors' snapshot arenas
+        pull(16)
+        if args.stripe and len(healthy) > 1:
+            pull(16, healthy)
     dist.barrier()
     base = mx(healthy_steps(args.steps) if rank != rec else 0.0)
     results = []
+    stripe = args.stripe and len(healthy) > 1
     for ctas in [int(c) for c in args.ctas.split(",")]:
         dist.barrier()
-        alone = pull(ctas)[0] if rank == rec else 0.0
+        dl = healthy if stripe else None
+        alone = pull(ctas, dl)[0] if rank == rec else 0.0
         alone = mx(alone)
         dist.barrier()
         if rank == rec:
-            loaded_ms, wall = pull(ctas)
+            loaded_ms, wall = pull(ctas, dl)
             step = 0.0
         else:
             step = healthy_steps(args.steps)
@@ -144,7 +149,8 @@ def main():
                         "pull_ms_under_load": round(loaded_ms, 3), "ms_per_GB_under_load": round(loaded_ms / gb, 3),
                         "healthy_step_ms_baseline": round(base, 4), "healthy_step_ms_during_pull": round(step, 4),
                         "healthy_replicas": len(healthy), "bucket_mib": args.bucket_mib,
-                        "pull_bit_exact": ok, "n_gpus": world})
+                        "pull_bit_exact": ok, "n_gpus": world,
+                        "donors": healthy if stripe else [donor]})
     if rank == 0:
         for r in results:
             print(json.dumps(r), flush=True)
