@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         s_blame = me;
       }
       ctl->started = tag;
-      ctl->tphase[0] = s_t0;
+      hdr->tph[0] = s_t0;
       if (s_status == ST_OK) {
         EntryRec* en = &hdr->entry;
         en->in_off = p.in_off[me];
@@ -587,8 +587,8 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         hdr->vec_ok = (orbits & 15u) == 0;
         st_release_gpu(&hdr->go, mk_flag(tag, 1));
       }
-      ctl->tphase[1] = globaltimer_ns();
-      hdr->dbg_t1 = ctl->tphase[1];
+      hdr->tph[1] = globaltimer_ns();
+      hdr->dbg_t1 = hdr->tph[1];
     } else {
       const uint32_t st = wait_go(hdr, mk_flag(tag, 1), s_t0, p.hard_timeout_ns);
       if (st != ST_OK) s_status = st;
@@ -650,26 +650,27 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
     // above, before the counter); the last CTA then publishes with ONE
     // sys-scope fence + release store, which is cumulative over everything
     // the counter chain made it observe.  Per-CTA sys fences cost ~100 us.
-    __threadfence();
-    const uint32_t old = atomicAdd(&hdr->rs_arrive, 1u);
+    if (gridDim.x > 1) __threadfence();  // my CTA's writes before the arrival counter
+    const uint32_t old = gridDim.x > 1 ? atomicAdd(&hdr->rs_arrive, 1u) : 0u;
     if (old == gridDim.x - 1) {
-      __threadfence();
+      // ONE sys-scope acq_rel fence: acquires the other CTAs' writes through
+      // the counter and releases everything before the relaxed flag stores
       hdr->dbg_fence[0] = globaltimer_ns();
-      __threadfence_system();
+      fence_acq_rel_sys();
       hdr->dbg_fence[1] = globaltimer_ns();
       if (ld_relaxed_sys32(&hdr->err) == 0) {
         const uint32_t bits = ld_relaxed_sys32(&hdr->nonfinite) ? kBitNonFinite : 0u;
-        st_release_sys(&hdr->rs_done, mk_flag(tag, bits));
+        st_relaxed_sys(&hdr->rs_done, mk_flag(tag, bits));
         if (s_push) {
-          // my whole slice is in every peer's out: tell them (the sys fence
-          // above made all my CTAs' posted writes visible first)
+          // my whole slice is in every peer's out: tell them (the fence above
+          // made all my CTAs' posted writes visible first)
           for (int j = 0; j < N; ++j) {
             if (j == me) continue;
             ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
-            st_release_sys(&ph->ag_in[me], mk_flag(tag, bits));
+            st_relaxed_sys(&ph->ag_in[me], mk_flag(tag, bits));
           }
         }
-        ctl->tphase[2] = globaltimer_ns();
+        hdr->tph[2] = globaltimer_ns();
       }
       ctl->progress = hdr->tiles_done;
     }
@@ -698,7 +699,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         }
         bits |= b;
       }
-      ctl->tphase[3] = globaltimer_ns();
+      hdr->tph[3] = globaltimer_ns();
       if (s_status == ST_OK && (bits & kBitNonFinite)) s_status = ST_NUMERICAL;
     }
     __syncthreads();
@@ -723,7 +724,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
           hdr->peer_bits = bits;
           st_release_gpu(&hdr->go, mk_flag(tag, 2));
         }
-        ctl->tphase[3] = globaltimer_ns();
+        hdr->tph[3] = globaltimer_ns();
       } else {
         const uint32_t st = wait_go(hdr, mk_flag(tag, 2), s_t0, p.hard_timeout_ns);
         if (st != ST_OK) s_status = st;
@@ -749,7 +750,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         mask |= 1u << j;
         st_release_gpu(&hdr->go2, mk_flag(tag, mask));
       }
-      ctl->tphase[3] = globaltimer_ns();
+      hdr->tph[3] = globaltimer_ns();
       if (s_status == ST_OK && (bits & kBitNonFinite)) s_status = ST_NUMERICAL;
     }
     __syncthreads();
@@ -790,18 +791,18 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
       hdr->err_peer = s_blame;
       if (st != ST_INJECTED && st != ST_NUMERICAL) st_release_sys(&hdr->poison, mk_flag(tag, st));
     }
-    __threadfence();
-    const uint32_t old = atomicAdd(&hdr->done_arrive, 1u);
+    if (gridDim.x > 1) __threadfence();
+    const uint32_t old = gridDim.x > 1 ? atomicAdd(&hdr->done_arrive, 1u) : 0u;
     if (old == gridDim.x - 1) {
-      __threadfence();
       hdr->dbg_fence[2] = globaltimer_ns();
-      __threadfence_system();
+      fence_acq_rel_sys();
       hdr->dbg_fence[3] = globaltimer_ns();
       const uint32_t err = ld_relaxed_sys32(&hdr->err);
       const uint64_t tiles = hdr->tiles_done;
       ctl->detail = err ? (int64_t)hdr->err_peer : -1;
       ctl->progress = tiles + 1;
-      ctl->tphase[4] = globaltimer_ns();
+      hdr->tph[4] = globaltimer_ns();
+      for (int i = 0; i < 5; ++i) ctl->tphase[i] = hdr->tph[i];
       hdr->rs_arrive = 0;
       hdr->done_arrive = 0;
       hdr->nonfinite = 0;
@@ -1760,7 +1761,15 @@ static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, ui
   p.rs_layout = rs_layout();
   p.diag = diag_mode();
   p.rs_ctas = rs_ctas_knob();
-  const dim3 grid(real_ctas((p.flags & kFlagPush) != 0), 1);
+  // small buckets: fewer CTAs (CTA arrival + fences dominate); ~256 KB of
+  // my slice per CTA, at least 1, at most the tuned shape
+  int G = real_ctas((p.flags & kFlagPush) != 0);
+  {
+    const uint64_t slice_bytes = p.slice * (uint64_t)esz;
+    const uint64_t want = (slice_bytes + (256ull << 10) - 1) / (256ull << 10);
+    if (g_ctas <= 0 && want < (uint64_t)G) G = (int)std::max<uint64_t>(1, want);
+  }
+  const dim3 grid(G, 1);
   cudaError_t e = in_dtype == FTAR_DT_BF16 ? launch_dispatch<BF16In>(c->n, p, grid, st, false)
                                             : launch_dispatch<F32In>(c->n, p, grid, st, false);
   if (e != cudaSuccess) {

@@ -69,6 +69,7 @@ struct alignas(128) ArenaHdr {
   uint64_t dbg_ag_end[256];               // per-CTA %globaltimer at end of all-gather
   uint64_t dbg_t1;                        // entry barrier passed (block 0)
   uint64_t dbg_fence[4];                  // last CTA: before/after the sys fence (RS, end)
+  uint64_t tph[6];                        // phase stamps (device copy; host gets them at completion)
   alignas(128) uint64_t go;               // CTA 0 -> local CTAs: (tag << 8) | barrier passed
   uint64_t peer_in[kMaxMembers];          // entry barrier result: member inputs (my VA)
   uint64_t peer_res[kMaxMembers];         // and member result slices (my VA)
