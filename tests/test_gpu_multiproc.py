@@ -155,6 +155,44 @@ def _worker(rank, world, port, scenario, outdir):
             pw, mw = orc.sgd_momentum(p0.copy(), m0.copy(), gw, 0.9, 0.01)
             good = np.array_equal(po.cpu().numpy(), pw) and np.array_equal(mo.cpu().numpy(), mw)
             (res["ok"] if good else res["errors"]).append("sgd")
+        elif scenario == "death":
+            # a member PROCESS dies with its kernel in flight and its arena
+            # still mapped by the others: survivors get Recoverable (no CUDA
+            # fault), their contexts stay usable, and they regroup without it
+            import time
+            victim = world - 1
+            group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, 1, deadline_s=30)
+            e = 2 << 20  # 8 MiB: fits the test pool
+            b = group.alloc_bucket(e)
+            b.fill_(1.0)
+            o = torch.empty(e, device=dev)
+            ftar.ftar_all_reduce(group, b, 0, out=o)
+            torch.cuda.synchronize()
+            store.set(f"armed{rank}", b"1")
+            store.wait([f"armed{r}" for r in range(world)])
+            cfg = ftar.PipelineConfig(per_chunk_timeout_s=1.0)
+            if rank == victim:
+                res["ok"].append("victim")
+                with open(os.path.join(outdir, f"r{rank}.json"), "w") as f:
+                    json.dump(res, f)
+                ftar.ftar_all_reduce_async(group, b, 1, cfg, out=o)
+                time.sleep(0.0002)
+                os._exit(0)
+            t0 = time.monotonic()
+            try:
+                for i in range(3):
+                    ftar.ftar_all_reduce(group, b, 1 + i, cfg, out=o)
+                res["errors"].append("no error")
+            except errors.Recoverable:
+                if time.monotonic() - t0 > 2 * cfg.per_chunk_timeout_s + 1.0:
+                    res["errors"].append("slow")
+                res["ok"].append("recoverable")
+            survivors = [r for r in range(world) if r != victim]
+            group.reconfig({r: ftar.PeerAddress(r) for r in survivors}, 2, deadline_s=30)
+            b.fill_(1.0)
+            ftar.ftar_all_reduce(group, b, 9, cfg, out=o)
+            (res["ok"] if torch.all(o == float(len(survivors))).item() else res["errors"]).append("regrouped")
+            store.set(f"fin{victim}", b"1")  # the victim cannot
         elif scenario == "catchup":
             from paper_2602_00277_b200 import checkpoint as ck
             snap = ck.SnapshotStore(capacity_bytes=64 << 20, device=dev, fabric=fabric, rank=0, replica_id=rank)
@@ -243,6 +281,14 @@ def test_fused_sgd_over_nvlink():
     for r in res:
         assert not r["errors"], r["errors"]
         assert "sgd" in r["ok"]
+
+
+def test_member_process_death_is_recoverable():
+    world = world_size()
+    res = run("death", world)
+    for r in res[:-1]:
+        assert not r["errors"], r["errors"]
+        assert "recoverable" in r["ok"] and "regrouped" in r["ok"]
 
 
 def test_catchup_pull_over_nvlink():
