@@ -47,6 +47,7 @@ constexpr uint32_t ST_FOLLOW = 254;  // stop because another CTA of mine failed
 constexpr uint32_t kFlagDirect = 1u << 8;  // internal launch flag: RS writes my slice of out
 constexpr uint32_t kFlagPush = 1u << 9;    // internal: all-gather by posted writes into peers' outs
 constexpr uint32_t kFlagSGD = 1u << 10;    // internal: apply SGD-momentum to the reduced gradient
+constexpr uint32_t kFlagSmallDirect = 1u << 11;  // internal: small one-shot folds straight into out
 
 struct LaunchParams {
   char* base[kMaxMembers];       // arena base of ring member i, as mapped here
@@ -407,6 +408,33 @@ __device__ __forceinline__ int fold_tiles(const LaunchParams& p, const typename 
 
 // Grid-stride fp32 copy (the all-gather pull), 16-byte vectors, UA loads in
 // flight per thread before the stores.
+// Byte copy of [0, bytes) with 16-byte vectors when aligned.
+__device__ __forceinline__ void copy_bytes_grid(char* dst, const char* src, uint64_t bytes,
+                                                uint64_t first, uint64_t stride) {
+  const bool vec = ((reinterpret_cast<uint64_t>(dst) | reinterpret_cast<uint64_t>(src)) & 15u) == 0;
+  if (!vec) {
+    for (uint64_t i = first; i < bytes; i += stride) dst[i] = src[i];
+    return;
+  }
+  const uint64_t nv = bytes >> 4;
+  constexpr int UA = 8;
+  for (uint64_t v = first; v < nv; v += stride * UA) {
+    uint4 r[UA];
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      const uint64_t i = v + (uint64_t)u * stride;
+      if (i < nv) r[u] = ld_stream(src + i * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      const uint64_t i = v + (uint64_t)u * stride;
+      if (i < nv) *reinterpret_cast<uint4*>(dst + i * 16) = r[u];
+    }
+  }
+  const uint64_t t = (nv << 4) + first;
+  if (t < bytes && first < 16) dst[t] = src[t];
+}
+
 // All-gather pull of a reduced slice straight into the optimizer update
 // (gradient never stored unless dst != nullptr).
 template <int UA>
@@ -815,6 +843,170 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
   }
 }
 
+
+// ---------------------------------------------------------------- small buckets
+// Push one-shot (input <= kSmallMax bytes): every member posts its whole
+// input into every peer's receive slot [seq parity][sender] and raises
+// sm_in[sender] (with a call fingerprint in sm_meta); then waits for the
+// N-1 peers' flags and folds all N copies LOCALLY in the reference order into
+// the result region, committing to `out` only if every sum is finite.  One
+// flag wait per call instead of entry + reduce-scatter barriers; nobody ever
+// reads a peer's memory, and the parity double buffer makes the receive
+// slots safe to reuse without an entry barrier (a member cannot start call
+// c+2 before every member finished call c+1, hence consumed call c).
+__device__ __forceinline__ uint64_t call_fingerprint(const LaunchParams& p, int n) {
+  uint64_t h = p.nelems * 0x9E3779B97F4A7C15ull;
+  h ^= (p.cap + 0x632BE59BD9B4E019ull) + (h << 6) + (h >> 2);
+  h ^= ((uint64_t)p.dtype | ((uint64_t)n << 8)) + (h << 6) + (h >> 2);
+  h ^= (p.ebase * 31 + p.total) + (h << 6) + (h >> 2);
+  return h;
+}
+
+template <int N, class In>
+__global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __grid_constant__ LaunchParams p) {
+  using T = typename In::T;
+  constexpr int U = Unroll<N, In>::U;
+  const int me = p.emulated ? (int)blockIdx.y : p.self;
+  char* const mybase = p.base[me];
+  ArenaHdr* const hdr = reinterpret_cast<ArenaHdr*>(mybase);
+  HostCtl* const ctl = p.ctl[me];
+  const uint64_t tag = p.tag;
+  const uint64_t E = p.nelems;
+  const uint64_t bytes = E * (uint64_t)In::kBytes;
+  const uint64_t parity = tag & 1ull;
+  const int tid = threadIdx.x;
+  const T* const my_in = reinterpret_cast<const T*>(reinterpret_cast<uint64_t>(mybase) + p.in_off[me]);
+  __shared__ const T* s_src[N];
+  __shared__ uint32_t s_status, s_nf;
+  __shared__ int s_blame;
+  __shared__ uint64_t s_t0;
+  if (tid == 0) {
+    s_status = ST_OK;
+    s_nf = 0;
+    s_blame = -1;
+    s_t0 = globaltimer_ns();
+    if (blockIdx.x == 0) {
+      ctl->started = tag;
+      hdr->tph[0] = s_t0;
+      if (ctl->epoch != tag_gen(tag)) {
+        s_status = ST_PROTOCOL;
+        s_blame = me;
+      }
+    }
+  }
+  __syncthreads();
+  const uint64_t fp = call_fingerprint(p, N);
+  const bool contributes = (p.contrib >> me) & 1u;
+  // 1. push my input to every peer (grid-stride 16-byte copies)
+  if (s_status == ST_OK && contributes && bytes) {
+    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+    const uint64_t first = (uint64_t)blockIdx.x * kThreads + tid;
+    for (int jj = 1; jj < N; ++jj) {
+      const int j = (me + jj) % N;
+      char* dst = p.base[j] + kRecvOff + (parity * 8 + (uint64_t)me) * kSmallMax;
+      copy_bytes_grid(dst, reinterpret_cast<const char*>(my_in), bytes, first, stride);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (gridDim.x > 1) __threadfence();
+    const uint32_t old = gridDim.x > 1 ? atomicAdd(&hdr->rs_arrive, 1u) : 0u;
+    if (old == gridDim.x - 1 && s_status == ST_OK) {
+      fence_acq_rel_sys();  // all my CTAs' posted writes before the flags
+      for (int jj = 1; jj < N; ++jj) {
+        const int j = (me + jj) % N;
+        ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
+        st_relaxed_sys(&ph->sm_meta[me], fp);
+        st_relaxed_sys(&ph->sm_in[me], mk_flag(tag, 0));
+      }
+      hdr->tph[1] = globaltimer_ns();
+    }
+  }
+  // 2. wait for every peer's push (each CTA's thread 0 polls local flags)
+  if (tid == 0 && s_status == ST_OK) {
+    for (int jj = 1; jj < N; ++jj) {
+      const int j = (me + jj) % N;
+      ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
+      uint32_t st = wait_flag(&hdr->sm_in[j], tag, &ph->poison, ctl, &hdr->err, s_t0, p.hard_timeout_ns, nullptr);
+      if (st == ST_OK && ld_relaxed_sys(&hdr->sm_meta[j]) != fp) st = ST_PROTOCOL;
+      if (st != ST_OK) {
+        s_status = st;
+        s_blame = j;
+        break;
+      }
+    }
+    for (int j = 0; j < N; ++j)
+      s_src[j] = j == me ? my_in
+                         : reinterpret_cast<const T*>(mybase + kRecvOff + (parity * 8 + (uint64_t)j) * kSmallMax);
+    if (blockIdx.x == 0) hdr->tph[2] = globaltimer_ns();
+  }
+  __syncthreads();
+  // 3. fold locally (reference order) into out directly (out-of-place calls:
+  // out is undefined after an error) or into the staging region (in place)
+  const bool sdirect = (p.flags & kFlagSmallDirect) != 0;
+  float* const res = sdirect ? p.out[me] : reinterpret_cast<float*>(mybase + p.res_off[me]);
+  uint32_t nf = 0;
+  if (s_status == ST_OK) {
+    uint64_t orbits = reinterpret_cast<uint64_t>(res) | reinterpret_cast<uint64_t>(p.out[me]);
+    for (int j = 0; j < N; ++j) orbits |= reinterpret_cast<uint64_t>(s_src[j]);
+    const bool vec_ok = (orbits & 15u) == 0;
+    LaunchParams g = p;
+    g.rs_layout = 1;
+    g.rs_ctas = 0;
+    fold_tiles<N, In>(g, s_src, SinkOne{res}, 0, E, vec_ok, (p.flags & FTAR_F_SCALE) != 0, nf, ctl, 0x7fffffff);
+  }
+  if (__any_sync(0xffffffffu, nf != 0) && (tid & 31) == 0) atomicOr(&s_nf, 1u);
+  __syncthreads();
+  if (tid == 0 && s_nf) atomicOr(&hdr->nonfinite, 1u);
+  if (tid == 0 && s_status != ST_OK && s_status != ST_FOLLOW) {
+    atomicMax(&hdr->err, severity_code(s_status));
+    hdr->err_peer = s_blame;
+    st_release_sys(&hdr->poison, mk_flag(tag, s_status));
+  }
+  // commit needs every CTA's fold: a grid-wide arrival, then the last CTA copies
+  if (tid == 0) {
+    if (gridDim.x > 1) __threadfence();
+    const uint32_t old = gridDim.x > 1 ? atomicAdd(&hdr->done_arrive, 1u) : 0u;
+    s_blame = (old == gridDim.x - 1) ? 1 : 0;  // reuse as "am last"
+  }
+  __syncthreads();
+  if (s_blame == 1) {
+    if (tid == 0) fence_acq_rel_gpu();
+    __syncthreads();
+    uint32_t err = ld_relaxed_sys32(&hdr->err);
+    if (err == 0 && ld_relaxed_sys32(&hdr->nonfinite)) err = severity_code(ST_NUMERICAL);
+    if (err == 0 && !sdirect) {
+      // copy the staged sums into out (one CTA; small buckets only)
+      const bool vec = ((reinterpret_cast<uint64_t>(res) | reinterpret_cast<uint64_t>(p.out[me])) & 15u) == 0;
+      float* out = p.out[me];
+      if (vec) {
+        const uint64_t nv = E >> 2;
+        for (uint64_t v = tid; v < nv; v += kThreads)
+          *reinterpret_cast<uint4*>(out + v * 4) = *reinterpret_cast<const uint4*>(res + v * 4);
+        for (uint64_t e = (nv << 2) + tid; e < E; e += kThreads) out[e] = res[e];
+      } else {
+        for (uint64_t e = tid; e < E; e += kThreads) out[e] = res[e];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      fence_acq_rel_sys();
+      ctl->detail = err ? (int64_t)hdr->err_peer : -1;
+      ctl->progress = 1;
+      hdr->tph[3] = hdr->tph[2];
+      hdr->tph[4] = globaltimer_ns();
+      for (int i = 0; i < 5; ++i) ctl->tphase[i] = hdr->tph[i];
+      hdr->rs_arrive = 0;
+      hdr->done_arrive = 0;
+      hdr->nonfinite = 0;
+      hdr->err = 0;
+      hdr->err_peer = -1;
+      __threadfence_system();
+      ctl->done = mk_flag(tag, err & 0xffu);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- operators
 template <class In>
 __global__ void __launch_bounds__(256) accumulate_kernel(float* __restrict__ dst,
@@ -845,33 +1037,6 @@ __global__ void snap_mark_kernel(SnapHdr* h, int64_t step, uint64_t pb, uint64_t
     __threadfence_system();
     st_release_sys(&h->seq, h->seq + 1);  // even: stable
   }
-}
-
-// Byte copy of [0, bytes) with 16-byte vectors when aligned.
-__device__ __forceinline__ void copy_bytes_grid(char* dst, const char* src, uint64_t bytes,
-                                                uint64_t first, uint64_t stride) {
-  const bool vec = ((reinterpret_cast<uint64_t>(dst) | reinterpret_cast<uint64_t>(src)) & 15u) == 0;
-  if (!vec) {
-    for (uint64_t i = first; i < bytes; i += stride) dst[i] = src[i];
-    return;
-  }
-  const uint64_t nv = bytes >> 4;
-  constexpr int UA = 8;
-  for (uint64_t v = first; v < nv; v += stride * UA) {
-    uint4 r[UA];
-#pragma unroll
-    for (int u = 0; u < UA; ++u) {
-      const uint64_t i = v + (uint64_t)u * stride;
-      if (i < nv) r[u] = ld_stream(src + i * 16);
-    }
-#pragma unroll
-    for (int u = 0; u < UA; ++u) {
-      const uint64_t i = v + (uint64_t)u * stride;
-      if (i < nv) *reinterpret_cast<uint4*>(dst + i * 16) = r[u];
-    }
-  }
-  const uint64_t t = (nv << 4) + first;
-  if (t < bytes && first < 16) dst[t] = src[t];
 }
 
 __global__ void __launch_bounds__(kThreads) snap_copy_kernel(char* dst, const char* p, uint64_t pb,
@@ -1270,6 +1435,12 @@ int real_ctas(bool push = false) {
   return push ? env_int("FTAR_CTAS_PUSH", 128) : env_int("FTAR_CTAS", 64);
 }
 int rs_ctas_knob() { return env_int("FTAR_RS_CTAS", 0); }
+// buckets up to this many input bytes take the single-barrier push one-shot
+uint64_t small_bytes() {
+  const int v = env_int("FTAR_SMALL_BYTES", 1 << 20);
+  return std::min<uint64_t>(v < 0 ? 0 : (uint64_t)v, kSmallMax);
+}
+int small_ctas(uint64_t bytes) { return (int)std::max<uint64_t>(1, std::min<uint64_t>(16, (bytes + (32u << 10) - 1) >> 15)); }
 int rs_layout() { return env_int("FTAR_RS_LAYOUT", 0); }
 int diag_mode() { return env_int("FTAR_DIAG", 0); }
 
@@ -1375,6 +1546,31 @@ cudaError_t launch_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bool coo
   }
   fn<<<grid, kThreads, 0, st>>>(p);
   return cudaGetLastError();
+}
+
+template <int N, class In>
+cudaError_t launch_small_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop) {
+  auto fn = small_allreduce_kernel<N, In>;
+  if (coop) {
+    void* args[] = {const_cast<LaunchParams*>(&p)};
+    return cudaLaunchCooperativeKernel((const void*)fn, grid, dim3(kThreads), args, 0, st);
+  }
+  fn<<<grid, kThreads, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <class In>
+cudaError_t launch_small(int n, const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop) {
+  switch (n) {
+    case 2: return launch_small_n<2, In>(p, grid, st, coop);
+    case 3: return launch_small_n<3, In>(p, grid, st, coop);
+    case 4: return launch_small_n<4, In>(p, grid, st, coop);
+    case 5: return launch_small_n<5, In>(p, grid, st, coop);
+    case 6: return launch_small_n<6, In>(p, grid, st, coop);
+    case 7: return launch_small_n<7, In>(p, grid, st, coop);
+    case 8: return launch_small_n<8, In>(p, grid, st, coop);
+  }
+  return cudaErrorInvalidValue;
 }
 
 template <class In>
@@ -1493,7 +1689,7 @@ int ftar_ctx_create(int device, uint64_t max_bucket_bytes, uint64_t pool_bytes, 
   c->device = device;
   c->exportable = exportable != 0;
   c->max_bucket_bytes = align_up(std::max<uint64_t>(max_bucket_bytes, 256), 256);
-  c->res_off = kHdrBytes;
+  c->res_off = kRecvOff + kRecvBytes;
   // result region: the fp32 image of a whole bucket (E <= max_bucket_bytes/2
   // for bf16 -> 2x bytes); the protocol kernel uses my slice of it, the
   // in-process one-shot kernel stages the whole fp32 sum in member 0's.
@@ -1706,7 +1902,8 @@ static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, ui
   const char* inp = static_cast<const char*>(in);
   uint64_t in_off;
   const bool registered = inp >= c->arena + c->pool_off && inp + in_bytes <= c->arena + c->arena_bytes;
-  if (registered || c->n == 1) {
+  const bool small = c->n >= 2 && !sgd && in_bytes > 0 && in_bytes <= small_bytes();
+  if (registered || c->n == 1 || small) {  // small buckets: peers never read my input
     in_off = (uint64_t)(inp - c->arena);
   } else {
     // Unregistered bucket: peers can only read the arena, so stage it (double
@@ -1766,12 +1963,20 @@ static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, ui
   int G = real_ctas((p.flags & kFlagPush) != 0);
   {
     const uint64_t slice_bytes = p.slice * (uint64_t)esz;
-    const uint64_t want = (slice_bytes + (256ull << 10) - 1) / (256ull << 10);
+    const uint64_t per = (uint64_t)env_int("FTAR_BYTES_PER_CTA", 64 << 10);
+    const uint64_t want = (slice_bytes + per - 1) / per;
     if (g_ctas <= 0 && want < (uint64_t)G) G = (int)std::max<uint64_t>(1, want);
   }
+  if (small) {
+    if (p.flags & kFlagDirect) p.flags |= kFlagSmallDirect;
+    p.flags &= ~(kFlagPush | kFlagDirect);
+    G = g_ctas > 0 ? g_ctas : small_ctas(in_bytes);
+  }
   const dim3 grid(G, 1);
-  cudaError_t e = in_dtype == FTAR_DT_BF16 ? launch_dispatch<BF16In>(c->n, p, grid, st, false)
-                                            : launch_dispatch<F32In>(c->n, p, grid, st, false);
+  cudaError_t e = small ? (in_dtype == FTAR_DT_BF16 ? launch_small<BF16In>(c->n, p, grid, st, false)
+                                                    : launch_small<F32In>(c->n, p, grid, st, false))
+                        : (in_dtype == FTAR_DT_BF16 ? launch_dispatch<BF16In>(c->n, p, grid, st, false)
+                                                    : launch_dispatch<F32In>(c->n, p, grid, st, false));
   if (e != cudaSuccess) {
     c->pop_last();
     return cuda_fail(e, "allreduce launch");
@@ -1925,6 +2130,21 @@ static int launch_local(ftar_ctx** ctxs, int n, const void* const* ins, int in_d
   int G = std::max(1, (sms * std::max(per_sm, 1)) / n);
   const int want = g_local_ctas > 0 ? g_local_ctas : env_int("FTAR_LOCAL_CTAS", 32);
   G = std::min(G, want);
+  const uint64_t in_bytes_l = n_elems * (in_dtype == FTAR_DT_BF16 ? 2 : 4);
+  const bool small = n >= 2 && !sgd_p && fault_member < 0 && in_bytes_l > 0 && in_bytes_l <= small_bytes();
+  if (small) {
+    if (p.flags & kFlagDirect) p.flags |= kFlagSmallDirect;
+    p.flags &= ~(kFlagPush | kFlagDirect);
+    G = std::min(G, small_ctas(in_bytes_l));
+    const dim3 sgrid(G, n);
+    cudaError_t e = in_dtype == FTAR_DT_BF16 ? launch_small<BF16In>(n, p, sgrid, st, true)
+                                              : launch_small<F32In>(n, p, sgrid, st, true);
+    if (e != cudaSuccess) {
+      for (int i = 0; i < n; ++i) ctxs[i]->pop_last();
+      return cuda_fail(e, "local small-bucket cooperative launch");
+    }
+    return FTAR_OK;
+  }
   const dim3 grid(G, n);
   cudaError_t e = in_dtype == FTAR_DT_BF16 ? launch_dispatch<BF16In>(n, p, grid, st, true)
                                             : launch_dispatch<F32In>(n, p, grid, st, true);

@@ -20,6 +20,11 @@ namespace ftar {
 constexpr int kMaxMembers = 8;
 constexpr int kThreads = 512;          // one CTA per SM (launch_bounds(512,1))
 constexpr uint64_t kHdrBytes = 64 * 1024;
+// small-bucket push one-shot: receive slots right after the header, at the
+// same offset in every member's arena: [parity][sender] x kSmallMax bytes
+constexpr uint64_t kSmallMax = 1ull << 20;
+constexpr uint64_t kRecvOff = kHdrBytes;
+constexpr uint64_t kRecvBytes = 2 * 8 * kSmallMax;
 constexpr uint32_t kBitNonFinite = 1u;
 
 // status codes (mirror include/ftar_b200.h)
@@ -79,6 +84,8 @@ struct alignas(128) ArenaHdr {
   uint64_t peer_out[kMaxMembers];         // push mode: members' `out` element 0 (my VA)
   uint32_t push_ok;                       // push mode agreed for this call
   alignas(128) uint64_t ag_in[kMaxMembers];  // push mode: member k finished writing its slice into my out
+  alignas(128) uint64_t sm_in[kMaxMembers];  // small one-shot: member k's whole input is in my recv slot
+  uint64_t sm_meta[kMaxMembers];             // its call fingerprint (validated like an entry record)
 };
 static_assert(sizeof(ArenaHdr) <= kHdrBytes, "header too large");
 

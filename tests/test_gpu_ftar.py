@@ -60,10 +60,15 @@ def to_dev(a, dtype=torch.float32):
     return torch.from_numpy(np.ascontiguousarray(a)).to(DEV).to(dtype)
 
 
-@pytest.mark.parametrize("mode", ["protocol", "oneshot"])
+@pytest.mark.parametrize("mode", ["protocol", "twoshot", "oneshot"])
 @pytest.mark.parametrize("case", cases(), ids=lambda c: f"{c['idx']}-{c['kind']}-n{c['n']}-e{c['elems']}")
-def test_golden_cases_bit_exact(ftar, rings, case, mode):
-    ring = rings(case["n"], protocol=(mode == "protocol"))
+def test_golden_cases_bit_exact(ftar, rings, case, mode, monkeypatch):
+    """protocol: the multi-GPU kernels (small buckets take the push one-shot);
+    twoshot: the same with the small-bucket path disabled; oneshot: the
+    in-process one-shot kernel."""
+    if mode == "twoshot":
+        monkeypatch.setenv("FTAR_SMALL_BYTES", "0")
+    ring = rings(case["n"], protocol=(mode != "oneshot"))
     cfg = ftar.PipelineConfig(chunk_bytes=case["chunk_bytes"], max_in_flight=case["max_in_flight"],
                               per_chunk_timeout_s=10.0)
     behind = behind_set(case)
