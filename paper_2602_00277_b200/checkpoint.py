@@ -24,6 +24,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import threading
+import time
 
 import torch
 
@@ -65,6 +66,7 @@ class SnapshotStore:
         self._step = None
         self._lens = (0, 0)
         self._peers: dict[tuple[int, int], int] = {}
+        self.map_log: list[tuple] = []
         if capacity_bytes:
             self._alloc(capacity_bytes)
 
@@ -121,6 +123,9 @@ class SnapshotStore:
             return self._lens
 
     def close(self) -> None:
+        t = self.__dict__.get("_connecting")
+        if t is not None:
+            t.join()
         if self._snap is not None:
             _lib.lib.ftar_snap_destroy(self._snap)
             self._snap = None
@@ -132,15 +137,62 @@ class SnapshotStore:
             pass
 
     # --- recovering side --------------------------------------------------------
+    def connect(self, donors, rank: int = 0, timeout_s: float = 5.0, background: bool = False) -> None:
+        """Map the donors' snapshot arenas ahead of the pull.  CUDA IPC mapping
+        of a multi-GB arena costs 0.1-0.5 s per donor; a respawned replica does
+        it while parked, so its first (gated) step is not late to the ring.
+        ``background=True`` maps on a helper thread (the caller keeps taking
+        part in quorum rounds); the next fetch joins it first."""
+        if self._snap is None:
+            raise Fatal(INTERNAL_INVARIANT, "connect needs a snapshot arena (capacity_bytes=)")
+        todo = [int(d) for d in donors if int(d) != self.replica_id]
+        if not background:
+            for d in todo:
+                self._map_donor(d, rank, timeout_s)
+            return
+        self.join_connect()
+        dev = self.device_index
+
+        def run():
+            torch.cuda.set_device(dev)
+            try:
+                for d in todo:
+                    self._map_donor(d, rank, timeout_s)
+            except Exception as exc:  # noqa: BLE001 - surfaced by join_connect
+                self._connect_err = exc
+
+        self._connect_err = None
+        self._connecting = threading.Thread(target=run, name="ftar-snap-connect", daemon=True)
+        self._connecting.start()
+
+    def connecting(self) -> bool:
+        """True while a background connect is still mapping donors."""
+        t = self.__dict__.get("_connecting")
+        return t is not None and t.is_alive()
+
+    def join_connect(self) -> None:
+        """Wait for a background connect; re-raise its failure."""
+        t = self.__dict__.get("_connecting")
+        if t is not None:
+            t.join()
+            self._connecting = None
+            if self._connect_err is not None:
+                err, self._connect_err = self._connect_err, None
+                raise err
+
     def _map_donor(self, donor_replica: int, rank: int, timeout_s: float) -> int:
+        t0 = time.monotonic()
         info = self.fabric.lookup(rank, donor_replica, timeout_s, what="snap")
         key = (donor_replica, info.incarnation)
         if key not in self._peers:
+            t1 = time.monotonic()
             slot = len(self._peers) % 256
             rc = _lib.lib.ftar_snap_import(self._snap, slot, info.handle, len(info.handle), info.arena_bytes)
             if rc:
                 raise Recoverable(PEER_DOWN, f"cannot map snapshot of replica {donor_replica}: {_lib.last_error()}")
             self._peers[key] = slot
+            # (donor, lookup s, IPC open s, bytes): start-up cost accounting
+            self.map_log.append((donor_replica, t1 - t0, time.monotonic() - t1, info.arena_bytes))
         return self._peers[key]
 
 
@@ -197,6 +249,7 @@ def start_fetch(local: SnapshotStore, donor, step: int, rank: int, params_out: t
     the whole catch-up."""
     p, m = _as_bytes_tensor(params_out), _as_bytes_tensor(momentum_out)
     pb, mb = p.numel() * p.element_size(), m.numel() * m.element_size()
+    local.join_connect()
     if local.handle is None:
         local._alloc(max(pb + mb, 16))
     if isinstance(donor, SnapshotStore):

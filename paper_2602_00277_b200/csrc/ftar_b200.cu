@@ -107,9 +107,13 @@ __device__ uint32_t wait_flag(const uint64_t* flag, uint64_t tag, const uint64_t
       if (bits) *bits = (uint32_t)(f & 0xffu);
       return ST_OK;
     }
-    if (ft > tag) return tag_gen(ft) > tag_gen(tag) ? ST_PEER_RESET : ST_PROTOCOL;
+    // A peer's flag can only move past an op I am still waiting in if that
+    // peer abandoned it (it cannot complete without me): a newer generation,
+    // or an abort cascade within this one.  Either way the ring is reset;
+    // mismatched calls are caught by the entry-record check, not here.
+    if (ft > tag) return ST_PEER_RESET;
     if ((it & 15u) == 15u) {
-      if (poison && flag_tag(ld_relaxed_sys(poison)) == tag) return ST_PEER_RESET;
+      if (poison && flag_tag(ld_relaxed_sys(poison)) >= tag) return ST_PEER_RESET;
       if (ctl->abort_tag == tag) return ST_ABORTED;
       if (own_err && ld_relaxed_sys32(own_err) != 0) return ST_FOLLOW;
       if (globaltimer_ns() - t0 > limit_ns) return ST_TIMEOUT;

@@ -333,6 +333,8 @@ class RingGroup:
             raise Fatal(INTERNAL_INVARIANT, "reconfig membership must include self")
         if generation > 0xFFFFFF:
             raise Fatal(INTERNAL_INVARIANT, "generation exceeds the 24-bit epoch word")
+        if self._ctx and not self._local:
+            _drain_pending(self)  # collectives queued under the old membership never complete
         self.close_links()
         self.members = sorted(addrs)
         self.generation = generation
@@ -463,12 +465,30 @@ class PendingAllReduce:
             det = C.c_int(-1)
             head.status = _lib.lib.ftar_wait(self.group.ctx, head.cfg.per_chunk_timeout_s, C.byref(det))
             head.detail, head.done = det.value, True
+            if head.status:
+                # the step is lost: abort and collect everything queued behind
+                # the failed bucket so the host and device queues stay in step
+                _drain_pending(self.group)
         if self.status:
             self.group.close_links()
             blame = self.group.members[self.detail] if 0 <= self.detail < self.group.n else None
             msg = _lib.last_error() if self.status == 10 else ""
             raise from_status(self.status, (msg + f" (peer replica {blame})") if blame is not None else msg)
         return self.result
+
+
+def _drain_pending(group) -> None:
+    """Abort every queued collective of `group` and collect its status (each
+    pending handle keeps its own: ABORTED, or OK if it had already finished)."""
+    q = group.__dict__.get("_pending")
+    if not q:
+        return
+    _lib.lib.ftar_abort(group.ctx)
+    while q:
+        p = q.popleft()
+        det = C.c_int(-1)
+        p.status = _lib.lib.ftar_wait(group.ctx, p.cfg.per_chunk_timeout_s, C.byref(det))
+        p.detail, p.done = det.value, True
 
 
 def ftar_all_reduce_async(group: RingGroup, buf: torch.Tensor, step: int, cfg: PipelineConfig | None = None,

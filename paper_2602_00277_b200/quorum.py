@@ -176,15 +176,24 @@ class StoreQuorum:
     """One membership round over the rendezvous store (multi-process runs).
 
     Every live replica posts ``Report(next_step, incarnation)`` for round
-    ``epoch``; the coordinator replica (lowest live id that posted) runs
-    ``QuorumEngine.decide`` and publishes the Decision; everyone reads it.
-    Replicas that do not post within ``round_deadline_s`` are absent, exactly
-    like the reference coordinator's round deadline (quorum.py:354-396)."""
+    ``round_id``; ONE designated replica (``coordinator``, default the lowest
+    id) plays the reference's coordinator process (quorum.py:213-441): it
+    collects reports until all of the world posted or ``round_deadline_s``
+    after it opened the round, runs ``QuorumEngine.decide`` — the only engine
+    whose incarnation/gate state is authoritative — and publishes the
+    Decision; everyone else reads it.  Replicas that miss the deadline are
+    absent from that round, exactly like the reference's round deadline
+    (quorum.py:354-396).  A single decider matters: a replica that posts
+    early and decides from its own partial view would publish a competing
+    decision for the same round."""
 
-    def __init__(self, store, world: list[int], prefix: str = "ftar/quorum"):
+    def __init__(self, store, world: list[int], prefix: str = "ftar/quorum", coordinator: int | None = None):
         self.store = store
         self.world = sorted(world)
         self.prefix = prefix
+        self.coordinator = self.world[0] if coordinator is None else coordinator
+        if self.coordinator not in self.world:
+            raise ValueError("coordinator must be a member of the world")
         self.engine = QuorumEngine()
 
     def _k(self, *p) -> str:
@@ -194,21 +203,18 @@ class StoreQuorum:
                  decide_timeout_s: float = 30.0) -> Decision:
         self.store.set(self._k(round_id, "report", replica_id),
                        json.dumps([report.next_step, report.incarnation]).encode())
-        t_end = time.monotonic() + round_deadline_s
-        reports: dict[int, Report] = {}
-        while True:
-            for rid in self.world:
-                if rid not in reports and self.store.check([self._k(round_id, "report", rid)]):
-                    ns, inc = json.loads(self.store.get(self._k(round_id, "report", rid)))
-                    reports[rid] = Report(ns, inc)
-            if len(reports) == len(self.world) or time.monotonic() >= t_end:
-                break
-            time.sleep(0.005)
-        # lowest posted id coordinates; the engine state replays identically on
-        # every replica because all replicas feed it the same posted reports
-        coord = min(reports)
         key = self._k(round_id, "decision")
-        if coord == replica_id:
+        if replica_id == self.coordinator:
+            t_end = time.monotonic() + round_deadline_s
+            reports: dict[int, Report] = {}
+            while True:
+                for rid in self.world:
+                    if rid not in reports and self.store.check([self._k(round_id, "report", rid)]):
+                        ns, inc = json.loads(self.store.get(self._k(round_id, "report", rid)))
+                        reports[rid] = Report(ns, inc)
+                if len(reports) == len(self.world) or time.monotonic() >= t_end:
+                    break
+                time.sleep(0.002)
             d = self.engine.decide(reports)
             self.store.set(key, json.dumps(d.to_json()).encode())
             return d
@@ -217,7 +223,47 @@ class StoreQuorum:
         except Exception as exc:  # noqa: BLE001
             raise Recoverable(PEER_DOWN, f"no decision for round {round_id}: {exc}")
         d = Decision.from_json(json.loads(self.store.get(key)))
+        self._follow(d)
+        return d
+
+    def _follow(self, d: Decision) -> None:
         # keep the local engine in lock-step for a future coordinator role
         self.engine.epoch, self.engine.target_step, self.engine.generation = d.epoch, d.target_step, d.generation
         self.engine._prev_roles = (d.healthy, tuple(sorted(d.behind)))
+
+    def follow(self, round_id: int, timeout_s: float = 60.0) -> Decision:
+        """Read round `round_id`'s decision without reporting (a replica that
+        is out of the group but keeps its round counter in step)."""
+        key = self._k(round_id, "decision")
+        self.store.wait([key], timedelta(seconds=timeout_s))
+        d = Decision.from_json(json.loads(self.store.get(key)))
+        self._follow(d)
         return d
+
+    def vote(self, round_id: int, decision: Decision, replica_id: int, ok: bool,
+             deadline_s: float = 2.0) -> bool:
+        """The commit round (the reference's 2PC, replica.py:589-603): every
+        member of the decision votes; the step commits iff all voted ok before
+        the deadline.  One member — the lowest id of the decision — collects
+        the votes and publishes the outcome that everyone applies, so a vote
+        arriving at the deadline cannot commit on one replica and abort on
+        another."""
+        self.store.set(self._k(round_id, "vote", replica_id), b"1" if ok else b"0")
+        out_key = self._k(round_id, "outcome")
+        members = decision.members
+        if not members:
+            return False
+        if replica_id == members[0]:
+            keys = [self._k(round_id, "vote", m) for m in members]
+            try:
+                self.store.wait(keys, timedelta(seconds=deadline_s))
+                commit = all(self.store.get(k) == b"1" for k in keys)
+            except Exception:  # noqa: BLE001 - a member never voted: abort the step
+                commit = False
+            self.store.set(out_key, b"commit" if commit else b"abort")
+            return commit
+        try:
+            self.store.wait([out_key], timedelta(seconds=deadline_s + 30.0))
+        except Exception:  # noqa: BLE001 - the decider is gone: nothing was committed
+            return False
+        return self.store.get(out_key) == b"commit"

@@ -193,6 +193,43 @@ def _worker(rank, world, port, scenario, outdir):
             ftar.ftar_all_reduce(group, b, 9, cfg, out=o)
             (res["ok"] if torch.all(o == float(len(survivors))).item() else res["errors"]).append("regrouped")
             store.set(f"fin{victim}", b"1")  # the victim cannot
+        elif scenario == "async_failure":
+            # a member skips a step while the others have 4 buckets queued:
+            # every handle resolves Recoverable, the host and device queues end
+            # empty, and after the regroup a fresh queue of buckets is bit-exact
+            # (a stale handle left behind would collect a later op's status)
+            import time
+
+            from paper_2602_00277_b200 import _lib
+            victim = world - 1
+            group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, 1, deadline_s=30)
+            cfg = ftar.PipelineConfig(per_chunk_timeout_s=1.0)
+            e = 300_007
+            bks = [member_inputs(world, e, seed=200 + b) for b in range(6)]
+            bufs = [torch.from_numpy(bk[rank]).to(dev) for bk in bks]
+            outs = [torch.empty_like(b) for b in bufs]
+            if rank != victim:
+                pend = [ftar.ftar_all_reduce_async(group, bufs[i], 1, cfg, out=outs[i]) for i in range(4)]
+                failed = 0
+                for p in pend:
+                    try:
+                        p.wait()
+                    except errors.Recoverable:
+                        failed += 1
+                (res["ok"] if failed == 4 else res["errors"]).append(f"all_failed:{failed}")
+                left = _lib.lib.ftar_inflight(group.ctx)
+                (res["ok"] if not group._pending and left == 0 else res["errors"]).append("queues_empty")
+                store.set(f"af_failed{rank}", b"1")
+            else:
+                store.wait([f"af_failed{r}" for r in range(world - 1)])
+                time.sleep(0.1)
+            group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, 2, deadline_s=30)
+            pend = [ftar.ftar_all_reduce_async(group, b, 2, cfg, out=o, scale=0.5) for b, o in zip(bufs, outs)]
+            for p in pend:
+                p.wait()
+            good = all(np.array_equal(o.cpu().numpy(), orc.oracle_reduce(bk, 8 << 20, 4) * np.float32(0.5))
+                       for bk, o in zip(bks, outs))
+            (res["ok"] if good else res["errors"]).append("regrouped_queue")
         elif scenario == "catchup":
             from paper_2602_00277_b200 import checkpoint as ck
             snap = ck.SnapshotStore(capacity_bytes=64 << 20, device=dev, fabric=fabric, rank=0, replica_id=rank)
@@ -211,7 +248,9 @@ def _worker(rank, world, port, scenario, outdir):
                 wp = torch.randn(8 << 20 >> 2, device=dev, generator=g0)
                 wm = torch.randn(8 << 20 >> 2, device=dev, generator=g0)
                 po, mo = torch.empty_like(p), torch.empty_like(m)
+                snap.connect(donors, 0, timeout_s=10, background=True)  # the fetch joins it
                 ck.fetch_shard(0, 5, 0, local=snap, out=(po, mo), timeout_s=10)
+                (res["ok"] if not snap.connecting() else res["errors"]).append("connected")
                 (res["ok"] if torch.equal(po, wp) and torch.equal(mo, wm) else res["errors"]).append("pull")
                 po.zero_()
                 mo.zero_()
@@ -291,12 +330,22 @@ def test_member_process_death_is_recoverable():
         assert "recoverable" in r["ok"] and "regrouped" in r["ok"]
 
 
+def test_failed_async_queue_is_drained():
+    world = world_size()
+    res = run("async_failure", world)
+    for r in res:
+        assert not r["errors"], r["errors"]
+        assert "regrouped_queue" in r["ok"]
+    for r in res[:-1]:
+        assert "all_failed:4" in r["ok"] and "queues_empty" in r["ok"]
+
+
 def test_catchup_pull_over_nvlink():
     world = world_size()
     res = run("catchup", world)
     rec = res[world - 1]
     assert not rec["errors"], rec["errors"]
-    assert {"pull", "striped", "unavailable"} <= set(rec["ok"])
+    assert {"connected", "pull", "striped", "unavailable"} <= set(rec["ok"])
 
 
 def _async_worker(rank, world, port, outdir):

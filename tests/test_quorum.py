@@ -114,3 +114,80 @@ def test_kill_trace_shape():
     assert rows[3] == (4, 3, 2, wo5, {})
     assert rows[6] == (7, 6, 3, wo5, {5: 1})
     assert rows[7] == (8, 7, 4, allm, {})
+
+
+# --- StoreQuorum over a real TCPStore (threads stand in for replicas) -------
+
+
+def _stores(n):
+    from datetime import timedelta
+
+    import torch.distributed as dist
+    master = dist.TCPStore("127.0.0.1", 0, is_master=True, wait_for_workers=False,
+                           timeout=timedelta(seconds=30))
+    clients = [dist.TCPStore("127.0.0.1", master.port, is_master=False, timeout=timedelta(seconds=30))
+               for _ in range(n)]
+    return master, clients
+
+
+def _run_threads(fns):
+    import threading
+    out, errs = [None] * len(fns), []
+
+    def wrap(i, f):
+        try:
+            out[i] = f()
+        except Exception as exc:  # noqa: BLE001
+            errs.append(exc)
+
+    ts = [threading.Thread(target=wrap, args=(i, f)) for i, f in enumerate(fns)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(60)
+    assert not errs, errs
+    return out
+
+
+def test_store_quorum_early_poster_does_not_decide():
+    """A replica that opens the round before the others (e.g. a parked
+    rejoiner looping fast) must read the coordinator's decision, not publish
+    one from its own partial view."""
+    import time
+
+    from paper_2602_00277_b200.quorum import StoreQuorum
+    master, cl = _stores(3)
+    qs = [StoreQuorum(cl[i], [0, 1, 2], prefix="tq") for i in range(3)]
+
+    def rep(i, delay):
+        def f():
+            time.sleep(delay)
+            return qs[i].exchange(1, i, Report(5, 0), round_deadline_s=1.0)
+        return f
+
+    ds = _run_threads([rep(0, 0.3), rep(1, 0.35), rep(2, 0.0)])
+    assert all(d == ds[0] for d in ds)
+    assert ds[0].healthy == (0, 1, 2) and ds[0].target_step == 5
+    # the follower path reads the same decision
+    assert qs[2].follow(1, timeout_s=5) == ds[0]
+
+
+def test_store_quorum_vote_outcome_is_shared():
+    import time
+
+    from paper_2602_00277_b200.quorum import StoreQuorum
+    master, cl = _stores(3)
+    qs = [StoreQuorum(cl[i], [0, 1, 2], prefix="tv") for i in range(3)]
+    d = Decision(1, 5, 1, (0, 1, 2), {})
+
+    def voter(i, rnd, ok, delay):
+        def f():
+            time.sleep(delay)
+            return qs[i].vote(rnd, d, i, ok, deadline_s=0.5)
+        return f
+
+    assert _run_threads([voter(i, 1, True, 0.0) for i in range(3)]) == [True] * 3
+    assert _run_threads([voter(0, 2, True, 0), voter(1, 2, False, 0), voter(2, 2, True, 0)]) == [False] * 3
+    # a vote that lands after the decider's deadline aborts the step everywhere,
+    # including on the late voter itself
+    assert _run_threads([voter(0, 3, True, 0), voter(1, 3, True, 0), voter(2, 3, True, 0.8)]) == [False] * 3
