@@ -93,6 +93,15 @@ __device__ __forceinline__ uint32_t severity_code(uint32_t st) {
 // flag (I am stale -> PEER_RESET), a newer call of the same generation
 // (sequence skew -> PROTOCOL), the host abort word, another CTA of mine
 // failing (FOLLOW), or the device hard timeout.
+// What a member believes the call is (validated against every peer's).
+__device__ __forceinline__ uint64_t call_fingerprint(const LaunchParams& p, int n) {
+  uint64_t h = p.nelems * 0x9E3779B97F4A7C15ull;
+  h ^= (p.cap + 0x632BE59BD9B4E019ull) + (h << 6) + (h >> 2);
+  h ^= ((uint64_t)p.dtype | ((uint64_t)n << 8)) + (h << 6) + (h >> 2);
+  h ^= (p.ebase * 31 + p.total) + (h << 6) + (h >> 2);
+  return h;
+}
+
 __device__ uint32_t wait_flag(const uint64_t* flag, uint64_t tag, const uint64_t* poison,
                               const HostCtl* ctl, const uint32_t* own_err, uint64_t t0,
                               uint64_t limit_ns, uint32_t* bits) {
@@ -113,10 +122,14 @@ __device__ uint32_t wait_flag(const uint64_t* flag, uint64_t tag, const uint64_t
     // mismatched calls are caught by the entry-record check, not here.
     if (ft > tag) return ST_PEER_RESET;
     if ((it & 15u) == 15u) {
-      if (poison && flag_tag(ld_relaxed_sys(poison)) >= tag) return ST_PEER_RESET;
-      if (ctl->abort_tag == tag) return ST_ABORTED;
       if (own_err && ld_relaxed_sys32(own_err) != 0) return ST_FOLLOW;
       if (globaltimer_ns() - t0 > limit_ns) return ST_TIMEOUT;
+      // the slow checks (a remote load, a PCIe read of the host's abort word:
+      // ~1.5 us each) run 4x less often so they rarely delay a flag's arrival
+      if ((it & 63u) == 63u) {
+        if (poison && flag_tag(ld_relaxed_sys(poison)) >= tag) return ST_PEER_RESET;
+        if (ctl->abort_tag == tag) return ST_ABORTED;
+      }
     }
     if (it > 4) __nanosleep(it < 64 ? 64 : 256);
   }
@@ -536,103 +549,148 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
   __shared__ int s_vec_ok;
   __shared__ uint64_t s_t0;
 
+  __shared__ uint64_t s_pin[N], s_pres[N], s_pout[N];  // CTA 0: entry results, staged for the fan-out
+  __shared__ uint32_t s_pushok;
+
   if (tid == 0) {
     s_status = ST_OK;
     s_blame = -1;
     s_nf = 0;
     s_push = 0;
     s_t0 = globaltimer_ns();
-    if (blockIdx.x == 0) {
+  }
+  if (blockIdx.x == 0 && tid < 32) {
+    // ---- 1a. entry (may overlap the previous call's tail: PDL) ------------
+    // Until griddepcontrol.wait below this touches only this call's control
+    // slot, slot `me` of the peers' ent_in[] and my own ent_in[] (no earlier
+    // call reads those any more) - never the rest of my header, which the
+    // previous kernel on this stream may still be resetting.
+    __syncwarp();
+    if (tid == 0) {
+      if (N > 1) {
+        // push my entry record into slot `me` of every peer's header: posted
+        // writes, ONE sys fence, then the flags (the peers poll locally)
+        const uint64_t fp = call_fingerprint(p, N);
+        const uint64_t oo = (p.flags & kFlagPush) ? p.out_off[me] : ~0ull;
+        const uint64_t sum = entry_sum(tag, fp, p.in_off[me], p.res_off[me], oo);
+        for (int jj = 1; jj < N; ++jj) {
+          EntryIn* e = &reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->ent_in[me];
+          st_relaxed_sys(&e->fp, fp);
+          st_relaxed_sys(&e->in_off, p.in_off[me]);
+          st_relaxed_sys(&e->res_off, p.res_off[me]);
+          st_relaxed_sys(&e->out_off, oo);
+          st_relaxed_sys(&e->sum, sum);
+        }
+        fence_acq_rel_sys();
+        for (int jj = 1; jj < N; ++jj)
+          st_relaxed_sys(&reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->ent_in[me].flag, mk_flag(tag, 0));
+      }
       // Epoch fence: an op queued under an older decision must not run
-      // against the membership the control plane has since installed.
+      // against the membership the control plane has since installed.  (A
+      // PCIe read, so it runs while the entry flags travel; a stale op that
+      // already published is harmless: its tag matches no current peer call,
+      // and it poisons itself below.)
       if (ctl->epoch != tag_gen(tag)) {
         s_status = ST_PROTOCOL;
         s_blame = me;
       }
       ctl->started = tag;
-      hdr->tph[0] = s_t0;
-      if (s_status == ST_OK) {
-        EntryRec* en = &hdr->entry;
-        en->in_off = p.in_off[me];
-        en->res_off = p.res_off[me];
-        en->nelems = E;
-        en->geom = p.cap;
-        en->dtype = p.dtype;
-        en->n = (uint32_t)N;
-        en->ebase = p.ebase;
-        en->total = p.total;
-        en->out_off = (p.flags & kFlagPush) ? p.out_off[me] : ~0ull;
-        __threadfence_system();
-        st_release_sys(&en->flag, mk_flag(tag, 0));
+    }
+    __syncwarp();
+    // lane j waits for member j's record and validates it (all peers at once)
+    const int j = tid;
+    uint32_t st = ST_OK;
+    uint64_t oo = 0;
+    if (s_status == ST_OK && j < N) {
+      if (j == me) {
+        s_pin[j] = reinterpret_cast<uint64_t>(mybase) + p.in_off[me];
+        s_pres[j] = reinterpret_cast<uint64_t>(mybase) + p.res_off[me];
+        s_pout[j] = reinterpret_cast<uint64_t>(p.out[me]);
+      } else {
+        const uint64_t want_fp = call_fingerprint(p, N);
+        ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
+        EntryIn* e = &hdr->ent_in[j];  // local: member j pushed it here
+        // own_err = null: hdr->err still belongs to the previous call here
+        st = wait_flag(&e->flag, tag, &ph->poison, ctl, nullptr, s_t0, p.hard_timeout_ns, nullptr);
+        if (st == ST_OK) {
+          const uint64_t fp = ld_relaxed_sys(&e->fp), in_off = ld_relaxed_sys(&e->in_off);
+          const uint64_t res_off = ld_relaxed_sys(&e->res_off);
+          oo = ld_relaxed_sys(&e->out_off);
+          const uint64_t sum = ld_relaxed_sys(&e->sum);
+          if (fp != want_fp) st = ST_PROTOCOL;  // a different call
+          else if (sum != entry_sum(tag, fp, in_off, res_off, oo)) st = ST_PEER_RESET;
+          s_pin[j] = reinterpret_cast<uint64_t>(p.base[j]) + in_off;
+          s_pres[j] = reinterpret_cast<uint64_t>(p.base[j]) + res_off;
+          s_pout[j] = reinterpret_cast<uint64_t>(p.base[j]) + oo;
+        }
       }
     }
+    const uint32_t bad = __ballot_sync(0xffffffffu, st != ST_OK);
+    // push mode only if every member accepts pushes
+    const uint32_t nopush = __ballot_sync(0xffffffffu, j < N && j != me && oo == ~0ull);
+    const uint32_t st_first = __shfl_sync(0xffffffffu, st, bad ? __ffs(bad) - 1 : 0);
+    if (tid == 0) {
+      if (bad) {
+        s_status = st_first;
+        s_blame = __ffs(bad) - 1;
+      }
+      s_pushok = ((p.flags & kFlagPush) && !nopush) ? 1u : 0u;
+    }
   }
+  // The previous kernel on this stream (if it let us start early) has now
+  // completed and its writes are visible; a no-op for ordinary launches.
+  pdl_wait();
   __syncthreads();
 
-  // ---- 1. entry barrier (CTA 0 polls the members, then fans out) ---------
-  if (tid == 0 && s_status == ST_OK) {
-    if (blockIdx.x == 0) {
-      int ok = 1;
-      uint32_t push_ok = (p.flags & kFlagPush) ? 1u : 0u;
-      for (int j = 0; j < N; ++j) {
-        if (j == me) {
-          hdr->peer_in[j] = reinterpret_cast<uint64_t>(mybase) + p.in_off[me];
-          hdr->peer_res[j] = reinterpret_cast<uint64_t>(mybase) + p.res_off[me];
-          hdr->peer_out[j] = reinterpret_cast<uint64_t>(p.out[me]);
-          continue;
+  // ---- 1b. fan the entry result out to my CTAs ----------------------------
+  if (blockIdx.x == 0) {
+    if (tid == 0) {
+      hdr->tph[0] = s_t0;
+      if (s_status == ST_OK) {
+        for (int k = 0; k < N; ++k) {
+          hdr->peer_in[k] = s_pin[k];
+          hdr->peer_res[k] = s_pres[k];
+          hdr->peer_out[k] = s_pout[k];
         }
-        ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
-        uint32_t st = wait_flag(&ph->entry.flag, tag, &ph->poison, ctl, &hdr->err, s_t0,
-                                p.hard_timeout_ns, nullptr);
-        uint64_t in_off = 0, res_off = 0;
-        if (st == ST_OK) {
-          in_off = ld_relaxed_sys(&ph->entry.in_off);
-          res_off = ld_relaxed_sys(&ph->entry.res_off);
-          const uint64_t ne = ld_relaxed_sys(&ph->entry.nelems);
-          const uint64_t ge = ld_relaxed_sys(&ph->entry.geom);
-          const uint64_t dn = ld_relaxed_sys(reinterpret_cast<const uint64_t*>(&ph->entry.dtype));
-          const uint64_t want_dn = (uint64_t)p.dtype | ((uint64_t)N << 32);
-          const uint64_t eb = ld_relaxed_sys(&ph->entry.ebase), et = ld_relaxed_sys(&ph->entry.total);
-          if (ne != E || ge != p.cap || dn != want_dn || eb != p.ebase || et != p.total) st = ST_PROTOCOL;
-        }
-        if (st != ST_OK) {
-          s_status = st;
-          s_blame = j;
-          ok = 0;
-          break;
-        }
-        hdr->peer_in[j] = reinterpret_cast<uint64_t>(p.base[j]) + in_off;
-        hdr->peer_res[j] = reinterpret_cast<uint64_t>(p.base[j]) + res_off;
-        const uint64_t oo = ld_relaxed_sys(&ph->entry.out_off);
-        if (oo == ~0ull) push_ok = 0;  // every member must accept pushes, or nobody pushes
-        hdr->peer_out[j] = reinterpret_cast<uint64_t>(p.base[j]) + oo;
-      }
-      hdr->push_ok = push_ok;
-      if (ok) {
+        const uint32_t push_ok = s_pushok;
+        hdr->push_ok = push_ok;
         uint64_t orbits = reinterpret_cast<uint64_t>(p.out[me]);
-        for (int j = 0; j < N; ++j) orbits |= hdr->peer_in[j] | hdr->peer_res[j];
+        for (int k = 0; k < N; ++k) orbits |= s_pin[k] | s_pres[k];
         if (push_ok)
-          for (int j = 0; j < N; ++j) orbits |= hdr->peer_out[j];
+          for (int k = 0; k < N; ++k) orbits |= s_pout[k];
         if (p.flags & kFlagSGD)
           orbits |= reinterpret_cast<uint64_t>(p.sgd_p[me]) | reinterpret_cast<uint64_t>(p.sgd_m[me]) |
                     reinterpret_cast<uint64_t>(p.sgd_po[me]) | reinterpret_cast<uint64_t>(p.sgd_mo[me]);
-        hdr->vec_ok = (orbits & 15u) == 0;
+        const uint32_t vec_ok = (orbits & 15u) == 0;
+        hdr->vec_ok = vec_ok;
         st_release_gpu(&hdr->go, mk_flag(tag, 1));
+        s_vec_ok = (int)vec_ok;
+        s_push = direct && N > 1 && push_ok != 0;
       }
       hdr->tph[1] = globaltimer_ns();
       hdr->dbg_t1 = hdr->tph[1];
-    } else {
+    }
+    __syncthreads();
+    if (s_status == ST_OK && tid < N) {
+      s_src[tid] = reinterpret_cast<const T*>(s_pin[tid]);
+      s_res[tid] = reinterpret_cast<const float*>(s_pres[tid]);
+      s_out[tid] = reinterpret_cast<float*>(s_pout[tid]);
+    }
+  } else {
+    if (tid == 0 && s_status == ST_OK) {
       const uint32_t st = wait_go(hdr, mk_flag(tag, 1), s_t0, p.hard_timeout_ns);
       if (st != ST_OK) s_status = st;
     }
+    __syncthreads();
+    // one L2 round trip: the 3N+1 words are read by different threads
     if (s_status == ST_OK) {
-      for (int j = 0; j < N; ++j) {
-        s_src[j] = reinterpret_cast<const T*>(ld_relaxed_gpu(&hdr->peer_in[j]));
-        s_res[j] = reinterpret_cast<const float*>(ld_relaxed_gpu(&hdr->peer_res[j]));
-        s_out[j] = reinterpret_cast<float*>(ld_relaxed_gpu(&hdr->peer_out[j]));
+      if (tid < N) s_src[tid] = reinterpret_cast<const T*>(ld_relaxed_gpu(&hdr->peer_in[tid]));
+      else if (tid < 2 * N) s_res[tid - N] = reinterpret_cast<const float*>(ld_relaxed_gpu(&hdr->peer_res[tid - N]));
+      else if (tid < 3 * N) s_out[tid - 2 * N] = reinterpret_cast<float*>(ld_relaxed_gpu(&hdr->peer_out[tid - 2 * N]));
+      else if (tid == 3 * N) {
+        s_vec_ok = (int)ld_relaxed_sys32(&hdr->vec_ok);
+        s_push = direct && N > 1 && ld_relaxed_sys32(&hdr->push_ok) != 0;
       }
-      s_vec_ok = (int)ld_relaxed_sys32(&hdr->vec_ok);
-      s_push = direct && N > 1 && ld_relaxed_sys32(&hdr->push_ok) != 0;
     }
   }
   __syncthreads();
@@ -817,6 +875,10 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
 
   // ---- 5. completion -----------------------------------------------------
   if (tid == 0) {
+    // this CTA is done with every data buffer of the call (push mode: CTA 0
+    // only gets here once all peers' slices are in my out), so the next call
+    // on the stream may start its entry while the tail below drains
+    pdl_trigger();
     const uint32_t st = s_status;
     if (st != ST_OK && st != ST_FOLLOW) {
       atomicMax(&hdr->err, severity_code(st));
@@ -826,12 +888,17 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
     if (gridDim.x > 1) __threadfence();
     const uint32_t old = gridDim.x > 1 ? atomicAdd(&hdr->done_arrive, 1u) : 0u;
     if (old == gridDim.x - 1) {
+      // Only my own CTAs write err/nonfinite/tiles: a gpu-scope acquire through
+      // the arrival counter suffices.  Nothing published here is read by a
+      // peer, and the outputs reach stream-ordered consumers at kernel
+      // completion, so the success path needs no sys fence (~1.5 us each);
+      // `detail` is only read after a failed `done`, so only errors fence it.
       hdr->dbg_fence[2] = globaltimer_ns();
-      fence_acq_rel_sys();
+      fence_acq_rel_gpu();
       hdr->dbg_fence[3] = globaltimer_ns();
-      const uint32_t err = ld_relaxed_sys32(&hdr->err);
+      const uint32_t err = ld_relaxed_gpu32(&hdr->err);
       const uint64_t tiles = hdr->tiles_done;
-      ctl->detail = err ? (int64_t)hdr->err_peer : -1;
+      const int64_t blame = hdr->err_peer;
       ctl->progress = tiles + 1;
       hdr->tph[4] = globaltimer_ns();
       for (int i = 0; i < 5; ++i) ctl->tphase[i] = hdr->tph[i];
@@ -841,7 +908,10 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
       hdr->err = 0;
       hdr->err_peer = -1;
       hdr->tiles_done = 0;
-      __threadfence_system();
+      if (err) {
+        ctl->detail = blame;
+        __threadfence_system();
+      }
       ctl->done = mk_flag(tag, err & 0xffu);
     }
   }
@@ -858,13 +928,6 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
 // reads a peer's memory, and the parity double buffer makes the receive
 // slots safe to reuse without an entry barrier (a member cannot start call
 // c+2 before every member finished call c+1, hence consumed call c).
-__device__ __forceinline__ uint64_t call_fingerprint(const LaunchParams& p, int n) {
-  uint64_t h = p.nelems * 0x9E3779B97F4A7C15ull;
-  h ^= (p.cap + 0x632BE59BD9B4E019ull) + (h << 6) + (h >> 2);
-  h ^= ((uint64_t)p.dtype | ((uint64_t)n << 8)) + (h << 6) + (h >> 2);
-  h ^= (p.ebase * 31 + p.total) + (h << 6) + (h >> 2);
-  return h;
-}
 
 template <int N, class In>
 __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __grid_constant__ LaunchParams p) {
@@ -977,8 +1040,8 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
   if (s_blame == 1) {
     if (tid == 0) fence_acq_rel_gpu();
     __syncthreads();
-    uint32_t err = ld_relaxed_sys32(&hdr->err);
-    if (err == 0 && ld_relaxed_sys32(&hdr->nonfinite)) err = severity_code(ST_NUMERICAL);
+    uint32_t err = ld_relaxed_gpu32(&hdr->err);
+    if (err == 0 && ld_relaxed_gpu32(&hdr->nonfinite)) err = severity_code(ST_NUMERICAL);
     if (err == 0 && !sdirect) {
       // copy the staged sums into out (one CTA; small buckets only)
       const bool vec = ((reinterpret_cast<uint64_t>(res) | reinterpret_cast<uint64_t>(p.out[me])) & 15u) == 0;
@@ -994,8 +1057,8 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
     }
     __syncthreads();
     if (tid == 0) {
-      fence_acq_rel_sys();
-      ctl->detail = err ? (int64_t)hdr->err_peer : -1;
+      // as in allreduce_kernel: no sys fence on the success path
+      const int64_t blame = hdr->err_peer;
       ctl->progress = 1;
       hdr->tph[3] = hdr->tph[2];
       hdr->tph[4] = globaltimer_ns();
@@ -1005,7 +1068,10 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
       hdr->nonfinite = 0;
       hdr->err = 0;
       hdr->err_peer = -1;
-      __threadfence_system();
+      if (err) {
+        ctl->detail = blame;
+        __threadfence_system();
+      }
       ctl->done = mk_flag(tag, err & 0xffu);
     }
   }
@@ -1444,6 +1510,8 @@ uint64_t small_bytes() {
   const int v = env_int("FTAR_SMALL_BYTES", 1 << 20);
   return std::min<uint64_t>(v < 0 ? 0 : (uint64_t)v, kSmallMax);
 }
+// programmatic dependent launch of the two-shot kernel (FTAR_PDL=0 disables)
+bool pdl_on() { return env_int("FTAR_PDL", 1) != 0; }
 int small_ctas(uint64_t bytes) { return (int)std::max<uint64_t>(1, std::min<uint64_t>(16, (bytes + (32u << 10) - 1) >> 15)); }
 int rs_layout() { return env_int("FTAR_RS_LAYOUT", 0); }
 int diag_mode() { return env_int("FTAR_DIAG", 0); }
@@ -1542,11 +1610,26 @@ struct ftar_snap {
 namespace {
 
 template <int N, class In>
-cudaError_t launch_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop) {
+cudaError_t launch_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop, bool pdl) {
   auto fn = allreduce_kernel<N, In>;
   if (coop) {
     void* args[] = {const_cast<LaunchParams*>(&p)};
     return cudaLaunchCooperativeKernel((const void*)fn, grid, dim3(kThreads), args, 0, st);
+  }
+  if (pdl) {
+    // programmatic dependent launch: when the previous kernel on the stream
+    // is one of ours, this call's entry overlaps that kernel's tail
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, p);
   }
   fn<<<grid, kThreads, 0, st>>>(p);
   return cudaGetLastError();
@@ -1578,16 +1661,16 @@ cudaError_t launch_small(int n, const LaunchParams& p, dim3 grid, cudaStream_t s
 }
 
 template <class In>
-cudaError_t launch_dispatch(int n, const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop) {
+cudaError_t launch_dispatch(int n, const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop, bool pdl = false) {
   switch (n) {
-    case 1: return launch_n<1, In>(p, grid, st, coop);
-    case 2: return launch_n<2, In>(p, grid, st, coop);
-    case 3: return launch_n<3, In>(p, grid, st, coop);
-    case 4: return launch_n<4, In>(p, grid, st, coop);
-    case 5: return launch_n<5, In>(p, grid, st, coop);
-    case 6: return launch_n<6, In>(p, grid, st, coop);
-    case 7: return launch_n<7, In>(p, grid, st, coop);
-    case 8: return launch_n<8, In>(p, grid, st, coop);
+    case 1: return launch_n<1, In>(p, grid, st, coop, pdl);
+    case 2: return launch_n<2, In>(p, grid, st, coop, pdl);
+    case 3: return launch_n<3, In>(p, grid, st, coop, pdl);
+    case 4: return launch_n<4, In>(p, grid, st, coop, pdl);
+    case 5: return launch_n<5, In>(p, grid, st, coop, pdl);
+    case 6: return launch_n<6, In>(p, grid, st, coop, pdl);
+    case 7: return launch_n<7, In>(p, grid, st, coop, pdl);
+    case 8: return launch_n<8, In>(p, grid, st, coop, pdl);
   }
   return cudaErrorInvalidValue;
 }
@@ -1979,8 +2062,8 @@ static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, ui
   const dim3 grid(G, 1);
   cudaError_t e = small ? (in_dtype == FTAR_DT_BF16 ? launch_small<BF16In>(c->n, p, grid, st, false)
                                                     : launch_small<F32In>(c->n, p, grid, st, false))
-                        : (in_dtype == FTAR_DT_BF16 ? launch_dispatch<BF16In>(c->n, p, grid, st, false)
-                                                    : launch_dispatch<F32In>(c->n, p, grid, st, false));
+                        : (in_dtype == FTAR_DT_BF16 ? launch_dispatch<BF16In>(c->n, p, grid, st, false, pdl_on())
+                                                    : launch_dispatch<F32In>(c->n, p, grid, st, false, pdl_on()));
   if (e != cudaSuccess) {
     c->pop_last();
     return cuda_fail(e, "allreduce launch");
@@ -2220,7 +2303,8 @@ int ftar_wait(ftar_ctx* c, double progress_timeout_s, int* detail) {
     if (flag_tag(d) == tag) {
       c->q_head = (c->q_head + 1) % kQueue;
       --c->q_count;
-      if (detail) *detail = (int)h->detail;
+      // the device writes `detail` (then fences) only for a failed call
+      if (detail) *detail = (d & 0xff) ? (int)h->detail : -1;
       return (int)(d & 0xff);
     }
     const double t = now_s();
@@ -2281,7 +2365,7 @@ int ftar_wait_local(ftar_ctx** ctxs, int n, double progress_timeout_s, int* stat
         c->q_head = (c->q_head + 1) % kQueue;
         --c->q_count;
         statuses[i] = (int)(d & 0xff);
-        if (details) details[i] = (int)h->detail;
+        if (details) details[i] = (d & 0xff) ? (int)h->detail : -1;
         continue;
       }
       ++left;

@@ -7,9 +7,12 @@
 // satisfies a wait when its (generation, seq) equals the waiter's, so a
 // straggler from an abandoned attempt (older generation) can never complete a
 // newer wait — the GPU analogue of the generation fencing at
-// ftar.py:281-282 / 390-393.  All writes a peer can observe are LOCAL to the
-// writer (peers pull), so a zombie kernel of a dead attempt cannot corrupt
-// anybody else's memory.
+// ftar.py:281-282 / 390-393.  Bulk data moves by peer PULLS, except in push
+// mode (out-of-place calls into registered buffers, whose `out` is undefined
+// after an error anyway).  Small control records (entry records, arrival
+// flags) are pushed into the reader's header so every poll is local; each is
+// bound to its call's tag (entry_sum), so a zombie of a dead attempt can delay
+// a reader but never redirect it.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -43,24 +46,34 @@ __host__ __device__ inline uint64_t mk_flag(uint64_t tag, uint32_t bits) {
 __host__ __device__ inline uint64_t flag_tag(uint64_t f) { return f >> 8; }
 __host__ __device__ inline uint64_t tag_gen(uint64_t t) { return t >> 32; }
 
-// What a member announces when it enters a call: where its input sits in its
-// arena and what it believes the call is.  Peers validate it (the analogue of
-// the (partition, ring_step, chunk, len) check at ftar.py:394-397).
-struct alignas(128) EntryRec {
+// What member j announces when it enters a call, PUSHED into slot j of every
+// peer's header (posted NVLink writes, one fence, then the flag), so each
+// member polls and reads only its own memory: pulling the record cost one
+// dependent NVLink round trip (~1.2 us) per field per peer — 25 us per call
+// at N=4.  Peers validate it (the analogue of the (partition, ring_step,
+// chunk, len) check at ftar.py:394-397): `fp` hashes what the member believes
+// the call is (length, geometry, dtype, n, range); `sum` binds the offsets to
+// the call's tag, so a stale writer from an aborted generation can never
+// redirect a reader.
+struct alignas(64) EntryIn {
   uint64_t flag;
-  uint64_t in_off;     // input address - arena base (mod 2^64)
-  uint64_t res_off;    // result region offset
-  uint64_t nelems;
-  uint64_t geom;       // partition cap (elements) the member folds with
-  uint32_t dtype;
-  uint32_t n;
-  uint64_t ebase;      // range calls: first element of this call in the bucket
-  uint64_t total;      // range calls: bucket length the geometry is built on
-  uint64_t out_off;    // push mode: my `out` (element 0) - arena base; ~0 = not addressable
+  uint64_t fp;       // call fingerprint
+  uint64_t in_off;   // input address - arena base (mod 2^64)
+  uint64_t res_off;  // result region offset
+  uint64_t out_off;  // push mode: `out` (element 0) - arena base; ~0 = not addressable
+  uint64_t sum;      // entry_sum(tag, fp, in_off, res_off, out_off)
 };
 
+__host__ __device__ inline uint64_t entry_sum(uint64_t tag, uint64_t fp, uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t h = tag * 0xD6E8FEB86659FD93ull ^ fp;
+  h ^= (a + 0x9E3779B97F4A7C15ull) + (h << 6) + (h >> 2);
+  h ^= (b + 0x632BE59BD9B4E019ull) + (h << 6) + (h >> 2);
+  h ^= (c + 0x85EBCA77C2B2AE63ull) + (h << 6) + (h >> 2);
+  return h;
+}
+
 struct alignas(128) ArenaHdr {
-  EntryRec entry;
+  EntryIn ent_in[kMaxMembers];      // member j's entry record for my current call
   alignas(128) uint64_t rs_done;    // flag: my slice is reduced (+kBitNonFinite)
   alignas(128) uint64_t poison;     // flag: I aborted this call (bits = reason)
   alignas(128) uint32_t rs_arrive;  // CTA arrival counters (local atomics)
@@ -145,9 +158,20 @@ __device__ __forceinline__ uint64_t ld_relaxed_gpu(const uint64_t* p) {
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_relaxed_gpu32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
+// Programmatic dependent launch: wait until the previous kernel on this stream
+// has completed (no-op unless this grid was launched with PDL allowed), and
+// let the next kernel start once every CTA of this grid has signalled.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
