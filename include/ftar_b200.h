@@ -131,6 +131,30 @@ int ftar_allreduce_sgd_launch(ftar_ctx* ctx, const void* in, int in_dtype, float
                               float* params_out, float* momentum_out, float lr, float beta,
                               void* stream);
 
+/* §8f rank 2: the intra-replica collectives of an HSDP replica (R ranks,
+ * one GPU each), replacing IntraGroup.reduce_scatter / all_gather
+ * (replica.py:241-262; tests/test_replica.py:61-97).  `ctx` is a group whose
+ * membership is the replica's ranks (ring index = rank).  Shard k of the
+ * vector is elements [offs[k], offs[k] + lens[k]) (ftar.segment_bounds at
+ * replica.py:731, or any caller-given bounds).
+ *   op 1, reduce-scatter: in = this rank's full vector (`total` elements,
+ *         f32 or bf16), out = this rank's fp32 shard (lens[rank] elements) =
+ *         sum over ranks 0..R-1 of vec_k[shard], folded rank 0 upward
+ *         (replica.py:247-249), bit-exact.
+ *   op 2, all-gather: in = this rank's fp32 shard, out = the full fp32
+ *         vector (`total` elements) on every rank (replica.py:254-262).
+ * Completion (ftar_wait) implies every rank has finished reading this rank's
+ * input, so the caller may reuse it (the reference's second barrier wait,
+ * replica.py:206-208).  Unregistered inputs are staged into the arena. */
+int ftar_intra_launch(ftar_ctx* ctx, int op, const void* in, int in_dtype, float* out,
+                      uint64_t total, const uint64_t* offs, const uint64_t* lens, void* stream);
+
+/* In-process form (all ranks on ONE device, one cooperative launch, waited
+ * with ftar_wait_local) — the shape of the reference's threaded IntraGroup. */
+int ftar_local_intra_launch(ftar_ctx** ctxs, int n, int op, const void* const* ins, int in_dtype,
+                            float* const* outs, uint64_t total, const uint64_t* offs,
+                            const uint64_t* lens, void* stream);
+
 /* In-process ring: all `n` members live on ONE device and are driven by one
  * cooperative launch (the members' kernels wait on one another, so they
  * must be co-resident).  ctxs[i] is the member at ring index i.

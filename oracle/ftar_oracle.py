@@ -119,3 +119,26 @@ def member_inputs(n: int, elems: int, seed: int = 0, dtype: str = "f32") -> list
         x = np.random.default_rng((seed, r)).standard_normal(elems).astype(np.float32)
         out.append(bf16_round(x) if dtype == "bf16" else x)
     return out
+
+
+# ---------------------------------------------------- intra-replica collectives
+
+
+def intra_reduce_scatter(vecs, bounds) -> list[np.ndarray]:
+    """replica.py:241-252 (IntraGroup.reduce_scatter): rank r's shard is
+    vec_0[b_r] + vec_1[b_r] + ..., an fp32 left fold from rank 0 upward."""
+    out = []
+    for off, ln in bounds:
+        acc = np.asarray(vecs[0], dtype=np.float32)[off:off + ln].copy()
+        for v in vecs[1:]:
+            acc += np.asarray(v, dtype=np.float32)[off:off + ln]
+        out.append(acc)
+    return out
+
+
+def intra_all_gather(shards, bounds, total: int) -> np.ndarray:
+    """replica.py:254-262 (IntraGroup.all_gather)."""
+    full = np.empty(total, dtype=np.float32)
+    for shard, (off, ln) in zip(shards, bounds):
+        full[off:off + ln] = shard
+    return full

@@ -44,6 +44,9 @@ SIGNATURES = {
                                               i32, C.c_float, u32, u32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                                               C.POINTER(vp), C.c_float, C.c_float, vp]),
     "ftar_allreduce_launch_range": (i32, [c_ctx_p, vp, i32, vp, u64, u64, u64, u64, i32, C.c_float, u32, vp]),
+    "ftar_intra_launch": (i32, [c_ctx_p, i32, vp, i32, vp, u64, C.POINTER(u64), C.POINTER(u64), vp]),
+    "ftar_local_intra_launch": (i32, [C.POINTER(c_ctx_p), i32, i32, C.POINTER(vp), i32, C.POINTER(vp), u64,
+                                      C.POINTER(u64), C.POINTER(u64), vp]),
     "ftar_local_allreduce_launch_range": (i32, [C.POINTER(c_ctx_p), i32, C.POINTER(vp), i32, C.POINTER(vp), u64,
                                                 u64, u64, u64, i32, C.c_float, u32, u32, i32, i32, vp]),
     "ftar_local_allreduce_launch": (i32, [C.POINTER(c_ctx_p), i32, C.POINTER(vp), i32,
@@ -78,6 +81,7 @@ SIGNATURES = {
 
 DT_F32 = 0
 DT_BF16 = 1
+OP_RS, OP_AG = 1, 2  # ftar_intra_launch ops
 F_SCALE = 1
 F_PROTOCOL = 2
 

@@ -80,6 +80,9 @@ struct LaunchParams {
   int rs_layout;                 // 0: contiguous span per CTA, 1: grid-strided tiles
   int diag;                      // timing diagnostics: 1 = RS stores skipped, 2 = RS reads local only
   int rs_ctas;                   // CTAs that reduce (the rest only all-gather); <= gridDim.x
+  uint32_t intra_op;             // intra-replica collective (kIntraRS / kIntraAG), 0 = FTAR
+  uint64_t seg_off[kMaxMembers]; // intra: rank k's shard is elements [seg_off[k], +seg_len[k])
+  uint64_t seg_len[kMaxMembers];
 };
 
 __device__ __forceinline__ uint32_t severity_code(uint32_t st) {
@@ -1077,6 +1080,215 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
   }
 }
 
+// ------------------------------------------------- intra-replica collectives
+// IntraGroup.reduce_scatter / all_gather (replica.py:241-262)
+// across the R GPUs of one replica (HSDP, R > 1), over NVLink peer loads.
+//   RS: rank r's shard = vec_0[b_r] + vec_1[b_r] + ... + vec_{R-1}[b_r], the
+//       fold running rank 0 upward on every rank (replica.py:247-249,
+//       tests/test_replica.py:71-86), fp32 (bf16 inputs upcast exactly).
+//   AG: full[b_k] = shard_k for every rank k (replica.py:254-262).
+// Same entry protocol as allreduce_kernel (pushed, tag-bound entry records).
+// A closing barrier - every peer has finished reading my input - lets the
+// caller reuse its buffer on return, like the reference's second barrier wait
+// (replica.py:206-208).
+constexpr uint32_t kIntraRS = 1, kIntraAG = 2;
+
+__device__ __forceinline__ uint64_t intra_fingerprint(const LaunchParams& p, int n) {
+  uint64_t h = call_fingerprint(p, n) ^ ((uint64_t)p.intra_op * 0xC2B2AE3D27D4EB4Full);
+  for (int k = 0; k < n; ++k) h ^= (p.seg_off[k] * 131 + p.seg_len[k] + 0x165667B19E3779F9ull) + (h << 6) + (h >> 2);
+  return h;
+}
+
+template <int N, class In>
+__global__ void __launch_bounds__(kThreads, 1) intra_kernel(const __grid_constant__ LaunchParams p) {
+  using T = typename In::T;
+  constexpr int U = Unroll<N, In>::U;
+  const int me = p.emulated ? (int)blockIdx.y : p.self;
+  char* const mybase = p.base[me];
+  ArenaHdr* const hdr = reinterpret_cast<ArenaHdr*>(mybase);
+  HostCtl* const ctl = p.ctl[me];
+  const uint64_t tag = p.tag;
+  const int tid = threadIdx.x;
+  const bool ag = p.intra_op == kIntraAG;
+  __shared__ uint64_t s_pin[N];
+  __shared__ const T* s_src[N];
+  __shared__ uint32_t s_status;
+  __shared__ int s_blame;
+  __shared__ uint64_t s_t0;
+
+  if (tid == 0) {
+    s_status = ST_OK;
+    s_blame = -1;
+    s_t0 = globaltimer_ns();
+  }
+  // ---- 1. entry: publish my record, collect every peer's (warp 0, CTA 0)
+  if (blockIdx.x == 0 && tid < 32) {
+    __syncwarp();
+    const uint64_t fp = intra_fingerprint(p, N);
+    if (tid == 0) {
+      const uint64_t sum = entry_sum(tag, fp, p.in_off[me], 0, ~0ull);
+      for (int jj = 1; jj < N; ++jj) {
+        EntryIn* e = &reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->ent_in[me];
+        st_relaxed_sys(&e->fp, fp);
+        st_relaxed_sys(&e->in_off, p.in_off[me]);
+        st_relaxed_sys(&e->res_off, 0);
+        st_relaxed_sys(&e->out_off, ~0ull);
+        st_relaxed_sys(&e->sum, sum);
+      }
+      if (N > 1) fence_acq_rel_sys();
+      for (int jj = 1; jj < N; ++jj)
+        st_relaxed_sys(&reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->ent_in[me].flag, mk_flag(tag, 0));
+      if (ctl->epoch != tag_gen(tag)) {
+        s_status = ST_PROTOCOL;
+        s_blame = me;
+      }
+      ctl->started = tag;
+    }
+    __syncwarp();
+    const int j = tid;
+    uint32_t st = ST_OK;
+    if (s_status == ST_OK && j < N) {
+      if (j == me) {
+        s_pin[j] = reinterpret_cast<uint64_t>(mybase) + p.in_off[me];
+      } else {
+        ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
+        EntryIn* e = &hdr->ent_in[j];
+        st = wait_flag(&e->flag, tag, &ph->poison, ctl, nullptr, s_t0, p.hard_timeout_ns, nullptr);
+        if (st == ST_OK) {
+          const uint64_t efp = ld_relaxed_sys(&e->fp), in_off = ld_relaxed_sys(&e->in_off);
+          const uint64_t r0 = ld_relaxed_sys(&e->res_off), oo = ld_relaxed_sys(&e->out_off);
+          const uint64_t sum = ld_relaxed_sys(&e->sum);
+          if (efp != fp) st = ST_PROTOCOL;  // a different collective or different bounds
+          else if (sum != entry_sum(tag, efp, in_off, r0, oo)) st = ST_PEER_RESET;
+          s_pin[j] = reinterpret_cast<uint64_t>(p.base[j]) + in_off;
+        }
+      }
+    }
+    const uint32_t bad = __ballot_sync(0xffffffffu, st != ST_OK);
+    const uint32_t st_first = __shfl_sync(0xffffffffu, st, bad ? __ffs(bad) - 1 : 0);
+    if (tid == 0 && bad) {
+      s_status = st_first;
+      s_blame = __ffs(bad) - 1;
+    }
+  }
+  __syncthreads();
+  // ---- 2. fan out to my CTAs
+  if (blockIdx.x == 0) {
+    if (tid == 0) {
+      hdr->tph[0] = s_t0;
+      if (s_status == ST_OK) {
+        for (int k = 0; k < N; ++k) hdr->peer_in[k] = s_pin[k];
+        st_release_gpu(&hdr->go, mk_flag(tag, 1));
+      }
+      hdr->tph[1] = globaltimer_ns();
+    }
+    __syncthreads();
+    if (s_status == ST_OK && tid < N) s_src[tid] = reinterpret_cast<const T*>(s_pin[tid]);
+  } else {
+    if (tid == 0 && s_status == ST_OK) {
+      const uint32_t st = wait_go(hdr, mk_flag(tag, 1), s_t0, p.hard_timeout_ns);
+      if (st != ST_OK) s_status = st;
+    }
+    __syncthreads();
+    if (s_status == ST_OK && tid < N) s_src[tid] = reinterpret_cast<const T*>(ld_relaxed_gpu(&hdr->peer_in[tid]));
+  }
+  __syncthreads();
+
+  // ---- 3. the collective
+  if (s_status == ST_OK) {
+    float* const out = p.out[me];
+    if (!ag) {
+      const uint64_t off = p.seg_off[me], len = p.seg_len[me];
+      uint64_t orbits = reinterpret_cast<uint64_t>(out - off);
+      for (int k = 0; k < N; ++k) orbits |= reinterpret_cast<uint64_t>(s_src[k]);
+      const bool vec_ok = (orbits & 15u) == 0;
+      // one contiguous span of my shard per CTA, folded in tiles
+      const uint64_t G = gridDim.x;
+      const uint64_t per = ((len + G - 1) / G + 7) & ~7ull;
+      const uint64_t a0 = off + umin((uint64_t)blockIdx.x * per, len);
+      const uint64_t a1 = off + umin((uint64_t)blockIdx.x * per + per, len);
+      const uint64_t TL = (uint64_t)kThreads * 4 * U;
+      uint32_t nf = 0;
+      for (uint64_t a = a0; a < a1; a += TL)
+        fold_range<N, In, U>(s_src, SinkOne{out - off}, a, umin(a + TL, a1), 0, 0xffffffffu, vec_ok, false, 1.0f, nf);
+    } else {
+      // every CTA starts on a different rank so all links stay busy
+      for (int i = 0; i < N; ++i) {
+        const int k = (int)((me + 1 + blockIdx.x + i) % N);
+        const float* src = reinterpret_cast<const float*>(s_src[k]);
+        float* dst = out + p.seg_off[k];
+        const bool vec_ok = ((reinterpret_cast<uint64_t>(src) | reinterpret_cast<uint64_t>(dst)) & 15u) == 0;
+        copy_f32<8>(dst, src, p.seg_len[k], vec_ok);
+      }
+    }
+  }
+  __syncthreads();
+  // ---- 4. closing barrier: I am done reading every peer's input
+  if (tid == 0) {
+    if (s_status != ST_OK && s_status != ST_FOLLOW) {
+      atomicMax(&hdr->err, severity_code(s_status));
+      hdr->err_peer = s_blame;
+      st_release_sys(&hdr->poison, mk_flag(tag, s_status));
+    }
+    if (gridDim.x > 1) __threadfence();
+    const uint32_t old = gridDim.x > 1 ? atomicAdd(&hdr->rs_arrive, 1u) : 0u;
+    if (old == gridDim.x - 1) {
+      fence_acq_rel_gpu();
+      if (ld_relaxed_gpu32(&hdr->err) == 0) {
+        // every CTA's loads have returned (their values are stored): tell the
+        // peers they may let their callers reuse the buffers I read
+        for (int jj = 1; jj < N; ++jj)
+          st_relaxed_sys(&reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->ag_in[me], mk_flag(tag, 0));
+      }
+      hdr->tph[2] = globaltimer_ns();
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0 && s_status == ST_OK) {
+    for (int jj = 1; jj < N; ++jj) {
+      const int j = (me + jj) % N;
+      const uint32_t st = wait_flag(&hdr->ag_in[j], tag, &reinterpret_cast<ArenaHdr*>(p.base[j])->poison, ctl,
+                                    &hdr->err, s_t0, p.hard_timeout_ns, nullptr);
+      if (st != ST_OK) {
+        s_status = st;
+        s_blame = j;
+        break;
+      }
+    }
+    hdr->tph[3] = globaltimer_ns();
+  }
+  __syncthreads();
+  // ---- 5. completion (as allreduce_kernel: no sys fence on success)
+  if (tid == 0) {
+    const uint32_t st = s_status;
+    if (st != ST_OK && st != ST_FOLLOW) {
+      atomicMax(&hdr->err, severity_code(st));
+      hdr->err_peer = s_blame;
+      st_release_sys(&hdr->poison, mk_flag(tag, st));
+    }
+    if (gridDim.x > 1) __threadfence();
+    const uint32_t old = gridDim.x > 1 ? atomicAdd(&hdr->done_arrive, 1u) : 0u;
+    if (old == gridDim.x - 1) {
+      fence_acq_rel_gpu();
+      const uint32_t err = ld_relaxed_gpu32(&hdr->err);
+      const int64_t blame = hdr->err_peer;
+      ctl->progress = 1;
+      hdr->tph[4] = globaltimer_ns();
+      for (int i = 0; i < 5; ++i) ctl->tphase[i] = hdr->tph[i];
+      hdr->rs_arrive = 0;
+      hdr->done_arrive = 0;
+      hdr->nonfinite = 0;
+      hdr->err = 0;
+      hdr->err_peer = -1;
+      hdr->tiles_done = 0;
+      if (err) {
+        ctl->detail = blame;
+        __threadfence_system();
+      }
+      ctl->done = mk_flag(tag, err & 0xffu);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- operators
 template <class In>
 __global__ void __launch_bounds__(256) accumulate_kernel(float* __restrict__ dst,
@@ -1644,6 +1856,32 @@ cudaError_t launch_small_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bo
   }
   fn<<<grid, kThreads, 0, st>>>(p);
   return cudaGetLastError();
+}
+
+template <int N, class In>
+cudaError_t launch_intra_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop) {
+  auto fn = intra_kernel<N, In>;
+  if (coop) {
+    void* args[] = {const_cast<LaunchParams*>(&p)};
+    return cudaLaunchCooperativeKernel((const void*)fn, grid, dim3(kThreads), args, 0, st);
+  }
+  fn<<<grid, kThreads, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <class In>
+cudaError_t launch_intra(int n, const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop) {
+  switch (n) {
+    case 1: return launch_intra_n<1, In>(p, grid, st, coop);
+    case 2: return launch_intra_n<2, In>(p, grid, st, coop);
+    case 3: return launch_intra_n<3, In>(p, grid, st, coop);
+    case 4: return launch_intra_n<4, In>(p, grid, st, coop);
+    case 5: return launch_intra_n<5, In>(p, grid, st, coop);
+    case 6: return launch_intra_n<6, In>(p, grid, st, coop);
+    case 7: return launch_intra_n<7, In>(p, grid, st, coop);
+    case 8: return launch_intra_n<8, In>(p, grid, st, coop);
+  }
+  return cudaErrorInvalidValue;
 }
 
 template <class In>
@@ -2269,6 +2507,139 @@ int ftar_poll(ftar_ctx* c, int* status, uint64_t* progress) {
   const uint64_t d = h->done;
   if (progress) *progress = h->progress;
   if (status) *status = flag_tag(d) == c->q_tag[c->q_head] ? (int)(d & 0xff) : FTAR_ST_PENDING;
+  return FTAR_OK;
+}
+
+// ---- intra-replica collectives (§8f rank 2) -------------------------------
+static int intra_check(int op, int in_dtype, int n, uint64_t total, const uint64_t* offs, const uint64_t* lens) {
+  if (op != (int)kIntraRS && op != (int)kIntraAG) return fail(FTAR_ST_INVARIANT, "op must be 1 (RS) or 2 (AG)");
+  if (in_dtype != FTAR_DT_F32 && in_dtype != FTAR_DT_BF16) return fail(FTAR_ST_INVARIANT, "dtype must be f32 or bf16");
+  if (op == (int)kIntraAG && in_dtype != FTAR_DT_F32) return fail(FTAR_ST_INVARIANT, "all-gather shards are fp32");
+  if (n < 1 || n > kMaxMembers) return fail(FTAR_ST_INVARIANT, "1..8 ranks");
+  if (!offs || !lens) return fail(FTAR_ST_INVARIANT, "null bounds");
+  for (int k = 0; k < n; ++k)
+    if (offs[k] > total || lens[k] > total - offs[k]) return fail(FTAR_ST_INVARIANT, "shard bounds exceed the vector");
+  return FTAR_OK;
+}
+
+static void intra_grid_params(LaunchParams& p, int op, int in_dtype, uint64_t total, const uint64_t* offs,
+                              const uint64_t* lens, int n) {
+  p.intra_op = (uint32_t)op;
+  p.nelems = total;
+  p.total = total;
+  p.cap = 0;
+  p.ebase = 0;
+  p.dtype = (uint32_t)in_dtype;
+  p.contrib = (n >= 32) ? 0xffffffffu : ((1u << n) - 1u);
+  for (int k = 0; k < n; ++k) {
+    p.seg_off[k] = offs[k];
+    p.seg_len[k] = lens[k];
+  }
+}
+
+static int intra_ctas(int op, int in_dtype, uint64_t total, const uint64_t* lens, int self, int n) {
+  // ~64 KB of my work per CTA, like the all-reduce grid sizing
+  uint64_t work = op == (int)kIntraRS ? lens[self] * (in_dtype == FTAR_DT_BF16 ? 2 : 4) : total * 4 / (uint64_t)n;
+  const uint64_t per = (uint64_t)env_int("FTAR_BYTES_PER_CTA", 64 << 10);
+  const int cap = g_ctas > 0 ? g_ctas : 64;
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)cap, (work + per - 1) / per));
+}
+
+int ftar_intra_launch(ftar_ctx* c, int op, const void* in, int in_dtype, float* out, uint64_t total,
+                      const uint64_t* offs, const uint64_t* lens, void* stream) {
+  if (!c) return fail(FTAR_ST_INVARIANT, "null ctx");
+  int v = intra_check(op, in_dtype, c->n, total, offs, lens);
+  if (v) return v;
+  if (c->q_count == kQueue) return fail(FTAR_ST_INVARIANT, "queue full: wait for the oldest first");
+  const uint64_t esz = in_dtype == FTAR_DT_BF16 ? 2 : 4;
+  const uint64_t in_bytes = op == (int)kIntraRS ? total * esz : lens[c->self] * 4;
+  if (in_bytes > c->max_bucket_bytes) return fail(FTAR_ST_INVARIANT, "input exceeds the group's staging capacity");
+  const uint64_t out_elems = op == (int)kIntraRS ? lens[c->self] : total;
+  if ((in_bytes && !in) || (out_elems && !out)) return fail(FTAR_ST_INVARIANT, "null buffer");
+  DeviceGuard g(c->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  c->seq += 1;
+  const uint64_t tag = mk_tag(c->gen, c->seq);
+  const char* inp = static_cast<const char*>(in);
+  uint64_t in_off;
+  const bool registered = inp >= c->arena + c->pool_off && inp + in_bytes <= c->arena + c->arena_bytes;
+  if (registered || c->n == 1) {
+    in_off = (uint64_t)(inp - c->arena);
+  } else {
+    // peers can only address my arena: stage the input there (the closing
+    // barrier keeps it alive until every peer has read it)
+    const uint64_t so = c->stage_off[c->seq & 1];
+    if (in_bytes) CK(cudaMemcpyAsync(c->arena + so, in, in_bytes, cudaMemcpyDeviceToDevice, st));
+    in_off = so;
+  }
+  LaunchParams p{};
+  intra_grid_params(p, op, in_dtype, total, offs, lens, c->n);
+  for (int i = 0; i < c->n; ++i) p.base[i] = (i == c->self) ? c->arena : c->peer[c->ring_slots[i]];
+  c->push(tag);
+  p.ctl[c->self] = c->ctl_d;
+  p.out[c->self] = out;
+  p.in_off[c->self] = in_off;
+  p.tag = tag;
+  p.hard_timeout_ns = c->hard_timeout_ns;
+  p.self = c->self;
+  p.emulated = 0;
+  p.fault_member = -1;
+  const dim3 grid(intra_ctas(op, in_dtype, total, lens, c->self, c->n), 1);
+  cudaError_t e = in_dtype == FTAR_DT_BF16 ? launch_intra<BF16In>(c->n, p, grid, st, false)
+                                            : launch_intra<F32In>(c->n, p, grid, st, false);
+  if (e != cudaSuccess) {
+    c->pop_last();
+    return cuda_fail(e, "intra-replica collective launch");
+  }
+  return FTAR_OK;
+}
+
+int ftar_local_intra_launch(ftar_ctx** ctxs, int n, int op, const void* const* ins, int in_dtype, float* const* outs,
+                            uint64_t total, const uint64_t* offs, const uint64_t* lens, void* stream) {
+  int v = intra_check(op, in_dtype, n, total, offs, lens);
+  if (v) return v;
+  if (!ctxs || !ins || !outs) return fail(FTAR_ST_INVARIANT, "null arrays");
+  const int dev = ctxs[0]->device;
+  for (int i = 0; i < n; ++i) {
+    ftar_ctx* c = ctxs[i];
+    if (!c || c->device != dev) return fail(FTAR_ST_INVARIANT, "in-process ranks must share a device");
+    if (c->q_count) return fail(FTAR_ST_INVARIANT, "in-process groups run one collective at a time");
+    if (c->gen != ctxs[0]->gen || c->seq != ctxs[0]->seq)
+      return fail(FTAR_ST_PROTOCOL, "ranks disagree on (generation, call sequence)");
+    const uint64_t in_elems = op == (int)kIntraRS ? total : lens[i], out_elems = op == (int)kIntraRS ? lens[i] : total;
+    if ((!ins[i] && in_elems) || (!outs[i] && out_elems)) return fail(FTAR_ST_INVARIANT, "null buffer");
+  }
+  DeviceGuard g(dev);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  LaunchParams p{};
+  intra_grid_params(p, op, in_dtype, total, offs, lens, n);
+  uint64_t tag = 0;
+  for (int i = 0; i < n; ++i) {
+    ftar_ctx* c = ctxs[i];
+    c->seq += 1;
+    tag = mk_tag(c->gen, c->seq);
+    c->push(tag);
+    p.base[i] = c->arena;
+    p.ctl[i] = c->ctl_d;
+    p.out[i] = outs[i];
+    p.in_off[i] = (uint64_t)(static_cast<const char*>(ins[i]) - c->arena);  // same process: any address
+  }
+  p.tag = tag;
+  p.hard_timeout_ns = ctxs[0]->hard_timeout_ns;
+  p.self = 0;
+  p.emulated = 1;
+  p.fault_member = -1;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int G = intra_ctas(op, in_dtype, total, lens, 0, n);
+  G = std::max(1, std::min(G, std::max(1, sms / n)));  // cooperative: every rank's CTAs co-resident
+  const dim3 grid(G, n);
+  cudaError_t e = in_dtype == FTAR_DT_BF16 ? launch_intra<BF16In>(n, p, grid, st, true)
+                                            : launch_intra<F32In>(n, p, grid, st, true);
+  if (e != cudaSuccess) {
+    for (int i = 0; i < n; ++i) ctxs[i]->pop_last();
+    return cuda_fail(e, "in-process intra-replica cooperative launch");
+  }
   return FTAR_OK;
 }
 

@@ -79,3 +79,42 @@ def case_inputs(spec: dict, garbage_behind: bool = False) -> list[np.ndarray]:
         arrays[b] = (rng.standard_normal(e).astype(np.float32) if garbage_behind
                      else np.zeros(e, dtype=np.float32))
     return arrays
+
+
+def intra_cases() -> list[dict]:
+    """Intra-replica reduce-scatter / all-gather cases (replica.py:241-262):
+    the reference tests' shapes (tests/test_replica.py:61-97: hand values,
+    n in 2..4 with a remainder-carrying last shard) plus segment_bounds
+    splits (replica.py:731) and empty / uneven shards, n = 1..8."""
+    rng = np.random.default_rng(0x1A7A)
+    out = []
+
+    def seg(total, n):
+        base, rem = divmod(total, n)
+        b, off = [], 0
+        for r in range(n):
+            ln = base + (1 if r < rem else 0)
+            b.append([off, ln])
+            off += ln
+        return b
+
+    for i in range(24):
+        n = int(rng.integers(2, 5))
+        total = int(rng.integers(n, 40))
+        cut = total // n
+        out.append(dict(n=n, total=total, seed=100 + i, kind="f32",
+                        bounds=[[r * cut, cut if r < n - 1 else total - (n - 1) * cut] for r in range(n)]))
+    for i, (n, total) in enumerate([(1, 17), (2, 1), (3, 2), (5, 1001), (7, 4097), (8, 65537), (8, 8),
+                                    (4, 300_007), (6, 123_457), (2, 1 << 18)]):
+        out.append(dict(n=n, total=total, seed=200 + i, kind="f32", bounds=seg(total, n)))
+    for i, (n, total) in enumerate([(4, 99_999), (8, 40_000), (3, 7)]):
+        out.append(dict(n=n, total=total, seed=300 + i, kind="bf16", bounds=seg(total, n)))
+    # uneven, empty and unaligned shards (any caller-given bounds)
+    for i in range(6):
+        n = int(rng.integers(2, 9))
+        total = int(rng.integers(0, 5000))
+        cuts = sorted(int(c) for c in rng.integers(0, total + 1, size=n - 1))
+        edges = [0, *cuts, total]
+        out.append(dict(n=n, total=total, seed=400 + i, kind="f32",
+                        bounds=[[edges[r], edges[r + 1] - edges[r]] for r in range(n)]))
+    return out

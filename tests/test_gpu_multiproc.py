@@ -230,6 +230,37 @@ def _worker(rank, world, port, scenario, outdir):
             good = all(np.array_equal(o.cpu().numpy(), orc.oracle_reduce(bk, 8 << 20, 4) * np.float32(0.5))
                        for bk, o in zip(bks, outs))
             (res["ok"] if good else res["errors"]).append("regrouped_queue")
+        elif scenario == "intra":
+            # §8f rank 2: the replica's ranks reduce-scatter / all-gather over
+            # NVLink (one process per GPU), bit-exact vs the reference goldens
+            from paper_2602_00277_b200.intra import IntraRank, segment_bounds
+            ir = IntraRank(rank, world, StoreFabric(dist.PrefixStore("intra/0", store)), device=dev,
+                           max_bytes=16 << 20, pool_bytes=48 << 20)
+            with open(os.path.join(ROOT, "tests", "golden", "intra_cases.json")) as f:
+                cases = [c for c in json.load(f) if c["n"] == world]
+            for c in cases:
+                vecs = member_inputs(world, c["total"], c["seed"], c["kind"])
+                bounds = [tuple(b) for b in c["bounds"]]
+                v = torch.from_numpy(vecs[rank]).to(dev)
+                if c["kind"] == "bf16":
+                    v = v.to(torch.bfloat16)
+                shard = ir.reduce_scatter(rank, v, bounds)
+                full = ir.all_gather(rank, shard, bounds, c["total"])
+                good = sha(shard.cpu().numpy()) == c["rs_sha"][rank] and sha(full.cpu().numpy()) == c["ag_sha"]
+                (res["ok"] if good else res["errors"]).append(f"intra{c['seed']}")
+            # registered (zero-copy) bf16 vector, 4M elements, segment_bounds
+            total = 4_000_037
+            vecs = member_inputs(world, total, 9, "bf16")
+            bounds = segment_bounds(total, world)
+            v = ir.alloc(total, torch.bfloat16)
+            v.copy_(torch.from_numpy(vecs[rank]).to(dev).to(torch.bfloat16))
+            shard = ir.reduce_scatter(rank, v, bounds)
+            want = orc.intra_reduce_scatter(vecs, bounds)
+            full = ir.all_gather(rank, shard, bounds, total)
+            good = np.array_equal(shard.cpu().numpy(), want[rank]) and \
+                np.array_equal(full.cpu().numpy(), orc.intra_all_gather(want, bounds, total))
+            (res["ok"] if good else res["errors"]).append("intra_big")
+            ir.close()
         elif scenario == "catchup":
             from paper_2602_00277_b200 import checkpoint as ck
             snap = ck.SnapshotStore(capacity_bytes=64 << 20, device=dev, fabric=fabric, rank=0, replica_id=rank)
@@ -338,6 +369,13 @@ def test_failed_async_queue_is_drained():
         assert "regrouped_queue" in r["ok"]
     for r in res[:-1]:
         assert "all_failed:4" in r["ok"] and "queues_empty" in r["ok"]
+
+
+def test_intra_replica_collectives_over_nvlink():
+    res = run("intra", world_size())
+    for r in res:
+        assert not r["errors"], r["errors"]
+        assert "intra_big" in r["ok"] and len(r["ok"]) >= 2
 
 
 def test_catchup_pull_over_nvlink():

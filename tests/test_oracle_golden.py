@@ -128,3 +128,35 @@ def test_reference_compiled_kernel_matches_port():
     want = dst + src
     mod.accumulate(dst, memoryview(src.tobytes()).cast("B"))
     np.testing.assert_array_equal(dst, want)
+
+
+# --- intra-replica collectives (replica.py:241-262), pinned to the reference ----
+
+
+def _intra_cases():
+    with open(os.path.join(GOLD, "intra_cases.json")) as f:
+        return json.load(f)
+
+
+def test_intra_oracle_matches_reference_goldens():
+    def sha(a):
+        return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float32).tobytes()).hexdigest()
+
+    cases = _intra_cases()
+    assert len(cases) >= 40
+    for c in cases:
+        vecs = member_inputs(c["n"], c["total"], c["seed"], c["kind"])
+        bounds = [tuple(b) for b in c["bounds"]]
+        shards = orc.intra_reduce_scatter(vecs, bounds)
+        assert [sha(s) for s in shards] == c["rs_sha"], c
+        assert sha(orc.intra_all_gather(shards, bounds, c["total"])) == c["ag_sha"], c
+
+
+def test_intra_oracle_hand_values():
+    """tests/test_replica.py:61-68 and :89-97."""
+    vecs = [np.array([1, 2, 3, 4], dtype=np.float32), np.array([10, 20, 30, 40], dtype=np.float32)]
+    s = orc.intra_reduce_scatter(vecs, [(0, 2), (2, 2)])
+    assert s[0].tolist() == [11.0, 22.0] and s[1].tolist() == [33.0, 44.0]
+    full = np.arange(10, dtype=np.float32)
+    b = [(0, 4), (4, 3), (7, 3)]
+    assert np.array_equal(orc.intra_all_gather([full[o:o + n] for o, n in b], b, 10), full)
