@@ -199,7 +199,8 @@ def workload_config(args, n):
             "in_dtype": args.dtype, "out_dtype": "f32", "chunk_bytes": 8 * MIB, "max_in_flight": 4,
             "fused": "x f32(1/n) normalisation" + (", bf16->fp32 cast" if args.dtype == "bf16" else ""),
             "result": "in place" if args.inplace else "out-of-place fp32 (out=)",
-            "kernel": "in-process one-shot (cooperative)" if emu else "two-shot NVLink pull",
+            "kernel": "in-process one-shot" if emu else "two-shot NVLink (push all-gather)",
+            "queue_depth": args.depth,
             "l2": "inputs larger than L2 (126 MB) per GPU; no flush needed",
             "parallelism": f"dp{n}" + (" (emulated)" if emu else "")}
 
@@ -237,14 +238,31 @@ def run_single(args):
     scale = 1.0 / n
     stream = torch.cuda.current_stream(dev)
 
+    # queued like the N>=2 path (--depth buckets in flight, as a bucketed
+    # backward pass issues them); each launch is still waited and checked
+    from collections import deque
+    pend = deque()
+
+    def collect():
+        for st in ring.wait(pend.popleft(), cfg):
+            if st:
+                raise RuntimeError(f"all-reduce failed with status {st}")
+
     def step():
-        ring.all_reduce(bufs, cfg, outs=outs, scale=scale)
+        pend.append(ring.launch(bufs, cfg, outs=outs, scale=scale))
+        while len(pend) >= max(1, args.depth):
+            collect()
+
+    def drain():
+        while pend:
+            collect()
 
     for _ in range(args.warmup):
         step()
+    drain()
     torch.cuda.synchronize()
     with ClockSampler(0) as clk:
-        total, per_launch = timed_loop(step, args.steps, stream, torch)
+        total, per_launch = timed_loop(step, args.steps, stream, torch, drain=drain)
     t_step = total / args.steps
     value = busbw(elems * in_bytes, t_step, n)
     peaks = measured_peaks()

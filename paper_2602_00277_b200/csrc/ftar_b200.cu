@@ -1434,6 +1434,7 @@ struct LocalParams {
   HostCtl* ctl[kMaxMembers];
   float* stage;             // nullptr: direct mode (outputs never alias inputs)
   uint32_t* flags;          // [0] nonfinite
+  uint32_t* arrive;         // direct mode: CTA arrival counter (no grid barrier)
   uint64_t tag[kMaxMembers];
   uint64_t nelems;
   uint64_t p_base, p_rem;
@@ -1490,6 +1491,28 @@ __global__ void __launch_bounds__(kThreads, 1) local_oneshot_kernel(const __grid
   if (__any_sync(0xffffffffu, nf != 0) && (tid & 31) == 0) atomicOr(&s_nf, 1u);
   __syncthreads();
   if (tid == 0 && s_nf) atomicOr(p.flags, 1u);
+  if (direct) {
+    // Direct mode wrote every output during the fold (outputs are undefined
+    // after a non-finite sum, as for out-of-place calls), so only the status
+    // needs every CTA: an arrival counter instead of a grid barrier, which
+    // also lets this mode launch without the cooperative-launch overhead.
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(p.arrive, 1u) == gridDim.x - 1) {
+        fence_acq_rel_gpu();
+        const bool nonfinite = ld_relaxed_gpu32(p.flags) != 0;
+        *p.flags = 0;
+        *p.arrive = 0;
+        for (int j = 0; j < N; ++j) {
+          p.ctl[j]->progress = ntiles + 1;
+          if (nonfinite) p.ctl[j]->detail = -1;
+        }
+        if (nonfinite) __threadfence_system();
+        for (int j = 0; j < N; ++j) p.ctl[j]->done = mk_flag(p.tag[j], nonfinite ? ST_NUMERICAL : ST_OK);
+      }
+    }
+    return;
+  }
   grid.sync();
   const bool bad = ld_relaxed_sys32(p.flags) != 0;
   if (!bad && !direct) {
@@ -1935,6 +1958,8 @@ cudaError_t oneshot_dispatch(int n, const LocalParams& lp, dim3 grid, cudaStream
 #undef CASE
     default: return cudaErrorInvalidValue;
   }
+  // the staged (in-place) mode needs its grid barrier; direct mode does not
+  if (lp.stage == nullptr) return cudaLaunchKernel(fn, grid, dim3(kThreads), args, 0, st);
   return cudaLaunchCooperativeKernel(fn, grid, dim3(kThreads), args, 0, st);
 }
 
@@ -2350,7 +2375,9 @@ static int launch_local(ftar_ctx** ctxs, int n, const void* const* ins, int in_d
   for (int i = 0; i < n; ++i) {
     ftar_ctx* c = ctxs[i];
     if (!c || c->device != dev) return fail(FTAR_ST_INVARIANT, "in-process ring members must share a device");
-    if (c->q_count) return fail(FTAR_ST_INVARIANT, "in-process rings run one all-reduce at a time");
+    // queued launches run back to back on the stream; ftar_wait_local
+    // collects each member's oldest (FIFO), like ftar_wait
+    if (c->q_count == kQueue) return fail(FTAR_ST_INVARIANT, "queue full: wait for the oldest first");
     if (n_elems * 4 > 2 * c->max_bucket_bytes)
       return fail(FTAR_ST_INVARIANT, "bucket exceeds the ring group's arena capacity");
     if (c->gen != ctxs[0]->gen || c->seq != ctxs[0]->seq)
@@ -2434,6 +2461,7 @@ static int launch_local(ftar_ctx** ctxs, int n, const void* const* ins, int in_d
       }
     lp.stage = alias ? reinterpret_cast<float*>(ctxs[0]->arena + ctxs[0]->res_off) : nullptr;
     lp.flags = &h0->nonfinite;
+    lp.arrive = &h0->done_arrive;
     lp.nelems = n_elems;
     lp.p_base = p.p_base;
     lp.p_rem = p.p_rem;

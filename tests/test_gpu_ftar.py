@@ -511,3 +511,25 @@ def test_fused_sgd_momentum_bit_exact(ftar, rings, dtype):
         np.testing.assert_array_equal(mout[i].cpu().numpy(), mw)
         np.testing.assert_array_equal(params[i].cpu().numpy(), p0)  # inputs untouched (commit is the caller's)
         np.testing.assert_array_equal(moms[i].cpu().numpy(), m0)
+
+
+def test_local_ring_queued_launches(ftar):
+    """In-process rings queue like the multi-GPU path: three buckets in
+    flight on one stream, collected oldest first, each bit-exact."""
+    ring = ftar.LocalRing(4, device=DEV, max_bucket_bytes=8 << 20)
+    try:
+        cfg = ftar.PipelineConfig()
+        jobs = []
+        for b in range(3):
+            arrays = member_inputs(4, 1_000_003 + b, seed=600 + b)
+            bufs = [to_dev(a) for a in arrays]
+            outs = [torch.empty_like(x) for x in bufs]
+            jobs.append((arrays, outs, ring.launch(bufs, cfg, outs=outs, scale=0.25)))
+        for arrays, outs, tok in jobs:
+            assert ring.wait(tok, cfg) == [0] * 4
+            want = orc.normalize(orc.oracle_reduce(arrays, cfg.chunk_bytes, cfg.max_in_flight), 4)
+            for o in outs:
+                np.testing.assert_array_equal(o.cpu().numpy(), want)
+    finally:
+        for g in ring.groups:
+            g.close()
