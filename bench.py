@@ -205,6 +205,20 @@ def workload_config(args, n):
             "parallelism": f"dp{n}" + (" (emulated)" if emu else "")}
 
 
+def _ncu_traffic(args):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the N=1
+    kernel, from the committed ncu --set full capture of this exact default
+    workload (profiles/r01/ncu/summary.json); None for any other workload."""
+    if args.dtype != "f32" or args.bucket_mib != 256 or args.replicas != 4 or args.inplace:
+        return None
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "ncu",
+                               "summary.json")) as f:
+            return json.load(f)["per_launch"]["traffic_bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def timed_loop(fn, steps, stream, torch, drain=None):
     """Run fn() `steps` times; CUDA events per launch and around the loop."""
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
@@ -269,7 +283,8 @@ def run_single(args):
     alg_bytes = n * elems * (in_bytes + 4)
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     roof = {"bound": "hbm", "achieved": round(alg_bytes / per_launch / 1e9, 1), "peak": hbm_peak,
-            "unit": "GB/s", "frac": round(alg_bytes / per_launch / 1e9 / hbm_peak, 4), "traffic": args.traffic,
+            "unit": "GB/s", "frac": round(alg_bytes / per_launch / 1e9 / hbm_peak, 4),
+            "traffic": args.traffic if args.traffic is not None else _ncu_traffic(args),
             "kernel": "local_oneshot_kernel",
             "algorithmic_bytes_per_launch": alg_bytes,
             "definition": "n*E*(in_bytes+4): every replica's bucket read once, every replica's fp32 result "
