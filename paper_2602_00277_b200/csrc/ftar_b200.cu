@@ -950,25 +950,23 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
   __shared__ uint32_t s_status, s_nf;
   __shared__ int s_blame;
   __shared__ uint64_t s_t0;
+  __shared__ uint64_t s_t1;
   if (tid == 0) {
     s_status = ST_OK;
     s_nf = 0;
     s_blame = -1;
     s_t0 = globaltimer_ns();
-    if (blockIdx.x == 0) {
-      ctl->started = tag;
-      hdr->tph[0] = s_t0;
-      if (ctl->epoch != tag_gen(tag)) {
-        s_status = ST_PROTOCOL;
-        s_blame = me;
-      }
-    }
+    s_t1 = 0;
   }
   __syncthreads();
   const uint64_t fp = call_fingerprint(p, N);
   const bool contributes = (p.contrib >> me) & 1u;
-  // 1. push my input to every peer (grid-stride 16-byte copies)
-  if (s_status == ST_OK && contributes && bytes) {
+  // 1. push my input to every peer (grid-stride 16-byte copies).  Under PDL
+  // this overlaps the previous call's tail: it writes only the peers' receive
+  // slots of THIS call's parity (the call before used the other one, and the
+  // call two back finished reading this one before the previous call could
+  // complete), a counter private to this parity, and the peers' arrival words.
+  if (contributes && bytes) {
     const uint64_t stride = (uint64_t)gridDim.x * kThreads;
     const uint64_t first = (uint64_t)blockIdx.x * kThreads + tid;
     for (int jj = 1; jj < N; ++jj) {
@@ -980,17 +978,32 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
   __syncthreads();
   if (tid == 0) {
     if (gridDim.x > 1) __threadfence();
-    const uint32_t old = gridDim.x > 1 ? atomicAdd(&hdr->rs_arrive, 1u) : 0u;
-    if (old == gridDim.x - 1 && s_status == ST_OK) {
-      fence_acq_rel_sys();  // all my CTAs' posted writes before the flags
-      for (int jj = 1; jj < N; ++jj) {
-        const int j = (me + jj) % N;
-        ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
-        st_relaxed_sys(&ph->sm_meta[me], fp);
-        st_relaxed_sys(&ph->sm_in[me], mk_flag(tag, 0));
-      }
-      hdr->tph[1] = globaltimer_ns();
+    const uint32_t old = gridDim.x > 1 ? atomicAdd(&hdr->sm_arrive[parity], 1u) : 0u;
+    if (old == gridDim.x - 1) {
+      hdr->sm_arrive[parity] = 0;  // nobody touches this parity's counter until the call after next
+      for (int jj = 1; jj < N; ++jj)
+        st_relaxed_sys(&reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->sm_meta[me], fp);
+      fence_acq_rel_sys();  // all my CTAs' posted writes (and the fingerprints) before the flags
+      for (int jj = 1; jj < N; ++jj)
+        st_relaxed_sys(&reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->sm_in[me], mk_flag(tag, 0));
+      s_t1 = globaltimer_ns();
     }
+    if (blockIdx.x == 0) {
+      // Epoch fence (a PCIe read, off the critical path): a stale op's pushes
+      // carry a tag no current peer call waits for, and it poisons itself.
+      if (ctl->epoch != tag_gen(tag)) {
+        s_status = ST_PROTOCOL;
+        s_blame = me;
+      }
+      ctl->started = tag;
+    }
+  }
+  // the previous kernel on this stream has completed (no-op without PDL)
+  pdl_wait();
+  __syncthreads();
+  if (tid == 0 && blockIdx.x == 0) {
+    hdr->tph[0] = s_t0;
+    hdr->tph[1] = s_t1 ? s_t1 : globaltimer_ns();
   }
   // 2. wait for every peer's push (each CTA's thread 0 polls local flags)
   if (tid == 0 && s_status == ST_OK) {
@@ -1038,6 +1051,10 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
     if (gridDim.x > 1) __threadfence();
     const uint32_t old = gridDim.x > 1 ? atomicAdd(&hdr->done_arrive, 1u) : 0u;
     s_blame = (old == gridDim.x - 1) ? 1 : 0;  // reuse as "am last"
+    // PDL: a CTA is done with the data buffers here, except the last one of a
+    // staged (in-place) call, which still copies the sums into out - the next
+    // call's input may alias that out, so it triggers after the copy
+    if (!s_blame || sdirect) pdl_trigger();
   }
   __syncthreads();
   if (s_blame == 1) {
@@ -1059,6 +1076,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
       }
     }
     __syncthreads();
+    if (tid == 0 && !sdirect) pdl_trigger();
     if (tid == 0) {
       // as in allreduce_kernel: no sys fence on the success path
       const int64_t blame = hdr->err_peer;
@@ -1871,11 +1889,23 @@ cudaError_t launch_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bool coo
 }
 
 template <int N, class In>
-cudaError_t launch_small_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop) {
+cudaError_t launch_small_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop, bool pdl) {
   auto fn = small_allreduce_kernel<N, In>;
   if (coop) {
     void* args[] = {const_cast<LaunchParams*>(&p)};
     return cudaLaunchCooperativeKernel((const void*)fn, grid, dim3(kThreads), args, 0, st);
+  }
+  if (pdl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, p);
   }
   fn<<<grid, kThreads, 0, st>>>(p);
   return cudaGetLastError();
@@ -1908,15 +1938,15 @@ cudaError_t launch_intra(int n, const LaunchParams& p, dim3 grid, cudaStream_t s
 }
 
 template <class In>
-cudaError_t launch_small(int n, const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop) {
+cudaError_t launch_small(int n, const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop, bool pdl = false) {
   switch (n) {
-    case 2: return launch_small_n<2, In>(p, grid, st, coop);
-    case 3: return launch_small_n<3, In>(p, grid, st, coop);
-    case 4: return launch_small_n<4, In>(p, grid, st, coop);
-    case 5: return launch_small_n<5, In>(p, grid, st, coop);
-    case 6: return launch_small_n<6, In>(p, grid, st, coop);
-    case 7: return launch_small_n<7, In>(p, grid, st, coop);
-    case 8: return launch_small_n<8, In>(p, grid, st, coop);
+    case 2: return launch_small_n<2, In>(p, grid, st, coop, pdl);
+    case 3: return launch_small_n<3, In>(p, grid, st, coop, pdl);
+    case 4: return launch_small_n<4, In>(p, grid, st, coop, pdl);
+    case 5: return launch_small_n<5, In>(p, grid, st, coop, pdl);
+    case 6: return launch_small_n<6, In>(p, grid, st, coop, pdl);
+    case 7: return launch_small_n<7, In>(p, grid, st, coop, pdl);
+    case 8: return launch_small_n<8, In>(p, grid, st, coop, pdl);
   }
   return cudaErrorInvalidValue;
 }
@@ -2323,8 +2353,8 @@ static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, ui
     G = g_ctas > 0 ? g_ctas : small_ctas(in_bytes);
   }
   const dim3 grid(G, 1);
-  cudaError_t e = small ? (in_dtype == FTAR_DT_BF16 ? launch_small<BF16In>(c->n, p, grid, st, false)
-                                                    : launch_small<F32In>(c->n, p, grid, st, false))
+  cudaError_t e = small ? (in_dtype == FTAR_DT_BF16 ? launch_small<BF16In>(c->n, p, grid, st, false, pdl_on())
+                                                    : launch_small<F32In>(c->n, p, grid, st, false, pdl_on()))
                         : (in_dtype == FTAR_DT_BF16 ? launch_dispatch<BF16In>(c->n, p, grid, st, false, pdl_on())
                                                     : launch_dispatch<F32In>(c->n, p, grid, st, false, pdl_on()));
   if (e != cudaSuccess) {

@@ -99,6 +99,7 @@ struct alignas(128) ArenaHdr {
   alignas(128) uint64_t ag_in[kMaxMembers];  // push mode: member k finished writing its slice into my out
   alignas(128) uint64_t sm_in[kMaxMembers];  // small one-shot: member k's whole input is in my recv slot
   uint64_t sm_meta[kMaxMembers];             // its call fingerprint (validated like an entry record)
+  alignas(128) uint32_t sm_arrive[2];        // small one-shot: push-arrival counter per call parity
 };
 static_assert(sizeof(ArenaHdr) <= kHdrBytes, "header too large");
 
