@@ -230,6 +230,48 @@ def _worker(rank, world, port, scenario, outdir):
             good = all(np.array_equal(o.cpu().numpy(), orc.oracle_reduce(bk, 8 << 20, 4) * np.float32(0.5))
                        for bk, o in zip(bks, outs))
             (res["ok"] if good else res["errors"]).append("regrouped_queue")
+        elif scenario == "chain":
+            # queued IN-PLACE calls on the same buffers: call k+1 reads what
+            # call k wrote, so programmatic dependent launch must never let
+            # k+1 publish or push its input before k has finished writing it
+            # (small push one-shot and two-shot kernels, alternating)
+            group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, 1, deadline_s=30)
+            cfg = ftar.PipelineConfig(per_chunk_timeout_s=10)
+            # not 1/world: identical inputs must still change every call, or a
+            # read of the previous call's output before it is final would go unseen
+            scale = 1.0 / 3.0
+            for elems in (65_537, 1_048_579, 200_003):  # small path, two-shot, small path
+                arrays = member_inputs(world, elems, seed=700 + elems % 97)
+                x = group.alloc_bucket(elems) if elems * 4 <= (8 << 20) else torch.empty(elems, device=dev)
+                x.copy_(torch.from_numpy(arrays[rank]).to(dev))
+                pend = [ftar.ftar_all_reduce_async(group, x, k, cfg, out=None, scale=scale) for k in range(3)]
+                pend += [ftar.ftar_all_reduce_async(group, x, 3 + k, cfg, scale=scale) for k in range(3)]
+                for p_ in pend:
+                    p_.wait()
+                want = [a.copy() for a in arrays]
+                for _ in range(6):
+                    r = orc.normalize(orc.oracle_reduce(want, 8 << 20, 4), 3)
+                    want = [r] * world
+                (res["ok"] if np.array_equal(x.cpu().numpy(), want[0]) else res["errors"]).append(f"chain{elems}")
+            # alternate sizes inside one queue (small -> two-shot -> small), in place
+            a_small = group.alloc_bucket(70_001)
+            b_big = torch.empty(1_500_007, device=dev)
+            sa = member_inputs(world, 70_001, seed=801)
+            sb = member_inputs(world, 1_500_007, seed=802)
+            a_small.copy_(torch.from_numpy(sa[rank]).to(dev))
+            b_big.copy_(torch.from_numpy(sb[rank]).to(dev))
+            pend = []
+            for k in range(4):
+                pend.append(ftar.ftar_all_reduce_async(group, a_small, k, cfg, scale=scale))
+                pend.append(ftar.ftar_all_reduce_async(group, b_big, k, cfg, scale=scale))
+            for p_ in pend:
+                p_.wait()
+            for arrays, t, tag in ((sa, a_small, "mix_small"), (sb, b_big, "mix_big")):
+                want = [a.copy() for a in arrays]
+                for _ in range(4):
+                    r = orc.normalize(orc.oracle_reduce(want, 8 << 20, 4), 3)
+                    want = [r] * world
+                (res["ok"] if np.array_equal(t.cpu().numpy(), want[0]) else res["errors"]).append(tag)
         elif scenario == "intra":
             # §8f rank 2: the replica's ranks reduce-scatter / all-gather over
             # NVLink (one process per GPU), bit-exact vs the reference goldens
@@ -369,6 +411,13 @@ def test_failed_async_queue_is_drained():
         assert "regrouped_queue" in r["ok"]
     for r in res[:-1]:
         assert "all_failed:4" in r["ok"] and "queues_empty" in r["ok"]
+
+
+def test_queued_in_place_chains_are_exact():
+    res = run("chain", world_size())
+    for r in res:
+        assert not r["errors"], r["errors"]
+        assert {"mix_small", "mix_big"} <= set(r["ok"]) and sum(x.startswith("chain") for x in r["ok"]) == 3
 
 
 def test_intra_replica_collectives_over_nvlink():
