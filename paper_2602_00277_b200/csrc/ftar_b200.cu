@@ -1171,6 +1171,7 @@ __global__ void __launch_bounds__(kThreads, 1) intra_kernel(const __grid_constan
       } else {
         ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
         EntryIn* e = &hdr->ent_in[j];
+        // own_err = null: under PDL hdr->err still belongs to the previous call
         st = wait_flag(&e->flag, tag, &ph->poison, ctl, nullptr, s_t0, p.hard_timeout_ns, nullptr);
         if (st == ST_OK) {
           const uint64_t efp = ld_relaxed_sys(&e->fp), in_off = ld_relaxed_sys(&e->in_off);
@@ -1189,6 +1190,9 @@ __global__ void __launch_bounds__(kThreads, 1) intra_kernel(const __grid_constan
       s_blame = __ffs(bad) - 1;
     }
   }
+  // PDL: the entry above touched only the entry slots and my control slot;
+  // from here on the previous kernel on this stream has completed
+  pdl_wait();
   __syncthreads();
   // ---- 2. fan out to my CTAs
   if (blockIdx.x == 0) {
@@ -1277,6 +1281,7 @@ __global__ void __launch_bounds__(kThreads, 1) intra_kernel(const __grid_constan
   __syncthreads();
   // ---- 5. completion (as allreduce_kernel: no sys fence on success)
   if (tid == 0) {
+    pdl_trigger();  // done with every buffer (CTA 0: after the closing barrier)
     const uint32_t st = s_status;
     if (st != ST_OK && st != ST_FOLLOW) {
       atomicMax(&hdr->err, severity_code(st));
@@ -1912,27 +1917,39 @@ cudaError_t launch_small_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bo
 }
 
 template <int N, class In>
-cudaError_t launch_intra_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop) {
+cudaError_t launch_intra_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop, bool pdl) {
   auto fn = intra_kernel<N, In>;
   if (coop) {
     void* args[] = {const_cast<LaunchParams*>(&p)};
     return cudaLaunchCooperativeKernel((const void*)fn, grid, dim3(kThreads), args, 0, st);
+  }
+  if (pdl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, p);
   }
   fn<<<grid, kThreads, 0, st>>>(p);
   return cudaGetLastError();
 }
 
 template <class In>
-cudaError_t launch_intra(int n, const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop) {
+cudaError_t launch_intra(int n, const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop, bool pdl = false) {
   switch (n) {
-    case 1: return launch_intra_n<1, In>(p, grid, st, coop);
-    case 2: return launch_intra_n<2, In>(p, grid, st, coop);
-    case 3: return launch_intra_n<3, In>(p, grid, st, coop);
-    case 4: return launch_intra_n<4, In>(p, grid, st, coop);
-    case 5: return launch_intra_n<5, In>(p, grid, st, coop);
-    case 6: return launch_intra_n<6, In>(p, grid, st, coop);
-    case 7: return launch_intra_n<7, In>(p, grid, st, coop);
-    case 8: return launch_intra_n<8, In>(p, grid, st, coop);
+    case 1: return launch_intra_n<1, In>(p, grid, st, coop, pdl);
+    case 2: return launch_intra_n<2, In>(p, grid, st, coop, pdl);
+    case 3: return launch_intra_n<3, In>(p, grid, st, coop, pdl);
+    case 4: return launch_intra_n<4, In>(p, grid, st, coop, pdl);
+    case 5: return launch_intra_n<5, In>(p, grid, st, coop, pdl);
+    case 6: return launch_intra_n<6, In>(p, grid, st, coop, pdl);
+    case 7: return launch_intra_n<7, In>(p, grid, st, coop, pdl);
+    case 8: return launch_intra_n<8, In>(p, grid, st, coop, pdl);
   }
   return cudaErrorInvalidValue;
 }
@@ -2643,8 +2660,10 @@ int ftar_intra_launch(ftar_ctx* c, int op, const void* in, int in_dtype, float* 
   p.emulated = 0;
   p.fault_member = -1;
   const dim3 grid(intra_ctas(op, in_dtype, total, lens, c->self, c->n), 1);
-  cudaError_t e = in_dtype == FTAR_DT_BF16 ? launch_intra<BF16In>(c->n, p, grid, st, false)
-                                            : launch_intra<F32In>(c->n, p, grid, st, false);
+  // staged inputs are written by a copy on this stream, which keeps the full
+  // dependency; PDL only relaxes kernel-after-kernel
+  cudaError_t e = in_dtype == FTAR_DT_BF16 ? launch_intra<BF16In>(c->n, p, grid, st, false, pdl_on())
+                                            : launch_intra<F32In>(c->n, p, grid, st, false, pdl_on());
   if (e != cudaSuccess) {
     c->pop_last();
     return cuda_fail(e, "intra-replica collective launch");

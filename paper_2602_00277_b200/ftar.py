@@ -452,11 +452,12 @@ class PendingAllReduce:
     taxonomy exception of its status (the links are then closed, as in
     ftar.py:323-325)."""
 
-    __slots__ = ("group", "result", "cfg", "status", "detail", "done")
+    __slots__ = ("group", "result", "cfg", "status", "detail", "done", "_keep")
 
     def __init__(self, group, result, cfg):
         self.group, self.result, self.cfg = group, result, cfg
         self.status, self.detail, self.done = 0, -1, False
+        self._keep = None  # buffers that must outlive the queued call
 
     def wait(self):
         q = self.group._pending

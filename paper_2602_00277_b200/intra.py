@@ -42,7 +42,7 @@ import torch
 from . import _lib
 from .errors import INTERNAL_INVARIANT, PEER_DOWN, Fatal, Recoverable, from_status
 from .fabric import LocalFabric
-from .ftar import MIB, PeerAddress, RingGroup, _stream_ptr, segment_bounds
+from .ftar import MIB, PeerAddress, PendingAllReduce, PipelineConfig, RingGroup, _stream_ptr, segment_bounds
 
 __all__ = ["IntraGroup", "IntraRank", "segment_bounds"]
 
@@ -208,6 +208,7 @@ class IntraRank:
         self.rank, self.n = rank, n_ranks
         self.group = RingGroup(rank, 0, fabric, incarnation=incarnation, device=device,
                                max_bucket_bytes=max_bytes, pool_bytes=pool_bytes)
+        self._cfg = PipelineConfig(per_chunk_timeout_s=30.0)
         self.device = self.group.device
         self.reconfig(1, deadline_s)
 
@@ -218,7 +219,7 @@ class IntraRank:
         """A buffer in the registered pool: read by the peers in place."""
         return self.group.alloc_bucket(numel, dtype)
 
-    def _run(self, op: int, x, bounds, total: int, out):
+    def _run(self, op: int, x, bounds, total: int, out, wait: bool = True):
         if not self.group.links_ready():
             raise Recoverable(PEER_DOWN, "intra-replica links not established")
         t, was_np = _as_device(x, self.device, (torch.float32, torch.bfloat16) if op == _lib.OP_RS
@@ -234,15 +235,20 @@ class IntraRank:
             out = torch.empty(want, device=self.device)
         elif not (out.is_cuda and out.dtype == torch.float32 and out.is_contiguous() and out.numel() == want):
             raise Fatal(INTERNAL_INVARIANT, f"out must be a contiguous fp32 CUDA tensor of {want} elements")
+        # shares the group's FIFO of queued collectives (up to 4 in flight)
+        q = self.group.__dict__.setdefault("_pending", __import__("collections").deque())
+        while len(q) >= 4:
+            q[0].wait()
         rc = _lib.lib.ftar_intra_launch(self.group.ctx, op, t.data_ptr(), code, out.data_ptr(), total, offs, lens,
                                         _stream_ptr(self.device))
         _lib.check(rc, "ftar_intra_launch")
-        det = C.c_int(-1)
-        st = _lib.lib.ftar_wait(self.group.ctx, 30.0, C.byref(det))
-        if st:
-            self.group.close_links()
-        _raise(st, det.value, list(range(self.n)))
-        return out.cpu().numpy() if was_np else out
+        pend = PendingAllReduce(self.group, out, self._cfg)
+        pend._keep = t  # the input must outlive the call (staged copy or peers' reads)
+        q.append(pend)
+        if not wait:
+            return pend
+        res = pend.wait()
+        return res.cpu().numpy() if was_np else res
 
     def reduce_scatter(self, rank: int, vec, bounds, *, out=None):
         if rank != self.rank:
@@ -254,6 +260,15 @@ class IntraRank:
         if rank != self.rank:
             raise Fatal(INTERNAL_INVARIANT, "IntraRank serves its own rank only")
         return self._run(_lib.OP_AG, shard, bounds, int(total), out)
+
+    def reduce_scatter_async(self, vec: torch.Tensor, bounds, *, out=None) -> PendingAllReduce:
+        """Queue a reduce-scatter (CUDA tensors); .wait() returns the shard.
+        Queued calls run back to back on the stream (programmatic dependent
+        launch overlaps each one's entry with the previous one's tail)."""
+        return self._run(_lib.OP_RS, vec, bounds, int(vec.numel()), out, wait=False)
+
+    def all_gather_async(self, shard: torch.Tensor, bounds, total: int, *, out=None) -> PendingAllReduce:
+        return self._run(_lib.OP_AG, shard, bounds, int(total), out, wait=False)
 
     def close(self) -> None:
         self.group.close()

@@ -302,6 +302,15 @@ def _worker(rank, world, port, scenario, outdir):
             good = np.array_equal(shard.cpu().numpy(), want[rank]) and \
                 np.array_equal(full.cpu().numpy(), orc.intra_all_gather(want, bounds, total))
             (res["ok"] if good else res["errors"]).append("intra_big")
+            # queued: RS -> AG -> RS back to back (the AG reads the RS output)
+            sh = torch.empty(bounds[rank][1], device=dev)
+            p1 = ir.reduce_scatter_async(v, bounds, out=sh)
+            p2 = ir.all_gather_async(sh, bounds, total)
+            p3 = ir.reduce_scatter_async(v, bounds)
+            s1, f2, s3 = p1.wait(), p2.wait(), p3.wait()
+            good = np.array_equal(s1.cpu().numpy(), want[rank]) and np.array_equal(s3.cpu().numpy(), want[rank]) \
+                and np.array_equal(f2.cpu().numpy(), orc.intra_all_gather(want, bounds, total))
+            (res["ok"] if good else res["errors"]).append("intra_queued")
             ir.close()
         elif scenario == "catchup":
             from paper_2602_00277_b200 import checkpoint as ck
@@ -424,7 +433,7 @@ def test_intra_replica_collectives_over_nvlink():
     res = run("intra", world_size())
     for r in res:
         assert not r["errors"], r["errors"]
-        assert "intra_big" in r["ok"] and len(r["ok"]) >= 2
+        assert "intra_big" in r["ok"] and "intra_queued" in r["ok"] and len(r["ok"]) >= 3
 
 
 def test_catchup_pull_over_nvlink():

@@ -6,7 +6,8 @@ one JSON line per (op, dtype, size).
 
 busbw (NCCL convention): RS = (total * in_bytes / t) * (n-1)/n;
 AG = (total * 4 / t) * (n-1)/n.  Inputs live in the registered pool
-(zero-copy); 20 warm-up + 50 timed calls, CUDA events, max over ranks.
+(zero-copy); queued 3 deep; 20 warm-up + 50 timed calls, CUDA events, max
+over ranks.
 """
 
 import argparse
@@ -22,7 +23,7 @@ from paper_2602_00277_b200.fabric import StoreFabric  # noqa: E402
 from paper_2602_00277_b200.intra import IntraRank, segment_bounds  # noqa: E402
 
 
-def timed(fn, iters, dev):
+def timed(fn, iters, dev, drain=None):
     st = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist.barrier()
@@ -30,6 +31,8 @@ def timed(fn, iters, dev):
     e0.record(st)
     for _ in range(iters):
         fn()
+    if drain is not None:
+        drain()
     e1.record(st)
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1) / iters], device=dev)
@@ -67,12 +70,30 @@ def main():
             ln = bounds[rank][1]
             shard = shard_buf[:ln]
             out_full = full[:total] if total <= emax else torch.empty(total, device=dev)
+            from collections import deque
+            pend = deque()
+
+            def queued(fn):
+                def step():
+                    pend.append(fn())
+                    while len(pend) >= 3:
+                        pend.popleft().wait()
+                return step
+
+            def drain():
+                while pend:
+                    pend.popleft().wait()
+
+            rs_step = queued(lambda: ir.reduce_scatter_async(v, bounds, out=shard))
+            ag_step = queued(lambda: ir.all_gather_async(shard, bounds, total, out=out_full))
             for _ in range(20):
-                ir.reduce_scatter(rank, v, bounds, out=shard)
-            t_rs = timed(lambda: ir.reduce_scatter(rank, v, bounds, out=shard), args.iters, dev)
+                rs_step()
+            drain()
+            t_rs = timed(lambda: rs_step(), args.iters, dev, drain)
             for _ in range(5):
-                ir.all_gather(rank, shard, bounds, total, out=out_full)
-            t_ag = timed(lambda: ir.all_gather(rank, shard, bounds, total, out=out_full), args.iters, dev)
+                ag_step()
+            drain()
+            t_ag = timed(lambda: ag_step(), args.iters, dev, drain)
             # NCCL on the same tensors (equal shards: pad to a multiple of n)
             tn = total - total % n
             nv = v[:tn].contiguous()
