@@ -230,6 +230,53 @@ def _worker(rank, world, port, scenario, outdir):
             good = all(np.array_equal(o.cpu().numpy(), orc.oracle_reduce(bk, 8 << 20, 4) * np.float32(0.5))
                        for bk, o in zip(bks, outs))
             (res["ok"] if good else res["errors"]).append("regrouped_queue")
+        elif scenario == "fuzz":
+            # randomized mixes of every mode, the same seeded sequence on every
+            # rank: sizes across the small-bucket and two-shot paths, fp32 and
+            # bf16, registered and staged inputs, in place / out of place, with
+            # and without scale, contributor subsets, 1-4 calls queued
+            rng = np.random.default_rng(4321)
+            gen = 0
+            cfg = ftar.PipelineConfig(per_chunk_timeout_s=10)
+            pool_left = [group.alloc_bucket(900_000), group.alloc_bucket(900_000, torch.bfloat16)]
+            for it in range(25):
+                gen += 1
+                contrib = [r for r in range(world) if rng.random() < 0.8] or [0]
+                group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, gen, deadline_s=30,
+                               contributors=contrib)
+                depth = int(rng.integers(1, 5))
+                jobs = []
+                for k in range(depth):
+                    elems = int(np.exp(rng.uniform(0, np.log(2_500_000))))
+                    bf16 = bool(rng.random() < 0.4)
+                    reg = bool(rng.random() < 0.5) and elems <= 900_000
+                    inplace = (not bf16) and bool(rng.random() < 0.4)
+                    scale = float(rng.choice([0.5, 1.0 / 3.0])) if rng.random() < 0.6 else None
+                    seed = int(rng.integers(1 << 30))
+                    arrays = member_inputs(world, elems, seed=seed, dtype="bf16" if bf16 else "f32")
+                    if reg:
+                        x = pool_left[1 if bf16 else 0][:elems]
+                        x.copy_(torch.from_numpy(arrays[rank]).to(dev).to(torch.bfloat16 if bf16 else torch.float32))
+                    else:
+                        x = torch.from_numpy(arrays[rank]).to(dev)
+                        if bf16:
+                            x = x.to(torch.bfloat16)
+                    out = None if inplace else torch.empty(elems, device=dev)
+                    pend = ftar.ftar_all_reduce_async(group, x, it, cfg, out=out, scale=scale)
+                    result = x if inplace else out
+                    if reg:
+                        pend.wait()  # the registered scratch is reused by the next job,
+                        if inplace:  # which would overwrite an in-place result living in it
+                            result = x.clone()
+                    jobs.append((pend, arrays, scale, result, (elems, bf16, reg, inplace, scale)))
+                for pend, arrays, sc, res_t, desc in jobs:
+                    pend.wait()
+                    want = orc.oracle_reduce(arrays, cfg.chunk_bytes, cfg.max_in_flight,
+                                             contrib=[r in contrib for r in range(world)])
+                    if sc is not None:
+                        want = want * np.float32(ftar._f32(sc))
+                    good = np.array_equal(res_t.float().cpu().numpy(), want)
+                    (res["ok"] if good else res["errors"]).append(f"fuzz{it}:{desc}")
         elif scenario == "chain":
             # queued IN-PLACE calls on the same buffers: call k+1 reads what
             # call k wrote, so programmatic dependent launch must never let
@@ -420,6 +467,13 @@ def test_failed_async_queue_is_drained():
         assert "regrouped_queue" in r["ok"]
     for r in res[:-1]:
         assert "all_failed:4" in r["ok"] and "queues_empty" in r["ok"]
+
+
+def test_randomized_mode_mix_is_exact():
+    res = run("fuzz", world_size())
+    for r in res:
+        assert not r["errors"], r["errors"]
+        assert len(r["ok"]) >= 25
 
 
 def test_queued_in_place_chains_are_exact():
