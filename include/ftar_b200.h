@@ -263,6 +263,10 @@ int ftar_debug_cta_times(ftar_ctx* ctx, uint64_t* rs_end, uint64_t* ag_end, int 
 int ftar_peer_enable(int device, int peer);
 /* Fence-cost probe: c = a + b (b remote), load flavour `kind`, per-CTA
  * %globaltimer stamps (loop end, bar.sync, gpu fence, sys fence). */
+/* Diagnostic: this GPU's %globaltimer offset to the host's CLOCK_MONOTONIC
+ * (min over `reps` pairings), for cross-GPU phase timelines. */
+int ftar_probe_clock(int device, int reps, int64_t* offset_ns);
+
 int ftar_probe_fence(float* c, const float* a, const float* b, uint64_t n, int kind, int ctas,
                      uint64_t* stamps, int device, void* stream);
 /* Access-pattern probe: mode 0 c=a+b, 1 c=b, 2 loads only, 3 all-local;

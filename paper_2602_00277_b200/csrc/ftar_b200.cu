@@ -26,9 +26,11 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <string>
 #include <thread>
 
@@ -109,13 +111,18 @@ __device__ uint32_t wait_flag(const uint64_t* flag, uint64_t tag, const uint64_t
                               const HostCtl* ctl, const uint32_t* own_err, uint64_t t0,
                               uint64_t limit_ns, uint32_t* bits) {
   // Relaxed polls (no fence per poll: acquire loads from many spinning CTAs
-  // slow down every other CTA's fences), one acquire fence on success,
+  // slow down every other CTA's fences), one acquire load on success,
   // exponential-ish backoff so idle pollers leave NVLink and L2 alone.
   for (uint32_t it = 0;; ++it) {
     const uint64_t f = ld_relaxed_sys(flag);
     const uint64_t ft = flag_tag(f);
     if (ft == tag) {
-      fence_acq_rel_sys();
+      // acquire-only: one ld.acquire.sys re-read orders this thread's later
+      // reads after the writer's release.  A fence.acq_rel.sys here would also
+      // wait for this thread's own outstanding writes (e.g. a PCIe write to
+      // the control block) - measured at ~2 us per flag.  A later tag read
+      // here still orders correctly: the writer released it after this one.
+      (void)ld_acquire_sys(flag);
       if (bits) *bits = (uint32_t)(f & 0xffu);
       return ST_OK;
     }
@@ -902,9 +909,11 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
       const uint32_t err = ld_relaxed_gpu32(&hdr->err);
       const uint64_t tiles = hdr->tiles_done;
       const int64_t blame = hdr->err_peer;
-      ctl->progress = tiles + 1;
+      (void)tiles;
+      // the phase stamps stay in device memory (ftar_phase_times reads them);
+      // `done` is the tail's only PCIe write: griddepcontrol.wait in the next
+      // call waits for this grid's writes to flush, host-memory ones included
       hdr->tph[4] = globaltimer_ns();
-      for (int i = 0; i < 5; ++i) ctl->tphase[i] = hdr->tph[i];
       hdr->rs_arrive = 0;
       hdr->done_arrive = 0;
       hdr->nonfinite = 0;
@@ -1080,10 +1089,8 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
     if (tid == 0) {
       // as in allreduce_kernel: no sys fence on the success path
       const int64_t blame = hdr->err_peer;
-      ctl->progress = 1;
       hdr->tph[3] = hdr->tph[2];
-      hdr->tph[4] = globaltimer_ns();
-      for (int i = 0; i < 5; ++i) ctl->tphase[i] = hdr->tph[i];
+      hdr->tph[4] = globaltimer_ns();  // device memory only: `done` is the one PCIe write
       hdr->rs_arrive = 0;
       hdr->done_arrive = 0;
       hdr->nonfinite = 0;
@@ -1294,9 +1301,7 @@ __global__ void __launch_bounds__(kThreads, 1) intra_kernel(const __grid_constan
       fence_acq_rel_gpu();
       const uint32_t err = ld_relaxed_gpu32(&hdr->err);
       const int64_t blame = hdr->err_peer;
-      ctl->progress = 1;
-      hdr->tph[4] = globaltimer_ns();
-      for (int i = 0; i < 5; ++i) ctl->tphase[i] = hdr->tph[i];
+      hdr->tph[4] = globaltimer_ns();  // device memory only: `done` is the one PCIe write
       hdr->rs_arrive = 0;
       hdr->done_arrive = 0;
       hdr->nonfinite = 0;
@@ -2838,8 +2843,14 @@ int ftar_wait_local(ftar_ctx** ctxs, int n, double progress_timeout_s, int* stat
 }
 
 int ftar_phase_times(ftar_ctx* c, uint64_t* out, int n) {
+  // the last completed call's %globaltimer stamps, kept in the arena header
+  // (the kernels spend no PCIe writes on them); synchronises the device
   if (!c || !out) return fail(FTAR_ST_INVARIANT, "bad args");
-  for (int i = 0; i < n && i < 6; ++i) out[i] = c->ctl_h->tphase[i];
+  DeviceGuard g(c->device);
+  uint64_t t[6];
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(t, c->arena + offsetof(ArenaHdr, tph), sizeof(t), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n && i < 6; ++i) out[i] = t[i];
   return FTAR_OK;
 }
 
@@ -2871,6 +2882,38 @@ int ftar_debug_cta_times(ftar_ctx* c, uint64_t* rs_end, uint64_t* ag_end, int n)
   if (n >= 260) {  // caller wants the fence stamps too (rs_end[256..259])
     for (int i = 0; i < 4; ++i) rs_end[256 + i] = h.dbg_fence[i];
   }
+  return FTAR_OK;
+}
+
+// Clock pairing for cross-GPU timelines (diagnostic): a one-thread kernel
+// writes %globaltimer into pinned host memory while the host spins on it and
+// stamps CLOCK_MONOTONIC the moment it appears.  host - gpu, minimised over
+// `reps`, is this GPU's timer offset to the host clock that every process on
+// the box shares (error ~ one PCIe write latency).
+__global__ void probe_clock_kernel(volatile uint64_t* slot) { *slot = globaltimer_ns(); }
+
+int ftar_probe_clock(int device, int reps, int64_t* offset_ns) {
+  if (!offset_ns || reps < 1) return fail(FTAR_ST_INVARIANT, "bad args");
+  DeviceGuard g(device);
+  uint64_t* h = nullptr;
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&h), sizeof(uint64_t), cudaHostAllocMapped));
+  uint64_t* d = nullptr;
+  cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), h, 0);
+  int64_t best = INT64_MAX;
+  for (int r = 0; r < reps; ++r) {
+    *reinterpret_cast<volatile uint64_t*>(h) = 0;
+    probe_clock_kernel<<<1, 1>>>(d);
+    uint64_t v;
+    while ((v = *reinterpret_cast<volatile uint64_t*>(h)) == 0) {
+    }
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    const int64_t host = (int64_t)ts.tv_sec * 1000000000ll + ts.tv_nsec;
+    best = std::min(best, host - (int64_t)v);
+    cudaDeviceSynchronize();
+  }
+  cudaFreeHost(h);
+  *offset_ns = best;
   return FTAR_OK;
 }
 

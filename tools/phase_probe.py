@@ -50,6 +50,8 @@ def main():
     buf.normal_()
     cfg = ftar.PipelineConfig()
     st = torch.cuda.current_stream(dev)
+    off = C.c_int64()
+    _lib.lib.ftar_probe_clock(dev.index, 200, C.byref(off))  # this GPU's timer -> host CLOCK_MONOTONIC
     for nb in sizes:
         e = nb // esz
         b, o = buf[:e], out[:e]
@@ -74,6 +76,7 @@ def main():
         _lib.lib.ftar_phase_times(g.ctx, t, 6)  # the last queued call
         q_ph = [round((t[i + 1] - t[i]) / 1e3, 2) for i in range(4)]
         q_t0 = int(t[0])
+        q_host = [int(t[i]) + off.value for i in range(5)]  # stamps on the shared host clock
         # device phases of blocking calls
         acc = [0.0] * 4
         k = 20
@@ -100,7 +103,8 @@ def main():
         _lib.lib.ftar_geometry(e, n, C.byref(slice_e), C.byref(ctas), C.byref(thr))
         rows = [None] * n
         dist.all_gather_object(rows, {"rank": rank, "phases_us": ph, "per_call_us": round(per_call, 2),
-                                      "queued_phases_us": q_ph, "queued_t0": q_t0, "detail": det})
+                                      "queued_phases_us": q_ph, "queued_t0": q_t0, "detail": det,
+                                      "queued_host_ns": q_host})
         if rank == 0:
             busbw = nb / (per_call * 1e-6) * 2 * (n - 1) / n / 1e9
             print(json.dumps({"n": n, "dtype": args.dtype, "bytes": nb, "per_call_us": round(per_call, 2),
@@ -108,9 +112,11 @@ def main():
                               "phases_entry_rs_wait_tail_us": [r["phases_us"] for r in rows],
                               "queued_phases_us": [r["queued_phases_us"] for r in rows],
                               "detail_rank0": rows[0]["detail"],
-                              # kernel start of the last queued call vs the earliest member (%globaltimer)
-                              "queued_t0_skew_us": [round((r["queued_t0"] - min(x["queued_t0"] for x in rows)) / 1e3, 2)
-                                                    for r in rows]}), flush=True)
+                              # the last queued call on one clock (host CLOCK_MONOTONIC via
+                              # ftar_probe_clock, ~1-2 us): [start, published, all peers in,
+                              # -, end] per rank, us after the earliest start
+                              "timeline_us": [[round((v - min(x["queued_host_ns"][0] for x in rows)) / 1e3, 2)
+                                               for v in r["queued_host_ns"]] for r in rows]}), flush=True)
     g.close()
     dist.barrier()
     dist.destroy_process_group()
