@@ -6,9 +6,11 @@
 
 Workload (BASELINE.json metric "FTAR bus GB/s vs bucket size at 2/4/8 B200"):
   * N >= 2: one replica per GPU (north_star), a 256 MiB fp32 gradient bucket
-    per replica in the group's registered pool, reduced in place with the
-    fused normalisation x f32(1/N) (replica.py:622-626) — the bucket class
-    the >= 64 MB target names; the two-shot NVLink pull kernel.
+    per replica in the group's registered pool, reduced out of place (fp32
+    out=, --inplace for the reference's in-place shape) with the fused
+    normalisation x f32(1/N) (replica.py:622-626) — the bucket class the
+    >= 64 MB target names; the two-shot NVLink kernel (reduce-scatter by peer
+    pulls, all-gather by pushes into the peers' registered outputs).
   * N = 1: the metric's multi-replica configs do not fit one GPU, so the
     replicas are emulated: 4 replicas (config 1's replica count) of the same
     bucket on cuda:0, reduced by the in-process one-shot kernel.  That number
@@ -387,10 +389,10 @@ def run_multi(args, rank, world, local_rank):
     nv_bytes = (n - 1) / n * elems * (in_bytes + 4)
     roof = {"bound": "nvlink", "achieved": round(nv_bytes / per_launch / 1e9, 1), "peak": NVLINK_PEER_GBS,
             "unit": "GB/s", "frac": round(nv_bytes / per_launch / 1e9 / NVLINK_PEER_GBS, 4), "traffic": None,
-            "kernel": "allreduce_kernel (two-shot NVLink pull)",
+            "kernel": "allreduce_kernel (two-shot: RS by NVLink pulls, AG by pushes)",
             "algorithmic_bytes_per_launch": int(nv_bytes),
             "definition": "NVLink ingress per GPU (n-1)/n*E*(in_bytes+4): RS pulls every peer's slice of my "
-                          "segment, AG pulls every peer's fp32 result; peak = 770 GB/s measured peer copy "
+                          "segment, AG receives every peer's fp32 result; peak = 770 GB/s measured peer copy "
                           "per direction (B200_PROFILING.md fallback; MEASURED_PEAKS.json has no NVLink entry)",
             "frac_of_nominal_900": round(nv_bytes / per_launch / 1e9 / NVLINK_NOMINAL_GBS, 4),
             "avg_launch_ms": round(per_launch * 1e3, 4)}

@@ -87,7 +87,8 @@ struct alignas(128) ArenaHdr {
   uint64_t dbg_ag_end[256];               // per-CTA %globaltimer at end of all-gather
   uint64_t dbg_t1;                        // entry barrier passed (block 0)
   uint64_t dbg_fence[4];                  // last CTA: before/after the sys fence (RS, end)
-  uint64_t tph[6];                        // phase stamps (device copy; host gets them at completion)
+  uint64_t tph[6];                        // phase stamps: [0] start [1] entry passed [2] RS published
+                                          // [3] AG barrier passed [4] end (ftar_phase_times)
   alignas(128) uint64_t go;               // CTA 0 -> local CTAs: (tag << 8) | barrier passed
   uint64_t peer_in[kMaxMembers];          // entry barrier result: member inputs (my VA)
   uint64_t peer_res[kMaxMembers];         // and member result slices (my VA)
@@ -114,9 +115,8 @@ struct alignas(64) HostCtl {
   volatile uint64_t done;          // device -> host: mk_flag(tag, status)
   volatile int64_t detail;         // device -> host: ring index blamed (-1 none)
   volatile int64_t available;      // device -> host: snapshot step available
-  volatile uint64_t tphase[6];     // device -> host: %globaltimer at phase ends
-                                   // [0] start [1] entry passed [2] RS published
-                                   // [3] AG barrier passed [4] end
+  // (per-call phase stamps live in ArenaHdr::tph: kernel tails keep `done`
+  // as their only PCIe write; ftar_phase_times copies the stamps out)
 };
 
 // Snapshot arena header (retention-1 seqlock, checkpoint.py:56-80).

@@ -2,7 +2,7 @@
 
     python -m torch.distributed.run --nproc-per-node N tools/sweep.py [--max-mib 1024]
 
-Per cell: FTAR (two-shot NVLink pull, fused x f32(1/n), fp32 out, buckets in
+Per cell: FTAR (push one-shot <= 1 MiB, else two-shot NVLink; fused x f32(1/n), fp32 out, buckets in
 the registered pool, queue depth 3) and NCCL all_reduce on a same-size
 tensor of the same input dtype (NCCL reduces in the input dtype; FTAR always
 accumulates and outputs fp32).  busbw = (E*in_bytes/t) * 2(n-1)/n; nvlink =
