@@ -2135,6 +2135,12 @@ int ftar_ctx_create(int device, uint64_t max_bucket_bytes, uint64_t pool_bytes, 
 int ftar_ctx_destroy(ftar_ctx* c) {
   if (!c) return FTAR_OK;
   DeviceGuard g(c->device);
+  // queued collectives waiting on a peer that is gone would otherwise hold the
+  // synchronize below until the device hard timeout: abort them first
+  for (int i = 0; i < c->q_count; ++i) {
+    const int slot = (c->q_head + i) % kQueue;
+    c->ctl_hs[slot].abort_tag = c->q_tag[slot];
+  }
   cudaDeviceSynchronize();
   for (int s = 0; s < kMaxSlots; ++s)
     if (c->peer[s] && !c->peer_local[s]) cudaIpcCloseMemHandle(c->peer[s]);
