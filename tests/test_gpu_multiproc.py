@@ -550,3 +550,20 @@ def test_async_queue_of_buckets():
                 res = json.load(f)
             assert not res["errors"], res["errors"]
             assert res["ok"].count("bucket") == 7
+
+
+def test_hsdp_step_with_ranks_is_bit_exact():
+    """tools/hsdp_r.py --check: R=2 ranks per replica on every visible GPU,
+    intra RS -> FTAR+SGD -> intra AG for 4 steps, final params bit-exact
+    against the oracle on every rank."""
+    import subprocess
+    world = world_size()
+    if world % 2:
+        pytest.skip("needs an even number of GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.join(ROOT, "tools", "hsdp_r.py"),
+           "--ranks", "2", "--params", "3000017", "--steps", "4", "--check"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["all_ranks_identical_params"] and line["bit_exact_vs_oracle"], line
