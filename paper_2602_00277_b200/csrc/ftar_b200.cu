@@ -315,8 +315,15 @@ struct SinkAll {
 // thread per round whatever the ring size.
 template <int N, class In>
 struct Unroll {
-  static constexpr int U0 = (16 * 16 / (int)sizeof(typename In::Raw)) / N;  // ~256 B of loads per thread
-  static constexpr int U = U0 < 1 ? 1 : (U0 > 16 ? 16 : U0);
+  // ~256 B of loads per thread; ~192 B from 5 members up, where the members'
+  // source and push pointers also live in registers (launch_bounds(512, 1)
+  // caps a thread at 128 registers; 256 B at N=8 spilled)
+  static constexpr int kBudget = (N >= 6 && sizeof(typename In::Raw) == 8) ? 8 : (N >= 5 ? 12 : 16);
+  static constexpr int U0 = (kBudget * 16 / (int)sizeof(typename In::Raw)) / N;
+  // the register allocator's sweet spots (ptxas -v); N <= 2 keeps the deep
+  // unroll: its bf16 form spills a little but measured 1-2% faster at >= 256 MiB
+  static constexpr int kMaxU = N <= 2 ? 16 : (N == 3 ? 6 : 8);
+  static constexpr int U = U0 < 1 ? 1 : (U0 > kMaxU ? kMaxU : U0);
 };
 
 // Reduce elements [a, b) whose fold starts at ring index s.  All threads of the
