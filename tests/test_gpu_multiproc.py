@@ -197,39 +197,41 @@ def _worker(rank, world, port, scenario, outdir):
             # a member skips a step while the others have 4 buckets queued:
             # every handle resolves Recoverable, the host and device queues end
             # empty, and after the regroup a fresh queue of buckets is bit-exact
-            # (a stale handle left behind would collect a later op's status)
+            # (a stale handle left behind would collect a later op's status).
+            # Two-shot buckets first, then small-path ones (push one-shot, PDL).
             import time
 
             from paper_2602_00277_b200 import _lib
             victim = world - 1
-            group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, 1, deadline_s=30)
             cfg = ftar.PipelineConfig(per_chunk_timeout_s=1.0)
-            e = 300_007
-            bks = [member_inputs(world, e, seed=200 + b) for b in range(6)]
-            bufs = [torch.from_numpy(bk[rank]).to(dev) for bk in bks]
-            outs = [torch.empty_like(b) for b in bufs]
-            if rank != victim:
-                pend = [ftar.ftar_all_reduce_async(group, bufs[i], 1, cfg, out=outs[i]) for i in range(4)]
-                failed = 0
+            for rnd, e in enumerate((300_007, 50_021)):
+                g0 = 1 + 2 * rnd
+                group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, g0, deadline_s=30)
+                bks = [member_inputs(world, e, seed=200 + 10 * rnd + b) for b in range(6)]
+                bufs = [torch.from_numpy(bk[rank]).to(dev) for bk in bks]
+                outs = [torch.empty_like(b) for b in bufs]
+                if rank != victim:
+                    pend = [ftar.ftar_all_reduce_async(group, bufs[i], 1, cfg, out=outs[i]) for i in range(4)]
+                    failed = 0
+                    for p in pend:
+                        try:
+                            p.wait()
+                        except errors.Recoverable:
+                            failed += 1
+                    (res["ok"] if failed == 4 else res["errors"]).append(f"all_failed:{failed}")
+                    left = _lib.lib.ftar_inflight(group.ctx)
+                    (res["ok"] if not group._pending and left == 0 else res["errors"]).append("queues_empty")
+                    store.set(f"af_failed{rnd}_{rank}", b"1")
+                else:
+                    store.wait([f"af_failed{rnd}_{r}" for r in range(world - 1)])
+                    time.sleep(0.1)
+                group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, g0 + 1, deadline_s=30)
+                pend = [ftar.ftar_all_reduce_async(group, b, 2, cfg, out=o, scale=0.5) for b, o in zip(bufs, outs)]
                 for p in pend:
-                    try:
-                        p.wait()
-                    except errors.Recoverable:
-                        failed += 1
-                (res["ok"] if failed == 4 else res["errors"]).append(f"all_failed:{failed}")
-                left = _lib.lib.ftar_inflight(group.ctx)
-                (res["ok"] if not group._pending and left == 0 else res["errors"]).append("queues_empty")
-                store.set(f"af_failed{rank}", b"1")
-            else:
-                store.wait([f"af_failed{r}" for r in range(world - 1)])
-                time.sleep(0.1)
-            group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, 2, deadline_s=30)
-            pend = [ftar.ftar_all_reduce_async(group, b, 2, cfg, out=o, scale=0.5) for b, o in zip(bufs, outs)]
-            for p in pend:
-                p.wait()
-            good = all(np.array_equal(o.cpu().numpy(), orc.oracle_reduce(bk, 8 << 20, 4) * np.float32(0.5))
-                       for bk, o in zip(bks, outs))
-            (res["ok"] if good else res["errors"]).append("regrouped_queue")
+                    p.wait()
+                good = all(np.array_equal(o.cpu().numpy(), orc.oracle_reduce(bk, 8 << 20, 4) * np.float32(0.5))
+                           for bk, o in zip(bks, outs))
+                (res["ok"] if good else res["errors"]).append(f"regrouped_queue{rnd}")
         elif scenario == "fuzz":
             # randomized mixes of every mode, the same seeded sequence on every
             # rank: sizes across the small-bucket and two-shot paths, fp32 and
@@ -464,9 +466,9 @@ def test_failed_async_queue_is_drained():
     res = run("async_failure", world)
     for r in res:
         assert not r["errors"], r["errors"]
-        assert "regrouped_queue" in r["ok"]
+        assert "regrouped_queue0" in r["ok"] and "regrouped_queue1" in r["ok"]
     for r in res[:-1]:
-        assert "all_failed:4" in r["ok"] and "queues_empty" in r["ok"]
+        assert r["ok"].count("all_failed:4") == 2 and r["ok"].count("queues_empty") == 2
 
 
 def test_randomized_mode_mix_is_exact():
