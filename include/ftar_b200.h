@@ -232,6 +232,13 @@ int ftar_snap_info(ftar_snap* s, int64_t* step, uint64_t* pbytes, uint64_t* mbyt
 /* Recovering side: map a donor's snapshot arena into `local` (slot cache). */
 int ftar_snap_import(ftar_snap* local, int slot, const void* handle, size_t len,
                      uint64_t capacity_bytes);
+
+/* §8f rank 4 (persistent checkpoint, checkpoint.py:157-198): the snapshot's
+ * device regions (params, then momentum) and its seqlock word.  A host
+ * writer reads `seq` before and after streaming the regions to storage; an
+ * odd or changed value means a capture ran in between (the copy is torn). */
+int ftar_snap_region(ftar_snap* snap, void** params, void** momentum, uint64_t* pbytes,
+                     uint64_t* mbytes, uint64_t* seq, int64_t* step);
 /* Pull donor `slot`'s (-1 = local snapshot, for in-process donors) snapshot of
  * `want_step` into dst_params/dst_momentum with `ctas` CTAs on `stream`.
  * The op reports FTAR_ST_UNAVAILABLE (and *available) when the donor holds a

@@ -59,6 +59,8 @@ SIGNATURES = {
     "ftar_wait_local": (i32, [C.POINTER(c_ctx_p), i32, dbl, C.POINTER(i32), C.POINTER(i32)]),
     "ftar_geometry": (i32, [u64, i32, C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]),
     "ftar_probe_clock": (i32, [i32, i32, C.POINTER(C.c_int64)]),
+    "ftar_snap_region": (i32, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(u64), C.POINTER(u64), C.POINTER(u64),
+                               C.POINTER(C.c_int64)]),
     "ftar_accumulate": (i32, [vp, vp, i32, u64, vp]),
     "ftar_copy_into": (i32, [vp, vp, i32, u64, vp]),
     "ftar_snap_create": (i32, [i32, u64, i32, C.POINTER(c_snap_p)]),

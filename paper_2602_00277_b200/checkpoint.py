@@ -15,21 +15,30 @@
 * ``serve_fetches``  kept for API shape: on NVLink the donor serves by
   publishing its snapshot arena once; no per-request thread is needed.
 
-Persistent checkpoints and the loader ledger (checkpoint.py:157-316) are out
-of scope.
+* Persistent checkpoints (checkpoint.py:155-230): the
+  reference's shard file and manifest format byte for byte (``write_shard``,
+  ``read_shard``, ``write_manifest``, ``find_latest``), written straight from
+  the device snapshot by ``SnapshotStore.persist`` (chunked D2H through pinned
+  buffers, seqlock-validated, atomic rename) without stopping the step.
+
+The loader ledger (checkpoint.py:233-316) is data-loader bookkeeping, not
+this path, and is out of scope.
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import json
 import os
+import re
+import struct
 import threading
 import time
 
 import torch
 
 from . import _lib
-from .errors import INTERNAL_INVARIANT, PEER_DOWN, Fatal, Recoverable, from_status
+from .errors import INTERNAL_INVARIANT, PEER_DOWN, PROTOCOL_VIOLATION, Fatal, Recoverable, from_status
 from .fabric import ArenaInfo, LocalFabric
 
 
@@ -298,3 +307,224 @@ def serve_fetches(router=None, store: SnapshotStore | None = None, stop=None, pr
     """API shape of checkpoint.py:83-95.  NVLink donors need no server: the
     snapshot arena is published when allocated and peers read it directly."""
     return None
+
+
+# ------------------------------------------------------------- persistence
+# checkpoint.py:155-230: one file per (step, rank) = MAGIC + header + params +
+# momentum, written atomically (tmp + fsync + rename), plus a JSON manifest.
+
+MAGIC = b"PAFTCKPT"
+_SHARD_HDR = struct.Struct("<IQIQQ")  # version, step, rank, params_len, momentum_len
+VERSION = 1
+_CHUNK = 64 << 20  # bytes per pinned D2H staging buffer (two of them)
+
+
+def shard_path(ckpt_dir: str, step: int, rank: int) -> str:
+    return os.path.join(ckpt_dir, f"state_{step:08d}_rank{rank}.bin")
+
+
+def manifest_path(ckpt_dir: str, step: int) -> str:
+    return os.path.join(ckpt_dir, f"state_{step:08d}.json")
+
+
+def _atomic_write(path: str, data: bytes) -> None:
+    tmp = path + ".tmp"
+    with open(tmp, "wb") as fh:
+        fh.write(data)
+        fh.flush()
+        os.fsync(fh.fileno())
+    os.rename(tmp, path)
+
+
+def _as_bytes(x) -> bytes:
+    if isinstance(x, torch.Tensor):
+        t = x.detach().contiguous().cpu()
+        return t.view(torch.uint8).numpy().tobytes() if t.numel() else b""
+    return bytes(x)
+
+
+def write_shard(ckpt_dir: str, step: int, rank: int, params, momentum) -> str:
+    """checkpoint.py:174-180.  params / momentum: bytes or tensors (CUDA
+    tensors are copied to the host); the file is byte-identical to the
+    reference's."""
+    os.makedirs(ckpt_dir, exist_ok=True)
+    p, m = _as_bytes(params), _as_bytes(momentum)
+    path = shard_path(ckpt_dir, step, rank)
+    _atomic_write(path, MAGIC + _SHARD_HDR.pack(VERSION, step, rank, len(p), len(m)) + p + m)
+    return path
+
+
+def _read_header(fh, path: str, step: int, rank: int):
+    head = fh.read(len(MAGIC) + _SHARD_HDR.size)
+    if head[:len(MAGIC)] != MAGIC:
+        raise Fatal(PROTOCOL_VIOLATION, f"bad checkpoint magic in {path}")
+    if len(head) < len(MAGIC) + _SHARD_HDR.size:
+        raise Fatal(PROTOCOL_VIOLATION, f"truncated checkpoint shard {path}")
+    version, got_step, got_rank, plen, mlen = _SHARD_HDR.unpack_from(head, len(MAGIC))
+    if version != VERSION:
+        raise Fatal(PROTOCOL_VIOLATION, f"unsupported checkpoint version {version}")
+    if (got_step, got_rank) != (step, rank):
+        raise Fatal(PROTOCOL_VIOLATION, f"checkpoint header ({got_step},{got_rank}) != ({step},{rank})")
+    if len(head) + plen + mlen != os.fstat(fh.fileno()).st_size:
+        raise Fatal(PROTOCOL_VIOLATION, f"truncated checkpoint shard {path}")
+    return plen, mlen
+
+
+def read_shard(ckpt_dir: str, step: int, rank: int) -> tuple[bytes, bytes]:
+    """checkpoint.py:183-198: (params bytes, momentum bytes)."""
+    path = shard_path(ckpt_dir, step, rank)
+    with open(path, "rb") as fh:
+        plen, mlen = _read_header(fh, path, step, rank)
+        return fh.read(plen), fh.read(mlen)
+
+
+def read_shard_into(ckpt_dir: str, step: int, rank: int, params_out: torch.Tensor,
+                    momentum_out: torch.Tensor) -> None:
+    """Restore a shard straight into device tensors (chunked H2D through
+    pinned buffers)."""
+    path = shard_path(ckpt_dir, step, rank)
+    with open(path, "rb") as fh:
+        plen, mlen = _read_header(fh, path, step, rank)
+        for t, n in ((params_out, plen), (momentum_out, mlen)):
+            if t.numel() * t.element_size() != n:
+                raise Fatal(INTERNAL_INVARIANT, f"restore target holds {t.numel() * t.element_size()} bytes, "
+                                                f"the shard {n}")
+            flat = t.view(-1).view(torch.uint8)
+            buf = torch.empty(min(n, _CHUNK) or 1, dtype=torch.uint8).pin_memory()
+            for off in range(0, n, _CHUNK):
+                k = min(_CHUNK, n - off)
+                fh.readinto(memoryview(buf.numpy())[:k])
+                flat[off:off + k].copy_(buf[:k], non_blocking=False)
+
+
+def write_manifest(ckpt_dir: str, step: int, n_ranks: int, dims: tuple[int, ...],
+                   cursors: dict[int, int]) -> str:
+    """checkpoint.py:201-213 (same JSON document)."""
+    doc = {"magic": MAGIC.decode(), "version": VERSION, "step": step, "n_ranks": n_ranks, "dims": list(dims),
+           "cursors": {str(rid): int(cur) for rid, cur in sorted(cursors.items())}}
+    path = manifest_path(ckpt_dir, step)
+    _atomic_write(path, json.dumps(doc, indent=1).encode())
+    return path
+
+
+_MANIFEST_RE = re.compile(r"^state_(\d{8})\.json$")
+
+
+def find_latest(ckpt_dir: str):
+    """checkpoint.py:219-230: newest step whose manifest parses and whose shard
+    files all exist, as (step, manifest)."""
+    if not os.path.isdir(ckpt_dir):
+        return None
+    steps = sorted((int(m.group(1)) for name in os.listdir(ckpt_dir) if (m := _MANIFEST_RE.match(name))),
+                   reverse=True)
+    for step in steps:
+        try:
+            with open(manifest_path(ckpt_dir, step), "rb") as fh:
+                doc = json.load(fh)
+        except (OSError, json.JSONDecodeError):
+            continue
+        if doc.get("magic") != MAGIC.decode() or doc.get("step") != step:
+            continue
+        if all(os.path.exists(shard_path(ckpt_dir, step, r)) for r in range(doc.get("n_ranks", 0))):
+            return step, doc
+    return None
+
+
+class PersistJob:
+    """A snapshot being written to storage (SnapshotStore.persist)."""
+
+    def __init__(self, thread: threading.Thread | None, box: dict):
+        self._thread, self._box = thread, box
+
+    def done(self) -> bool:
+        return self._thread is None or not self._thread.is_alive()
+
+    def wait(self) -> str:
+        """The written path; SnapshotUnavailable if a capture overwrote the
+        snapshot mid-write (nothing is left behind then)."""
+        if self._thread is not None:
+            self._thread.join()
+        if "error" in self._box:
+            raise self._box["error"]
+        return self._box["path"]
+
+
+def _persist_snapshot(store: "SnapshotStore", ckpt_dir: str, rank: int, box: dict, hook=None) -> None:
+    try:
+        torch.cuda.set_device(store.device_index)
+        pp, mp, pb, mb = C.c_void_p(), C.c_void_p(), C.c_uint64(), C.c_uint64()
+        seq0, step0 = C.c_uint64(), C.c_int64()
+        _lib.check(_lib.lib.ftar_snap_region(store.handle, C.byref(pp), C.byref(mp), C.byref(pb), C.byref(mb),
+                                             C.byref(seq0), C.byref(step0)), "ftar_snap_region")
+        if step0.value < 0:
+            raise SnapshotUnavailable(None)
+        step = int(step0.value)
+        os.makedirs(ckpt_dir, exist_ok=True)
+        path = shard_path(ckpt_dir, step, rank)
+        tmp = path + ".tmp"
+        stream = torch.cuda.Stream(device=store.device_index)
+        bufs = [torch.empty(_CHUNK, dtype=torch.uint8).pin_memory() for _ in range(2)]
+        events = [torch.cuda.Event(), torch.cuda.Event()]
+        from .ftar import _CudaView
+        regions = [torch.as_tensor(_CudaView(ptr, (n,), "|u1"), device=store.device)
+                   for ptr, n in ((pp.value, pb.value), (mp.value, mb.value)) if n]
+        try:
+            with open(tmp, "wb") as fh:
+                fh.write(MAGIC + _SHARD_HDR.pack(VERSION, step, rank, pb.value, mb.value))
+                # double-buffered: chunk i+1 is copied while chunk i is written
+                spans = [(r, off, min(_CHUNK, r.numel() - off)) for r in regions for off in range(0, r.numel(), _CHUNK)]
+
+                def issue(i):
+                    r, off, n = spans[i]
+                    with torch.cuda.stream(stream):
+                        bufs[i % 2][:n].copy_(r[off:off + n], non_blocking=True)
+                        events[i % 2].record(stream)
+
+                if spans:
+                    issue(0)
+                for i in range(len(spans)):
+                    if i + 1 < len(spans):
+                        issue(i + 1)  # its buffer's previous chunk was written to the file already
+                    events[i % 2].synchronize()
+                    fh.write(memoryview(bufs[i % 2].numpy())[:spans[i][2]])
+                    if hook is not None:
+                        hook(i)
+                fh.flush()
+                os.fsync(fh.fileno())
+            seq1, step1 = C.c_uint64(), C.c_int64()
+            _lib.check(_lib.lib.ftar_snap_region(store.handle, None, None, None, None, C.byref(seq1),
+                                                 C.byref(step1)), "ftar_snap_region")
+            if seq1.value != seq0.value:  # a capture ran while we copied: torn
+                raise SnapshotUnavailable(None if step1.value < 0 else int(step1.value))
+            os.rename(tmp, path)
+        except BaseException:
+            try:
+                os.unlink(tmp)
+            except OSError:
+                pass
+            raise
+        box["path"] = path
+    except BaseException as exc:  # noqa: BLE001 - surfaced by PersistJob.wait
+        box["error"] = exc
+
+
+def _persist(self, ckpt_dir: str, rank: int | None = None, background: bool = True, _hook=None) -> PersistJob:
+    """Write the snapshot's step to ``ckpt_dir`` in the reference's shard
+    format (§8f rank 4).  The device snapshot is streamed through two pinned
+    64 MiB buffers on a side stream; the seqlock is checked after the copy,
+    so a capture of the next step during the write yields
+    SnapshotUnavailable instead of a torn file."""
+    if self._snap is None:
+        raise SnapshotUnavailable(None)
+    rank = self.rank if rank is None else rank
+    box: dict = {}
+    if not background:
+        _persist_snapshot(self, ckpt_dir, rank, box, _hook)
+        return PersistJob(None, box)
+    t = threading.Thread(target=_persist_snapshot, args=(self, ckpt_dir, rank, box, _hook),
+                         name="ftar-snap-persist", daemon=True)
+    t.start()
+    return PersistJob(t, box)
+
+
+SnapshotStore.persist = _persist

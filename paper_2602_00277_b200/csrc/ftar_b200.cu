@@ -3067,6 +3067,26 @@ int ftar_snap_info(ftar_snap* s, int64_t* step, uint64_t* pbytes, uint64_t* mbyt
   return FTAR_OK;
 }
 
+int ftar_snap_region(ftar_snap* s, void** params, void** momentum, uint64_t* pbytes, uint64_t* mbytes,
+                     uint64_t* seq, int64_t* step) {
+  // §8f rank 4: where the retention-1 snapshot lives, and its seqlock word,
+  // for a host-side writer streaming it to storage.  A writer reads `seq`
+  // before and after copying: an odd or changed value means a capture ran in
+  // between and the copy is torn.  Synchronises the device.
+  if (!s) return fail(FTAR_ST_INVARIANT, "null snapshot");
+  DeviceGuard g(s->device);
+  SnapHdr h;
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(&h, s->arena, sizeof(h), cudaMemcpyDeviceToHost));
+  if (params) *params = s->arena + kSnapHdrBytes;
+  if (momentum) *momentum = s->arena + kSnapHdrBytes + h.pbytes;
+  if (pbytes) *pbytes = h.pbytes;
+  if (mbytes) *mbytes = h.mbytes;
+  if (seq) *seq = h.seq;
+  if (step) *step = (h.seq & 1u) ? -1 : h.step;
+  return FTAR_OK;
+}
+
 int ftar_snap_import(ftar_snap* s, int slot, const void* handle, size_t len, uint64_t capacity_bytes) {
   (void)capacity_bytes;
   if (!s || slot < 0 || slot >= kMaxSlots || !handle || len < sizeof(cudaIpcMemHandle_t))

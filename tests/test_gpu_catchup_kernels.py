@@ -96,3 +96,53 @@ def test_pick_donor():
     assert ck.pick_donor([0, 3], 3, rank=1) == 0
     with pytest.raises(errors.Recoverable):
         ck.pick_donor([3], 3, rank=0)
+
+
+def test_persist_snapshot_to_reference_format(tmp_path):
+    """§8f rank 4: the device snapshot streamed to the reference's shard file
+    (checkpoint.py:174-198) in the background; read back bit-exact through
+    both the bytes reader and the device restore."""
+    from paper_2602_00277_b200 import checkpoint as ck
+    store = ck.SnapshotStore(device=DEV, rank=2)
+    g = torch.Generator(device=DEV).manual_seed(5)
+    p = torch.randn(20_000_003, device=DEV, generator=g)  # > one 64 MiB staging chunk
+    m = torch.randn(3_000_001, device=DEV, generator=g)
+    store.capture(11, p, m)
+    job = store.persist(str(tmp_path))
+    path = job.wait()
+    assert path == ck.shard_path(str(tmp_path), 11, 2) and job.done()
+    rp, rm = ck.read_shard(str(tmp_path), 11, 2)
+    assert rp == p.cpu().numpy().tobytes() and rm == m.cpu().numpy().tobytes()
+    p2, m2 = torch.empty_like(p), torch.empty_like(m)
+    ck.read_shard_into(str(tmp_path), 11, 2, p2, m2)
+    assert torch.equal(p2, p) and torch.equal(m2, m)
+    ck.write_manifest(str(tmp_path), 11, 3, (1,), {})
+    for r in (0, 1):
+        ck.write_shard(str(tmp_path), 11, r, b"", b"")
+    assert ck.find_latest(str(tmp_path))[0] == 11
+    store.close()
+
+
+def test_persist_detects_a_capture_during_the_write(tmp_path):
+    """A capture of the next step while the snapshot is being streamed out
+    must not leave a torn file: SnapshotUnavailable, nothing on disk."""
+    import os
+
+    from paper_2602_00277_b200 import checkpoint as ck
+    store = ck.SnapshotStore(device=DEV)
+    p = torch.ones(40_000_000, device=DEV)
+    m = torch.zeros(10, device=DEV)
+    store.capture(3, p, m)
+
+    def recapture(i):
+        if i == 0:
+            store.capture(4, p * 2, m)
+            torch.cuda.synchronize()
+
+    job = store.persist(str(tmp_path), rank=0, background=False, _hook=recapture)
+    with pytest.raises(ck.SnapshotUnavailable):
+        job.wait()
+    assert not os.listdir(str(tmp_path))
+    # the new step persists cleanly afterwards
+    assert store.persist(str(tmp_path), rank=0).wait() == ck.shard_path(str(tmp_path), 4, 0)
+    store.close()

@@ -3,6 +3,8 @@ symbol the header declares; the geometry helpers match the reference's
 (tests/test_ftar.py:48-107); error mapping follows errors.py."""
 
 import ctypes as C
+import json
+import os
 
 import numpy as np
 import pytest
@@ -104,3 +106,50 @@ def test_no_cpu_fallback_without_library(tmp_path, monkeypatch):
         importlib.reload(_lib)
     monkeypatch.undo()
     importlib.reload(_lib)
+
+
+# --- persistent checkpoint format (§8f rank 4), pinned to the reference -------
+
+
+def _ckpt_cases():
+    with open(os.path.join(os.path.dirname(__file__), "golden", "ckpt_cases.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("case", _ckpt_cases(), ids=lambda c: f"step{c['step']}-rank{c['rank']}")
+def test_checkpoint_files_match_reference_bytes(tmp_path, case):
+    import hashlib
+
+    import numpy as np
+    from paper_2602_00277_b200 import checkpoint as ck
+    rng = np.random.default_rng(case["seed"])
+    p = rng.standard_normal(case["n_params"]).astype(np.float32)
+    m = rng.standard_normal(case["n_momentum"]).astype(np.float32)
+    path = ck.write_shard(str(tmp_path), case["step"], case["rank"], p.tobytes(), m.tobytes())
+    assert os.path.basename(path) == case["file_name"]
+    assert hashlib.sha256(open(path, "rb").read()).hexdigest() == case["file_sha256"]
+    rp, rm = ck.read_shard(str(tmp_path), case["step"], case["rank"])
+    assert rp == p.tobytes() and rm == m.tobytes()
+    mpath = ck.write_manifest(str(tmp_path), case["step"], case["rank"] + 1, (4, 8), {0: 5, 2: 9})
+    assert open(mpath, "rb").read().decode() == case["manifest"]
+
+
+def test_checkpoint_find_latest_and_validation(tmp_path):
+    from paper_2602_00277_b200 import checkpoint as ck
+    from paper_2602_00277_b200.errors import Fatal
+    d = str(tmp_path)
+    assert ck.find_latest(d) is None
+    for step in (3, 5):
+        for r in range(2):
+            ck.write_shard(d, step, r, b"\x01" * 8, b"\x02" * 4)
+        ck.write_manifest(d, step, 2, (1,), {0: step})
+    ck.write_manifest(d, 9, 2, (1,), {})  # a manifest without its shards is skipped
+    step, doc = ck.find_latest(d)
+    assert step == 5 and doc["n_ranks"] == 2
+    os.rename(ck.shard_path(d, 3, 0), ck.shard_path(d, 7, 0))  # header says (3, 0)
+    with pytest.raises(Fatal):
+        ck.read_shard(d, 7, 0)
+    with open(ck.shard_path(d, 5, 1), "r+b") as fh:  # truncated
+        fh.truncate(20)
+    with pytest.raises(Fatal):
+        ck.read_shard(d, 5, 1)
