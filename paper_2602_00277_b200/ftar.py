@@ -24,6 +24,7 @@ links closed; non-finite sums and protocol mismatches are Fatal, also with
 from __future__ import annotations
 
 import ctypes as C
+from collections import deque
 import logging
 import os
 import struct
@@ -244,6 +245,7 @@ class RingGroup:
         _lib.lib.ftar_ctx_pool(ctx, C.byref(ptr), C.byref(nbytes))
         self._pool_ptr, self._pool_bytes = ptr.value, nbytes.value
         self._lock = threading.Lock()
+        self._pending: deque = deque()  # queued collectives, oldest first (PendingAllReduce)
         if self._local:
             self.router.register(self)
         else:
@@ -481,7 +483,7 @@ class PendingAllReduce:
 def _drain_pending(group) -> None:
     """Abort every queued collective of `group` and collect its status (each
     pending handle keeps its own: ABORTED, or OK if it had already finished)."""
-    q = group.__dict__.get("_pending")
+    q = group._pending
     if not q:
         return
     _lib.lib.ftar_abort(group.ctx)
@@ -506,7 +508,7 @@ def ftar_all_reduce_async(group: RingGroup, buf: torch.Tensor, step: int, cfg: P
     code, dst = _check_buffers(buf, out)
     if group.n > 1 and not group.links_ready():
         raise Recoverable(PEER_RESET, "ring links not established")
-    q = group.__dict__.setdefault("_pending", __import__("collections").deque())
+    q = group._pending
     while len(q) >= 4:
         q[0].wait()
     flags = _lib.F_SCALE if scale is not None else 0
@@ -549,7 +551,7 @@ def ftar_all_reduce_sgd(group: RingGroup, grad: torch.Tensor, step: int, cfg: Pi
     momentum_out = torch.empty_like(momentum) if momentum_out is None else momentum_out
     if group.n > 1 and not group.links_ready():
         raise Recoverable(PEER_RESET, "ring links not established")
-    q = group.__dict__.get("_pending")
+    q = group._pending
     while q:
         q[0].wait()
     flags = _lib.F_SCALE if scale is not None else 0
@@ -582,7 +584,7 @@ def _host_all_reduce(group, buf, step, cfg, out, scale):
     hout = _as_host_tensor(out) if out is not None else None
     if group.n > 1 and not group.links_ready():
         raise Recoverable(PEER_RESET, "ring links not established")
-    q = group.__dict__.get("_pending")
+    q = group._pending
     while q:
         q[0].wait()
     if group._local:
@@ -620,7 +622,7 @@ def _host_all_reduce(group, buf, step, cfg, out, scale):
 
 
 def _remote_all_reduce(group, buf, dst, code, cfg, f_scale, flags):
-    q = group.__dict__.get("_pending")
+    q = group._pending
     while q:
         q[0].wait()
     with group._lock:

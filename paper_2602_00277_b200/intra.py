@@ -236,7 +236,7 @@ class IntraRank:
         elif not (out.is_cuda and out.dtype == torch.float32 and out.is_contiguous() and out.numel() == want):
             raise Fatal(INTERNAL_INVARIANT, f"out must be a contiguous fp32 CUDA tensor of {want} elements")
         # shares the group's FIFO of queued collectives (up to 4 in flight)
-        q = self.group.__dict__.setdefault("_pending", __import__("collections").deque())
+        q = self.group._pending
         while len(q) >= 4:
             q[0].wait()
         rc = _lib.lib.ftar_intra_launch(self.group.ctx, op, t.data_ptr(), code, out.data_ptr(), total, offs, lens,
