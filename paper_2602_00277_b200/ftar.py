@@ -401,9 +401,13 @@ class RingGroup:
 # --------------------------------------------------------------- all-reduce
 
 
-def _check_buffers(buf, out):
+def _check_buffers(buf, out, device=None):
     if not isinstance(buf, torch.Tensor) or not buf.is_cuda:
         raise Fatal(INTERNAL_INVARIANT, "all-reduce buffer must be a CUDA tensor")
+    if device is not None and buf.device.index != device:
+        # the kernel runs on the group's GPU: another GPU's tensor would be
+        # read through a peer mapping that may not exist
+        raise Fatal(INTERNAL_INVARIANT, f"buffer on {buf.device}, ring group on cuda:{device}")
     if not buf.is_contiguous():
         raise Fatal(INTERNAL_INVARIANT, "all-reduce buffer must be contiguous float32")
     code = _dtype_code(buf)
@@ -429,7 +433,7 @@ def ftar_all_reduce(group: RingGroup, buf: torch.Tensor, step: int, cfg: Pipelin
     cfg = cfg or PipelineConfig()
     if not (isinstance(buf, torch.Tensor) and buf.is_cuda):
         return _host_all_reduce(group, buf, step, cfg, out, scale)
-    code, dst = _check_buffers(buf, out)
+    code, dst = _check_buffers(buf, out, group.device_index)
     if group.n > 1 and not group.links_ready():
         raise Recoverable(PEER_RESET, "ring links not established")
     flags = _lib.F_SCALE if scale is not None else 0
@@ -505,7 +509,7 @@ def ftar_all_reduce_async(group: RingGroup, buf: torch.Tensor, step: int, cfg: P
         p = PendingAllReduce(group, ftar_all_reduce(group, buf, step, cfg, out=out, scale=scale), cfg)
         p.done = True
         return p
-    code, dst = _check_buffers(buf, out)
+    code, dst = _check_buffers(buf, out, group.device_index)
     if group.n > 1 and not group.links_ready():
         raise Recoverable(PEER_RESET, "ring links not established")
     q = group._pending
@@ -543,7 +547,10 @@ def ftar_all_reduce_sgd(group: RingGroup, grad: torch.Tensor, step: int, cfg: Pi
         raise Fatal(INTERNAL_INVARIANT, "gradient bucket must be a contiguous CUDA tensor")
     code = _dtype_code(grad)
     if grad_out is not None:
-        _check_buffers(grad, grad_out)
+        _check_buffers(grad, grad_out, group.device_index)
+    for t in (grad, params, momentum):
+        if t.device.index != group.device_index:
+            raise Fatal(INTERNAL_INVARIANT, f"tensor on {t.device}, ring group on cuda:{group.device_index}")
     for t in (params, momentum):
         if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.numel() == grad.numel()):
             raise Fatal(INTERNAL_INVARIANT, "params/momentum must be contiguous fp32 CUDA tensors shaped like grad")

@@ -569,3 +569,21 @@ def test_hsdp_step_with_ranks_is_bit_exact():
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["all_ranks_identical_params"] and line["bit_exact_vs_oracle"], line
+
+
+def test_buffer_on_another_gpu_is_rejected():
+    """The kernel runs on the group's GPU; a tensor living on another GPU is an
+    invariant violation, not a silent peer read."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    sys.path.insert(0, ROOT)
+    from paper_2602_00277_b200 import errors, ftar
+    g = ftar.RingGroup(0, 0, device=torch.device("cuda", 0))
+    try:
+        with pytest.raises(errors.Fatal):
+            ftar.ftar_all_reduce(g, torch.ones(16, device="cuda:1"), 0)
+        with pytest.raises(errors.Fatal):
+            ftar.ftar_all_reduce(g, torch.ones(16, device="cuda:0"), 0, out=torch.empty(16, device="cuda:1"))
+        assert torch.equal(ftar.ftar_all_reduce(g, torch.ones(16, device="cuda:0"), 0), torch.ones(16, device="cuda:0"))
+    finally:
+        g.close()
