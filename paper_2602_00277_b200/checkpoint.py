@@ -100,6 +100,8 @@ class SnapshotStore:
         """Replace the snapshot with `step`'s shard (stream-ordered on the
         current stream: the copy sees every prior write to params/momentum)."""
         p, m = _as_bytes_tensor(params), _as_bytes_tensor(momentum)
+        if p.device.index != self.device_index or m.device.index != self.device_index:
+            raise Fatal(INTERNAL_INVARIANT, f"snapshot tensors must live on cuda:{self.device_index}")
         pb, mb = p.numel() * p.element_size(), m.numel() * m.element_size()
         with self._lock:
             if self._snap is None:
