@@ -150,7 +150,7 @@ __device__ uint32_t wait_flag(const uint64_t* flag, uint64_t tag, const uint64_t
 __device__ uint32_t wait_go(const ArenaHdr* hdr, uint64_t want, uint64_t t0, uint64_t limit_ns) {
   for (uint32_t it = 0;; ++it) {
     if (ld_relaxed_gpu(&hdr->go) == want) {
-      fence_acq_rel_gpu();
+      (void)ld_acquire_gpu(&hdr->go);  // acquire-only (see wait_flag): no wait on this thread's writes
       return ST_OK;
     }
     if ((it & 15u) == 15u) {
@@ -166,7 +166,7 @@ __device__ uint32_t wait_go_bit(const ArenaHdr* hdr, uint64_t tag, int k, uint64
   for (uint32_t it = 0;; ++it) {
     const uint64_t v = ld_relaxed_gpu(&hdr->go2);
     if (flag_tag(v) == tag && ((v >> k) & 1u)) {
-      fence_acq_rel_gpu();
+      (void)ld_acquire_gpu(&hdr->go2);  // acquire-only; go2 only gains bits within a call
       return ST_OK;
     }
     if ((it & 15u) == 15u) {
