@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--max-mib", type=int, default=1024)
     ap.add_argument("--dtypes", default="bf16,f32")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--min-steps", type=int, default=5, help="timed calls per cell at the largest sizes")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -92,7 +93,7 @@ def main():
             buf = group.alloc_bucket(elems, tdt)
             buf.copy_(torch.randn(elems, device=dev).to(tdt))
             out = group.alloc_bucket(elems, torch.float32)
-            k = max(5, min(200, int(2e9 // max(nbytes, 1) // 8)))
+            k = max(args.min_steps, min(200, int(2e9 // max(nbytes, 1) // 8)))
             pend = []
 
             def step():
