@@ -186,6 +186,37 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------------------- inputs / parity
+
+
+def member_bucket(rank: int, elems: int, dtype: str):
+    """Replica `rank`'s synthetic gradient bucket:
+    default_rng((0, rank)).standard_normal(E) as fp32, bf16 buckets rounded
+    to nearest even.  A CPU tensor; the oracle regenerates the same bits."""
+    import numpy as np
+    import torch
+    x = torch.from_numpy(np.random.default_rng((0, rank)).standard_normal(elems).astype(np.float32))
+    return x.to(torch.bfloat16) if dtype == "bf16" else x
+
+
+def expected_digest(n: int, elems: int, dtype: str) -> str:
+    """sha256 of the reference result for the bench bucket: the oracle's fold
+    (tests/test_ftar.py:20-40 restated in oracle/ftar_oracle.py) of every
+    replica's bucket with the default geometry, times f32(1/n)
+    (replica.py:622-626).  The checker only: it never produces a timed
+    result."""
+    import hashlib
+    from oracle import ftar_oracle as orc  # checker (test infrastructure)
+    arrays = [member_bucket(r, elems, dtype).float().numpy() for r in range(n)]
+    want = orc.normalize(orc.oracle_reduce(arrays, 8 * MIB, 4), n)
+    return hashlib.sha256(want.tobytes()).hexdigest()
+
+
+def digest(t) -> str:
+    import hashlib
+    return hashlib.sha256(t.detach().float().cpu().numpy().tobytes()).hexdigest()
+
+
 # --------------------------------------------------------------------------- GPU
 
 METRIC = "FTAR bus GB/s vs bucket size at 2/4/8 B200 (% NVLink peak); catch-up ms/GB"
@@ -241,17 +272,49 @@ def timed_loop(fn, steps, stream, torch, drain=None):
     return t_start.elapsed_time(t_end) / 1e3, sum(per) / len(per) / 1e3
 
 
+class NvlinkBytes:
+    """This GPU's NVLink data bytes (TX, RX) from NVML field values
+    (NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX, KiB counters summed over all
+    links with scopeId = UINT_MAX), read around the timed region: the
+    measured traffic behind roofline.traffic for N >= 2."""
+
+    def __init__(self, cuda_index: int):
+        self.h = None
+        try:
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            pr = torch.cuda.get_device_properties(cuda_index)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            self.nv, self.h = nv, nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception as exc:  # noqa: BLE001
+            self.err = str(exc)[:120]
+
+    def read(self):
+        if self.h is None:
+            return None
+        nv = self.nv
+        try:
+            vals = nv.nvmlDeviceGetFieldValues(self.h, [(nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, 0xFFFFFFFF),
+                                                        (nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, 0xFFFFFFFF)])
+        except Exception as exc:  # noqa: BLE001
+            self.err = str(exc)[:120]
+            return None
+        if any(v.nvmlReturn != 0 for v in vals):
+            return None
+        return [int(v.value.ullVal) * 1024 for v in vals]
+
+
 def run_single(args):
     import torch
     from paper_2602_00277_b200 import ftar
     dev = torch.device("cuda", 0)
     n = args.replicas
     elems = args.bucket_mib * MIB // 4
-    tdtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     in_bytes = 2 if args.dtype == "bf16" else 4
     ring = ftar.LocalRing(n, device=dev, max_bucket_bytes=elems * in_bytes)
-    g = torch.Generator(device=dev).manual_seed(0)
-    bufs = [torch.randn(elems, device=dev, generator=g).to(tdtype) for _ in range(n)]
+    hosts = [member_bucket(r, elems, args.dtype) for r in range(n)]
+    bufs = [h.to(dev) for h in hosts]
     outs = bufs if args.inplace else [torch.empty(elems, device=dev) for _ in range(n)]
     cfg = ftar.PipelineConfig()
     scale = 1.0 / n
@@ -279,10 +342,27 @@ def run_single(args):
     for _ in range(args.warmup):
         step()
     drain()
+    # self-check outside the timed region: one call from the pristine inputs
+    # against the oracle's digest (in place: restore the inputs afterwards)
+    if args.inplace:
+        for b, h in zip(bufs, hosts):
+            b.copy_(h)
+    step()
+    drain()
+    got = [digest(o) for o in outs]
+    want = None if args.no_check else expected_digest(n, elems, args.dtype)
+    if args.inplace:
+        for b, h in zip(bufs, hosts):
+            b.copy_(h)
     torch.cuda.synchronize()
     with ClockSampler(0) as clk:
         total, per_launch = timed_loop(step, args.steps, stream, torch, drain=drain)
     t_step = total / args.steps
+    after = None if args.inplace else [digest(o) for o in outs]
+    parity = {"checked": "every replica's output of one call (before the timed region) vs the oracle digest"
+                         + ("" if args.inplace else "; outputs after the timed steps identical"),
+              "oracle_sha256": want, "ok": (want is not None and all(g == want for g in got)
+                                           and (after is None or after == got))}
     value = busbw(elems * in_bytes, t_step, n)
     peaks = measured_peaks()
     alg_bytes = n * elems * (in_bytes + 4)
@@ -295,17 +375,33 @@ def run_single(args):
             "definition": "n*E*(in_bytes+4): every replica's bucket read once, every replica's fp32 result "
                           "written once; peak = MEASURED_PEAKS.json hbm_gbs (measured copy)",
             "avg_launch_ms": round(per_launch * 1e3, 4)}
+    # the same replicas through the multi-GPU protocol kernel (allreduce_kernel,
+    # members as CTA groups of one cooperative launch): the product kernel's
+    # code path, timed here for the record (not the headline)
+    proto = None
+    if not args.no_protocol:
+        pring = ftar.LocalRing(n, device=dev, max_bucket_bytes=elems * in_bytes, protocol=True)
+        pout = [torch.empty(elems, device=dev) for _ in range(n)]
+        for _ in range(2):
+            pring.all_reduce(bufs, cfg, outs=pout, scale=scale)
+        pok = want is not None and all(digest(o) == want for o in pout)
+        tp, pl = timed_loop(lambda: pring.all_reduce(bufs, cfg, outs=pout, scale=scale), max(3, args.steps // 2),
+                            stream, torch)
+        proto = {"kernel": "allreduce_kernel (emulated: members as CTA groups)", "ms_per_call": round(pl * 1e3, 4),
+                 "busbw_gbs": round(busbw(elems * in_bytes, pl, n), 3),
+                 "hbm_gbs": round(alg_bytes / pl / 1e9, 1), "parity_ok": pok}
+        pring.close()
     # e2e through the public API with HOST buffers (the reference's call
     # shape): LocalRing.all_reduce_host pipelines chunked H2D, the range
     # all-reduce and D2H; every step moves the replicas' buckets in and the
     # reduced buckets out over PCIe inside the timed region
     e2e = None
     if not args.no_e2e:
-        hosts = [b.cpu().pin_memory() for b in bufs]
+        phost = [h.pin_memory() for h in hosts]
         hout = [torch.empty(elems, dtype=torch.float32).pin_memory() for _ in range(n)]
 
         def e2e_step():
-            ring.all_reduce_host(hosts, cfg, outs=hout, scale=scale, chunk_elems=args.host_chunk_elems)
+            ring.all_reduce_host(phost, cfg, outs=hout, scale=scale, chunk_elems=args.host_chunk_elems)
 
         for _ in range(2):
             e2e_step()
@@ -315,14 +411,18 @@ def run_single(args):
                "h2d_bytes_per_step": n * elems * in_bytes, "d2h_bytes_per_step": n * elems * 4,
                "ms_per_step": round(tot / ke * 1e3, 3), "steps": ke,
                "api": "LocalRing.all_reduce_host (pinned host buffers; chunked H2D/reduce/D2H pipeline)"}
+        if want is not None:
+            e2e["parity_ok"] = all(digest(h) == want for h in hout)
     cpu = None if args.no_cpu_baseline else cpu_ring_rate(n, elems, seconds=args.cpu_seconds)
     line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32" if args.dtype == "f32" else "bf16->f32", "data": "synthetic (torch.randn buckets)",
+            "dtype": "f32" if args.dtype == "f32" else "bf16->f32", "data": "synthetic (numpy default_rng normal buckets)",
             "config": workload_config(args, n), "roofline": roof,
             "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": e2e, "gpu_launches": args.steps, "clocks": clk.summary(),
+            "parity": parity["ok"], "parity_detail": parity,
+            "protocol_kernel_emulated": proto,
             "algbw_gbs": round(elems * in_bytes / t_step / 1e9, 3)}
     ring.close()
     print(json.dumps(line), flush=True)
@@ -344,10 +444,15 @@ def run_multi(args, rank, world, local_rank):
     group = ftar.RingGroup(rank, 0, fabric, device=dev, max_bucket_bytes=elems * in_bytes,
                            pool_bytes=elems * (in_bytes + 4) + 4096)
     group.reconfig({r: ftar.PeerAddress(r) for r in range(n)}, 1, deadline_s=60.0)
-    g = torch.Generator(device=dev).manual_seed(rank)
-    buf = group.alloc_bucket(elems, tdtype)
-    buf.copy_(torch.randn(elems, device=dev, generator=g).to(tdtype))
-    out = buf if args.inplace else group.alloc_bucket(elems, torch.float32)
+    host = member_bucket(rank, elems, args.dtype)
+    if args.unregistered:
+        # the reference call shape on an ordinary caching-allocator tensor
+        buf = host.to(dev)
+        out = buf if args.inplace else torch.empty(elems, device=dev)
+    else:
+        buf = group.alloc_bucket(elems, tdtype)
+        buf.copy_(host)
+        out = buf if args.inplace else group.alloc_bucket(elems, torch.float32)
     cfg = ftar.PipelineConfig()
     scale = 1.0 / n
     stream = torch.cuda.current_stream(dev)
@@ -369,8 +474,22 @@ def run_multi(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     drain()
+    # self-check outside the timed region (in place: from the pristine inputs)
+    if args.inplace:
+        buf.copy_(host)
+    step()
+    drain()
+    got = digest(out)
+    want = None
+    if not args.no_check:
+        box = [expected_digest(n, elems, args.dtype) if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        want = box[0]
+    if args.inplace:
+        buf.copy_(host)
     torch.cuda.synchronize()
     dist.barrier()
+    nvl = NvlinkBytes(local_rank)
     with ClockSampler(local_rank) as clk:
         # One untimed collective right before the window: it is a device-side
         # barrier, so the timed region starts on every rank when all streams
@@ -378,17 +497,35 @@ def run_multi(args, rank, world, local_rank):
         # skew from dist.barrier() (and the sampler's start) into the first
         # timed launch (measured: 0.7-1.5 ms vs 0.64 ms steady at 256 MiB, N=4).
         step()
+        drain()
+        c0 = nvl.read()
         total, per_launch = timed_loop(step, args.steps, stream, torch, drain)
+        c1 = nvl.read()
     dist.barrier()
+    after = None if args.inplace else digest(out)
     phases = phase_us(group)
     tt = torch.tensor([total, per_launch], dtype=torch.float64)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     total, per_launch = tt.tolist()
+    oks = [None] * n
+    dist.all_gather_object(oks, bool(want is not None and got == want and (after is None or after == got)))
+    nv_meas = None
+    if c0 is not None and c1 is not None:
+        nv_meas = [(b - a) / args.steps for a, b in zip(c0, c1)]
+    all_nv = [None] * n
+    dist.all_gather_object(all_nv, nv_meas)
     t_step = total / args.steps
     value = busbw(elems * in_bytes, t_step, n)
     nv_bytes = (n - 1) / n * elems * (in_bytes + 4)
+    rx = [m[1] for m in all_nv if m is not None]
+    tx = [m[0] for m in all_nv if m is not None]
     roof = {"bound": "nvlink", "achieved": round(nv_bytes / per_launch / 1e9, 1), "peak": NVLINK_PEER_GBS,
-            "unit": "GB/s", "frac": round(nv_bytes / per_launch / 1e9 / NVLINK_PEER_GBS, 4), "traffic": None,
+            "unit": "GB/s", "frac": round(nv_bytes / per_launch / 1e9 / NVLINK_PEER_GBS, 4),
+            "traffic": round(max(rx)) if rx else None,
+            "traffic_source": ("NVML NVLink data RX bytes per launch (field 139, all links), max over ranks, "
+                               "sampled around the timed region" if rx else "NVML NVLink counters unavailable"),
+            "nvlink_rx_bytes_per_launch": [round(x) for x in rx] if rx else None,
+            "nvlink_tx_bytes_per_launch": [round(x) for x in tx] if tx else None,
             "kernel": "allreduce_kernel (two-shot: RS by NVLink pulls, AG by pushes)",
             "algorithmic_bytes_per_launch": int(nv_bytes),
             "definition": "NVLink ingress per GPU (n-1)/n*E*(in_bytes+4): RS pulls every peer's slice of my "
@@ -398,11 +535,11 @@ def run_multi(args, rank, world, local_rank):
             "avg_launch_ms": round(per_launch * 1e3, 4)}
     e2e = None
     if not args.no_e2e:
-        host = buf.cpu().pin_memory()
+        phost = host.pin_memory()
         hout = torch.empty(elems, dtype=torch.float32).pin_memory()
 
         def e2e_step():
-            ftar.ftar_all_reduce(group, host, 0, cfg, out=hout, scale=scale)
+            ftar.ftar_all_reduce(group, phost, 0, cfg, out=hout, scale=scale)
 
         for _ in range(2):
             e2e_step()
@@ -412,22 +549,29 @@ def run_multi(args, rank, world, local_rank):
         tot, _ = timed_loop(e2e_step, ke, stream, torch)
         t = torch.tensor([tot], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ok = [None] * n
+        dist.all_gather_object(e_ok, bool(want is not None and digest(hout) == want))
         e2e = {"value": round(busbw(elems * in_bytes, t.item() / ke, n), 3), "unit": "GB/s",
                "h2d_bytes_per_step": elems * in_bytes, "d2h_bytes_per_step": elems * 4,
                "ms_per_step": round(t.item() / ke * 1e3, 3), "steps": ke,
-               "per": "rank (each GPU its own PCIe)",
+               "per": "rank (each GPU its own PCIe)", "parity_ok": all(e_ok),
                "api": "ftar_all_reduce(group, pinned host tensor, out=host tensor): chunked H2D/reduce/D2H"}
     nccl = None
     if not args.no_nccl:
         nccl = nccl_busbw(args, n, elems, tdtype, dev, stream)
     group.close()
     if rank == 0:
+        parity = {"checked": "every rank's output of one call (before the timed region) vs the oracle digest"
+                             + ("" if args.inplace else "; outputs after the timed steps identical"),
+                  "oracle_sha256": want, "ranks_ok": oks}
         line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": n, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None,
-                "dtype": "f32" if args.dtype == "f32" else "bf16->f32", "data": "synthetic (torch.randn buckets)",
+                "dtype": "f32" if args.dtype == "f32" else "bf16->f32",
+                "data": "synthetic (numpy default_rng normal buckets)",
                 "config": workload_config(args, n), "roofline": roof, "cpu_baseline": None,
                 "e2e": e2e, "gpu_launches": args.steps, "clocks": clk.summary(),
+                "parity": all(oks), "parity_detail": parity,
                 "algbw_gbs": round(elems * in_bytes / t_step / 1e9, 3),
                 "pct_nvlink_nominal": round(100 * value / NVLINK_NOMINAL_GBS, 2),
                 "phases_us_rank0": phases,
@@ -470,6 +614,30 @@ def nccl_busbw(args, n, elems, tdtype, dev, stream):
         return {"error": str(exc)[:200]}
 
 
+def _reexec_under_torchrun(n: int) -> None:
+    """`bench.py --gpus N` (N > 1) outside torchrun: one rank per GPU is the
+    only meaningful shape, so re-launch this command under
+    torch.distributed.run with N local ranks (never emulate silently)."""
+    import socket
+    try:
+        import torch
+        have = torch.cuda.device_count()
+    except Exception:  # noqa: BLE001
+        have = 0
+    if have < n:
+        log(f"bench.py --gpus {n}: only {have} CUDA device(s) visible; refusing to emulate {n} GPUs")
+        sys.exit(2)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    log("bench.py: re-launching under torchrun:", " ".join(cmd))
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -487,7 +655,13 @@ def main():
     ap.add_argument("--host-chunk-elems", type=int, default=8 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--no-check", action="store_true", help="skip the oracle self-check")
+    ap.add_argument("--no-protocol", action="store_true", help="N=1: skip the protocol-kernel record")
+    ap.add_argument("--unregistered", action="store_true",
+                    help="N>=2: buckets are ordinary torch.empty tensors (reference call shape), not pool buffers")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _reexec_under_torchrun(args.gpus)
     args.warmup = max(args.warmup, 3) if args.impl == "ftar" else args.warmup
     if args.dtype == "bf16":
         args.inplace = False

@@ -79,14 +79,16 @@ int ftar_ctx_pool(ftar_ctx* ctx, uint64_t* dev_ptr, uint64_t* bytes);
 int ftar_ctx_export(ftar_ctx* ctx, void* buf, size_t buflen, size_t* written);
 
 /* Map member `slot`'s arena from its exported handle (cached by slot until
- * ftar_ctx_unmap).  Replaces the dial-right/accept-left of
- * RingGroup.reconfig ftar.py:206-224. */
+ * ftar_ctx_unmap).  Importing a DIFFERENT handle into an occupied slot fails
+ * (FTAR_ST_INVARIANT): slots are never silently re-pointed.  Replaces the
+ * dial-right/accept-left of RingGroup.reconfig ftar.py:206-224. */
 int ftar_ctx_import(ftar_ctx* ctx, int slot, const void* handle, size_t len,
                     uint64_t arena_bytes);
 /* Single-process multi-GPU: map `other` (a context of this process on
  * another device) as member `slot` through peer access (no IPC). */
 int ftar_ctx_link_local(ftar_ctx* ctx, int slot, ftar_ctx* other);
-/* Drop a member mapping (RingGroup.close_links ftar.py:226-230). */
+/* Drop a member mapping (RingGroup.close_links ftar.py:226-230); refused for
+ * a slot of the current ring. */
 int ftar_ctx_unmap(ftar_ctx* ctx, int slot);
 
 /* Write the quorum decision into the control words (quorum.py:49-75 ->
@@ -229,9 +231,16 @@ int ftar_snap_capture(ftar_snap* s, uint64_t step, const void* params, uint64_t 
                       const void* momentum, uint64_t mbytes, void* stream);
 /* Host read of the snapshot header (step, lengths); -1 step if empty. */
 int ftar_snap_info(ftar_snap* s, int64_t* step, uint64_t* pbytes, uint64_t* mbytes);
-/* Recovering side: map a donor's snapshot arena into `local` (slot cache). */
+/* Recovering side: map a donor's snapshot arena into `local` (slot cache;
+ * a different handle in an occupied slot is refused). */
 int ftar_snap_import(ftar_snap* local, int slot, const void* handle, size_t len,
                      uint64_t capacity_bytes);
+/* Drop a donor mapping (a dead incarnation's snapshot stays pinned until its
+ * last importer unmaps it). */
+int ftar_snap_unmap(ftar_snap* local, int slot);
+/* The mapped donor's snapshot header, read over NVLink: the step it holds
+ * (-1 if none or mid-capture) and its lengths (checkpoint.py:76-80, 132-133). */
+int ftar_snap_peer_info(ftar_snap* local, int slot, int64_t* step, uint64_t* pbytes, uint64_t* mbytes);
 
 /* §8f rank 4 (persistent checkpoint, checkpoint.py:157-198): the snapshot's
  * device regions (params, then momentum) and its seqlock word.  A host
@@ -262,6 +271,9 @@ int ftar_snap_wait(ftar_snap* s, double progress_timeout_s, int64_t* available);
  * peer-access enabling for single-process multi-GPU probes.  Not on the
  * FTAR path; used to characterise NVLink pull vs push bandwidth. */
 int ftar_probe_copy(void* dst, const void* src, uint64_t bytes, int ctas, void* stream);
+/* The same copy by the TMA engine (cp.async.bulk global->shared->global),
+ * one thread per CTA driving a `stages`-deep pipeline of `tile`-byte tiles. */
+int ftar_probe_bulk(void* dst, const void* src, uint64_t bytes, int ctas, int tile, int stages, void* stream);
 /* %globaltimer stamps of the last call's phases (start, entry passed,
  * reduce-scatter published, all-gather barrier passed, end). */
 int ftar_phase_times(ftar_ctx* ctx, uint64_t* out, int n);

@@ -69,12 +69,15 @@ SIGNATURES = {
     "ftar_snap_capture": (i32, [c_snap_p, u64, vp, u64, vp, u64, vp]),
     "ftar_snap_info": (i32, [c_snap_p, C.POINTER(i64), C.POINTER(u64), C.POINTER(u64)]),
     "ftar_snap_import": (i32, [c_snap_p, i32, vp, C.c_size_t, u64]),
+    "ftar_snap_unmap": (i32, [c_snap_p, i32]),
+    "ftar_snap_peer_info": (i32, [c_snap_p, i32, C.POINTER(i64), C.POINTER(u64), C.POINTER(u64)]),
     "ftar_snap_pull_launch": (i32, [c_snap_p, i32, c_snap_p, u64, vp, u64, vp, u64, i32, vp]),
     "ftar_snap_pull_multi_launch": (i32, [c_snap_p, C.POINTER(i32), i32, c_snap_p, u64, vp, u64, vp, u64, i32, vp]),
     "ftar_snap_poll": (i32, [c_snap_p, C.POINTER(i32), C.POINTER(u64), C.POINTER(i64)]),
     "ftar_snap_abort": (i32, [c_snap_p]),
     "ftar_snap_wait": (i32, [c_snap_p, dbl, C.POINTER(i64)]),
     "ftar_probe_copy": (i32, [vp, vp, u64, i32, vp]),
+    "ftar_probe_bulk": (i32, [vp, vp, u64, i32, i32, i32, vp]),
     "ftar_peer_enable": (i32, [i32, i32]),
     "ftar_probe_fence": (i32, [vp, vp, vp, u64, i32, i32, vp, i32, vp]),
     "ftar_phase_times": (i32, [c_ctx_p, C.POINTER(u64), i32]),

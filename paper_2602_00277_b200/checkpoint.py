@@ -8,12 +8,19 @@
 * ``fetch_shard``    the recovering replica pulls the donor's snapshot over
   NVLink with a rate-limited kernel (``ctas`` SMs) on a low-priority side
   stream, so the donor's and everyone else's FTAR steps keep running
-  (checkpoint.py:117-144, replica.py:452-493).  A donor that holds another
+  (checkpoint.py:117-144, replica.py:452-493).  Called with the reference's
+  arguments ``fetch_shard(addr, step, rank, replica_id, incarnation,
+  timeout_s, plan)`` it resolves the caller's own store from a per-process
+  registry keyed by (replica_id, rank) and the donor from ``addr.replica_id``
+  (in this process, or through the store's fabric), and returns
+  ``(params, momentum)`` as device byte tensors.  A donor that holds another
   step — or re-captures during the pull — yields ``SnapshotUnavailable``
-  with the step it has (checkpoint.py:132-133).
+  with the step it has (checkpoint.py:132-133); a donor that never published
+  or whose process is gone yields ``Recoverable(PEER_DOWN)``.
 * ``pick_donor``     round-robin donor choice (checkpoint.py:147-154).
-* ``serve_fetches``  kept for API shape: on NVLink the donor serves by
-  publishing its snapshot arena once; no per-request thread is needed.
+* ``serve_fetches``  the reference's server thread target: on NVLink the
+  donor serves by publishing its snapshot arena once, so the thread only
+  waits for ``stop``.
 
 * Persistent checkpoints (checkpoint.py:155-230): the
   reference's shard file and manifest format byte for byte (``write_shard``,
@@ -34,6 +41,8 @@ import re
 import struct
 import threading
 import time
+
+import weakref
 
 import torch
 
@@ -56,6 +65,12 @@ def _as_bytes_tensor(t: torch.Tensor) -> torch.Tensor:
     return t
 
 
+# Every SnapshotStore of this process by (replica_id, rank): how the
+# reference-shaped fetch_shard(addr, step, rank, replica_id, ...) finds the
+# caller's own store and in-process donors.
+_STORES: "weakref.WeakValueDictionary[tuple[int, int], SnapshotStore]" = weakref.WeakValueDictionary()
+
+
 class SnapshotStore:
     """Latest committed (params, momentum) shard of this rank on its GPU."""
 
@@ -74,8 +89,13 @@ class SnapshotStore:
         self._cap = 0
         self._step = None
         self._lens = (0, 0)
+        # donor snapshot mappings by (donor replica, incarnation); slots from a
+        # free list, a donor's older incarnation is unmapped when a newer one
+        # is mapped, and retain() drops donors that left the decision
         self._peers: dict[tuple[int, int], int] = {}
+        self._free_slots: list[int] = list(range(255, -1, -1))
         self.map_log: list[tuple] = []
+        _STORES[(replica_id, rank)] = self
         if capacity_bytes:
             self._alloc(capacity_bytes)
 
@@ -98,8 +118,10 @@ class SnapshotStore:
 
     def capture(self, step: int, params: torch.Tensor, momentum: torch.Tensor) -> None:
         """Replace the snapshot with `step`'s shard (stream-ordered on the
-        current stream: the copy sees every prior write to params/momentum)."""
-        p, m = _as_bytes_tensor(params), _as_bytes_tensor(momentum)
+        current stream: the copy sees every prior write to params/momentum).
+        Host bytes (the reference's call shape) are copied to the device
+        first."""
+        p, m = self._device_bytes(params), self._device_bytes(momentum)
         if p.device.index != self.device_index or m.device.index != self.device_index:
             raise Fatal(INTERNAL_INVARIANT, f"snapshot tensors must live on cuda:{self.device_index}")
         pb, mb = p.numel() * p.element_size(), m.numel() * m.element_size()
@@ -126,11 +148,41 @@ class SnapshotStore:
         _lib.check(_lib.lib.ftar_snap_info(self._snap, C.byref(st), C.byref(pb), C.byref(mb)), "ftar_snap_info")
         return None if st.value < 0 else st.value
 
+    def _device_bytes(self, x):
+        if isinstance(x, torch.Tensor):
+            if x.is_cuda:
+                return _as_bytes_tensor(x)
+            x = x.contiguous().view(-1).view(torch.uint8)
+        else:
+            import numpy as np
+            x = torch.from_numpy(np.frombuffer(bytes(x), dtype=np.uint8).copy())
+        return x.to(self.device) if x.numel() else torch.empty(0, dtype=torch.uint8, device=self.device)
+
     def get(self, step: int):
-        """Lengths of the held shard if it is `step` (checkpoint.py:76-80)."""
+        """The held shard if it is `step` (checkpoint.py:76-80): (params,
+        momentum) as device byte tensors viewing the snapshot arena (valid
+        until the next capture); SnapshotUnavailable(held step) otherwise."""
         with self._lock:
             if self._step != step:
                 raise SnapshotUnavailable(self._step)
+            pb, mb = self._lens
+            pp, mp = C.c_void_p(), C.c_void_p()
+            _lib.check(_lib.lib.ftar_snap_region(self._snap, C.byref(pp), C.byref(mp), None, None, None, None),
+                       "ftar_snap_region")
+            from .ftar import _CudaView
+
+            def view(ptr, n):
+                if not n:
+                    return torch.empty(0, dtype=torch.uint8, device=self.device)
+                t = torch.as_tensor(_CudaView(ptr, (n,), "|u1"), device=self.device)
+                t._ftar_owner = self
+                return t
+            return view(pp.value, pb), view(mp.value, mb)
+
+    @property
+    def lengths(self) -> tuple[int, int]:
+        """(params bytes, momentum bytes) of the held shard."""
+        with self._lock:
             return self._lens
 
     def close(self) -> None:
@@ -192,19 +244,55 @@ class SnapshotStore:
                 raise err
 
     def _map_donor(self, donor_replica: int, rank: int, timeout_s: float) -> int:
+        if self.fabric is None:
+            raise Recoverable(PEER_DOWN, f"replica {donor_replica} is not in this process and no fabric is set")
         t0 = time.monotonic()
         info = self.fabric.lookup(rank, donor_replica, timeout_s, what="snap")
         key = (donor_replica, info.incarnation)
         if key not in self._peers:
+            # an older incarnation of this donor is dead: release its snapshot
+            for old in [k for k in self._peers if k[0] == donor_replica]:
+                self._unmap(old)
+            if not self._free_slots:
+                raise Fatal(INTERNAL_INVARIANT, "no free donor slots (256 mapped)")
             t1 = time.monotonic()
-            slot = len(self._peers) % 256
+            slot = self._free_slots.pop()
             rc = _lib.lib.ftar_snap_import(self._snap, slot, info.handle, len(info.handle), info.arena_bytes)
             if rc:
+                self._free_slots.append(slot)
                 raise Recoverable(PEER_DOWN, f"cannot map snapshot of replica {donor_replica}: {_lib.last_error()}")
             self._peers[key] = slot
             # (donor, lookup s, IPC open s, bytes): start-up cost accounting
             self.map_log.append((donor_replica, t1 - t0, time.monotonic() - t1, info.arena_bytes))
         return self._peers[key]
+
+    def _unmap(self, key) -> None:
+        slot = self._peers.pop(key)
+        _lib.check(_lib.lib.ftar_snap_unmap(self._snap, slot), f"unmap snapshot of replica {key[0]}")
+        self._free_slots.append(slot)
+
+    def retain(self, live) -> None:
+        """Unmap every donor snapshot whose (replica, incarnation) is not in
+        `live` (a {replica: incarnation} map of the current decision, or an
+        iterable of replica ids: any incarnation of those is kept)."""
+        self.join_connect()
+        if isinstance(live, dict):
+            drop = [k for k in self._peers if live.get(k[0]) != k[1]]
+        else:
+            keep = {int(r) for r in live}
+            drop = [k for k in self._peers if k[0] not in keep]
+        for k in drop:
+            self._unmap(k)
+
+    @property
+    def mapped_donors(self) -> list[tuple[int, int]]:
+        return sorted(self._peers)
+
+    def _peer_header(self, slot: int):
+        st, pb, mb = C.c_int64(), C.c_uint64(), C.c_uint64()
+        _lib.check(_lib.lib.ftar_snap_peer_info(self._snap, slot, C.byref(st), C.byref(pb), C.byref(mb)),
+                   "ftar_snap_peer_info")
+        return (None if st.value < 0 else int(st.value)), int(pb.value), int(mb.value)
 
 
 class CatchupPull:
@@ -267,6 +355,8 @@ def start_fetch(local: SnapshotStore, donor, step: int, rank: int, params_out: t
         slots, src = [], donor.handle
         if src is None:
             raise SnapshotUnavailable(None)
+        if donor.device_index != local.device_index:  # in-process donor on another GPU: peer access
+            _lib.check(_lib.lib.ftar_peer_enable(local.device_index, donor.device_index), "ftar_peer_enable")
     else:
         donors = list(donor) if isinstance(donor, (list, tuple)) else [donor]
         slots, src = [local._map_donor(int(d), rank, timeout_s) for d in donors], None
@@ -279,19 +369,64 @@ def start_fetch(local: SnapshotStore, donor, step: int, rank: int, params_out: t
     return CatchupPull(local, p, m, stream, timeout_s)
 
 
-def fetch_shard(donor, step: int, rank: int, replica_id: int = 0, incarnation: int = 0,
+def _donor_id(addr) -> int:
+    rid = getattr(addr, "replica_id", addr)
+    return int(rid)
+
+
+def _default_fabric():
+    for st in list(_STORES.values()):
+        if st.fabric is not None and not isinstance(st.fabric, LocalFabric):
+            return st.fabric
+    return None
+
+
+def fetch_shard(addr, step: int, rank: int, replica_id: int = 0, incarnation: int = 0,
                 timeout_s: float = 5.0, plan=None, *, local: SnapshotStore | None = None,
                 out: tuple[torch.Tensor, torch.Tensor] | None = None, ctas: int = 16):
     """Pull (params, momentum) of one rank shard of a committed step
-    (checkpoint.py:117-144).  Blocks until done; raises SnapshotUnavailable
-    when the donor holds another step and Recoverable when it is gone."""
+    (checkpoint.py:117-144); the reference's signature.
+
+    ``addr`` names the donor: a ``PeerAddress`` (its ``replica_id``), a
+    replica id, a list of replica ids (striped pull), or a SnapshotStore of
+    this process.  The caller's own store is ``local`` or the registered
+    store of (replica_id, rank) (one is created on first use).  Returns
+    (params, momentum) as device byte tensors (``out`` if given).  Raises
+    SnapshotUnavailable(held step) when the donor holds another step and
+    Recoverable(PEER_DOWN) when the donor never published or is gone; ``plan``
+    (the reference's socket fault plan) has no NVLink analogue."""
     if local is None:
-        raise Fatal(INTERNAL_INVARIANT, "fetch_shard needs the recovering replica's SnapshotStore (local=)")
+        local = _STORES.get((replica_id, rank))
+        if local is None:
+            local = SnapshotStore(device=torch.cuda.current_device(), fabric=_default_fabric(), rank=rank,
+                                  replica_id=replica_id, incarnation=incarnation)
+    if isinstance(addr, SnapshotStore):
+        donor = addr
+    elif isinstance(addr, (list, tuple)):
+        donor = [_donor_id(a) for a in addr]
+    else:
+        did = _donor_id(addr)
+        donor = _STORES.get((did, rank))
+        if donor is None or donor is local:
+            donor = did
+    if isinstance(donor, SnapshotStore):
+        held = donor.step
+        if held != step:
+            raise SnapshotUnavailable(held)
+        pb, mb = donor.lengths
+    else:
+        ids = donor if isinstance(donor, list) else [donor]
+        if local.handle is None:
+            local._alloc(16)
+        pb = mb = None
+        for d in ids:
+            held, dpb, dmb = local._peer_header(local._map_donor(d, rank, timeout_s))
+            if held != step:
+                raise SnapshotUnavailable(held)
+            if pb is not None and (dpb, dmb) != (pb, mb):
+                raise Fatal(PROTOCOL_VIOLATION, "donors disagree on the shard's lengths")
+            pb, mb = dpb, dmb
     if out is None:
-        if isinstance(donor, SnapshotStore):
-            pb, mb = donor._lens
-        else:
-            raise Fatal(INTERNAL_INVARIANT, "out= tensors are required for a remote donor")
         out = (torch.empty(pb, dtype=torch.uint8, device=local.device),
                torch.empty(mb, dtype=torch.uint8, device=local.device))
     return start_fetch(local, donor, step, rank, out[0], out[1], timeout_s, ctas).wait()
@@ -306,8 +441,14 @@ def pick_donor(healthy, self_replica: int, rank: int, attempt: int = 0) -> int:
 
 
 def serve_fetches(router=None, store: SnapshotStore | None = None, stop=None, pred=None) -> None:
-    """API shape of checkpoint.py:83-95.  NVLink donors need no server: the
-    snapshot arena is published when allocated and peers read it directly."""
+    """Thread target of checkpoint.py:83-95.  An NVLink donor serves by
+    publishing its snapshot arena (done when the arena is allocated; peers
+    then read it directly), so there is no per-request work: the thread
+    only waits for ``stop``, as the reference's server loop does."""
+    if stop is None:
+        return None
+    while not stop.wait(0.25):
+        pass
     return None
 
 

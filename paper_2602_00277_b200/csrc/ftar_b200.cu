@@ -74,6 +74,7 @@ struct LaunchParams {
   float scale;
   uint32_t flags;
   uint32_t contrib;              // bit i: ring index i contributes data (healthy)
+  uint32_t workers;              // bit i: ring index i reduces a slice (contributors; all if none)
   uint32_t dtype;
   int self;                      // my ring index (real mode)
   int emulated;                  // 1: ring index = blockIdx.y (in-process ring)
@@ -82,6 +83,7 @@ struct LaunchParams {
   int rs_layout;                 // 0: contiguous span per CTA, 1: grid-strided tiles
   int diag;                      // timing diagnostics: 1 = RS stores skipped, 2 = RS reads local only
   int rs_ctas;                   // CTAs that reduce (the rest only all-gather); <= gridDim.x
+  uint32_t tma_stages;           // > 0: bulk-copy (TMA) data path with this many smem stages
   uint32_t intra_op;             // intra-replica collective (kIntraRS / kIntraAG), 0 = FTAR
   uint64_t seg_off[kMaxMembers]; // intra: rank k's shard is elements [seg_off[k], +seg_len[k])
   uint64_t seg_len[kMaxMembers];
@@ -104,7 +106,38 @@ __device__ __forceinline__ uint64_t call_fingerprint(const LaunchParams& p, int 
   h ^= (p.cap + 0x632BE59BD9B4E019ull) + (h << 6) + (h >> 2);
   h ^= ((uint64_t)p.dtype | ((uint64_t)n << 8)) + (h << 6) + (h >> 2);
   h ^= (p.ebase * 31 + p.total) + (h << 6) + (h >> 2);
+  h ^= ((uint64_t)p.contrib * 0x94D049BB133111EBull) + (h << 6) + (h >> 2);  // members agree on who contributes
   return h;
+}
+
+// The control plane's words for this op, in ONE 16-byte PCIe read of the
+// pinned control block: the epoch must be this call's generation and, for a
+// real (one GPU per member) launch, the live mask and contributor mask must
+// be the ones the launch was built from — a queued op never runs against a
+// membership the control plane has since replaced.
+__device__ __forceinline__ bool ctl_mismatch(const HostCtl* ctl, uint64_t tag, int n, uint32_t contrib, bool real,
+                                             bool check_contrib) {
+  uint64_t e, m;
+  asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];" : "=l"(e), "=l"(m) : "l"(ctl) : "memory");
+  if (e != tag_gen(tag)) return true;
+  if (!real) return false;
+  const uint32_t all = (n >= 32) ? 0xffffffffu : ((1u << n) - 1u);
+  if ((uint32_t)m != all) return true;
+  return check_contrib && (uint32_t)(m >> 32) != contrib;
+}
+
+// Member i's reduce-scatter slice.  Only contributors (the workers) reduce:
+// a behind replica (replica.py:574-577) owns no slice, issues no loads and
+// is served by the others; the fold order is set by the segment owner, not
+// by who executes it, so the bits do not change.
+__device__ __forceinline__ void slice_of(const LaunchParams& p, int i, uint64_t E, uint64_t& lo, uint64_t& hi) {
+  if (!((p.workers >> i) & 1u)) {
+    lo = hi = E;
+    return;
+  }
+  const uint64_t w = (uint64_t)__popc(p.workers & ((1u << i) - 1u));
+  lo = umin(w * p.slice, E);
+  hi = umin(lo + p.slice, E);
 }
 
 __device__ uint32_t wait_flag(const uint64_t* flag, uint64_t tag, const uint64_t* poison,
@@ -328,9 +361,9 @@ struct Unroll {
 
 // Reduce elements [a, b) whose fold starts at ring index s.  All threads of the
 // CTA cooperate; each round a thread issues U x N coalesced vector loads
-// (unconditionally: out-of-range vectors re-read a valid one and are masked,
-// non-contributors read and are zeroed by select) before the first add, so no
-// branch separates the loads; scalars at the ragged edges.
+// (out-of-range vectors re-read a valid one and are masked; a
+// non-contributor's loads are predicated off and read as +0.0) before the
+// first add, so no branch separates the loads; scalars at the ragged edges.
 template <int N, class In, int U, class Sink>
 __device__ __forceinline__ void fold_range(const typename In::T* const* src, const Sink& sink,
                                            uint64_t a, uint64_t b, int s, uint32_t contrib,
@@ -371,16 +404,16 @@ __device__ __forceinline__ void fold_range(const typename In::T* const* src, con
         const uint64_t v = v0 + (uint64_t)u * kThreads;
         const uint64_t vv = v < ve ? v : vb;  // clamp: keep the load unconditional
 #pragma unroll
-        for (int k = 0; k < N; ++k) raw[u][k] = In::load4(rs[k], vv * 4);
+        for (int k = 0; k < N; ++k) raw[u][k] = In::load4_if(rs[k], vv * 4, cb[k]);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint64_t v = v0 + (uint64_t)u * kThreads;
         float acc[4], x[4];
-        In::cvt4(cb[0] ? raw[u][0] : In::zero(), acc);
+        In::cvt4(raw[u][0], acc);
 #pragma unroll
         for (int k = 1; k < N; ++k) {
-          In::cvt4(cb[k] ? raw[u][k] : In::zero(), x);
+          In::cvt4(raw[u][k], x);
 #pragma unroll
           for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], x[i]);
         }
@@ -539,6 +572,269 @@ __device__ __forceinline__ void copy_f32(float* dst, const float* src, uint64_t 
   if (t < cnt && first < 4) dst[t] = src[t];
 }
 
+// ---------------------------------------------------------------- bulk-copy (TMA) data path
+// The reduce-scatter with the TMA engine moving every byte.  Per CTA, a ring
+// of S smem stages; stage s holds one tile (kTmaTile elements) of every
+// contributing member's input, landed by cp.async.bulk (peer -> shared) on
+// mbarrier full[s].  Thread 0 keeps S-1 tiles of loads in flight (issued one
+// tile ahead of the fold that frees their stage), so the bytes in flight per
+// SM are ~(S-1) x (N-1) x tile, not a register budget: 16-32 CTAs saturate
+// NVLink where the register-staged loop needed 64-128 (tools/tma_probe.py).
+// All 512 threads fold the tile from shared memory (one 4-element vector
+// each, reference order from the segment owner, fused cast / scale /
+// non-finite vote) into an fp32 out tile, which thread 0 bulk-stores to every
+// destination: the result region, my `out`, and in push mode every peer's
+// `out` (the all-gather fused in: one smem tile, N posted bulk writes).
+// Non-contributors' tiles are never loaded (their +0.0 is folded from a
+// register).  Needs every segment to be >= one tile (at most one owner change
+// per tile) and 16-byte aligned buffers; anything else takes fold_tiles.
+constexpr uint32_t kTmaTile = kThreads * 4;           // elements per tile
+constexpr uint32_t kTmaMetaBytes = 1024;              // mbarriers + per-stage tile metadata
+// dynamic smem per CTA (1 CTA / SM): 227 KB less room for the kernel's
+// static shared variables and the 1 KB alignment of the dynamic window
+constexpr uint32_t kTmaSmemMax = 227 * 1024 - 2048;
+
+struct TmaMeta {            // what the producer recorded for the tile in a stage
+  uint64_t a;               // first element (call-local)
+  uint32_t cnt;             // elements (multiple of 8)
+  int s0, s1;               // owner of [a, bnd) and of [bnd, a + cnt)
+  uint32_t bnd;             // boundary offset within the tile (>= cnt: none)
+};
+
+__host__ __device__ __forceinline__ uint64_t tma_out_off() { return kTmaMetaBytes; }
+__host__ __device__ __forceinline__ uint64_t tma_stage_off() { return kTmaMetaBytes + 2ull * kTmaTile * 4; }
+__host__ __device__ __forceinline__ uint32_t tma_stages_for(int n, int in_bytes) {
+  const uint64_t stage = (uint64_t)n * kTmaTile * (uint64_t)in_bytes;
+  const uint64_t s = (kTmaSmemMax - tma_stage_off()) / stage;
+  return (uint32_t)(s > 16 ? 16 : s);
+}
+__host__ __device__ __forceinline__ uint64_t tma_smem_bytes(int n, int in_bytes, uint32_t stages) {
+  return tma_stage_off() + (uint64_t)stages * n * kTmaTile * (uint64_t)in_bytes;
+}
+
+// Issue the bulk loads of tile t (elements [lo + t*TE, ...)) into stage s.
+template <int N, class In>
+__device__ __forceinline__ void tma_issue(const LaunchParams& p, const typename In::T* const* src, char* smem,
+                                          uint32_t S, uint64_t lo, uint64_t lenv, uint64_t t, uint64_t j) {
+  // stage (and mbarrier phase) by the CTA-local sequence number j
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  TmaMeta* meta = reinterpret_cast<TmaMeta*>(smem + 256);
+  const uint32_t s = (uint32_t)(j % S);
+  const uint64_t a = lo + t * kTmaTile;
+  const uint32_t cnt = (uint32_t)umin(kTmaTile, lo + lenv - a);
+  int s0;
+  uint64_t send;
+  owner_of(a, p, N, s0, send);
+  TmaMeta m;
+  m.a = a;
+  m.cnt = cnt;
+  m.s0 = s0;
+  m.s1 = s0;
+  m.bnd = 0xffffffffu;
+  if (send < a + cnt) {  // one owner change inside the tile (segments >= a tile)
+    uint64_t send2;
+    owner_of(send, p, N, m.s1, send2);
+    m.bnd = (uint32_t)(send - a);
+  }
+  meta[s] = m;
+  const uint32_t bytes = cnt * (uint32_t)In::kBytes;
+  const uint32_t nsrc = __popc(p.contrib & ((1u << N) - 1u));
+  char* stage = smem + tma_stage_off() + (uint64_t)s * N * kTmaTile * In::kBytes;
+  if (nsrc == 0) {
+    mbar_arrive(&full[s]);
+    return;
+  }
+  mbar_expect_tx(&full[s], bytes * nsrc);
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+    if ((p.contrib >> j) & 1u) bulk_g2s(stage + (uint64_t)j * kTmaTile * In::kBytes, src[j] + a, bytes, &full[s]);
+}
+
+// Fold one 4-element vector (elements e..e+3 of the tile at offset `off`)
+// whose fold starts at ring index `own`, reading every contributor's copy
+// from the stage.
+template <int N, class In>
+__device__ __forceinline__ void tma_fold_vec(const char* stage, uint32_t off, int own, uint32_t contrib,
+                                             float (&acc)[4]) {
+  using Raw = typename In::Raw;
+  bool first = true;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    int m = own + k;
+    if (m >= N) m -= N;
+    float x[4];
+    if ((contrib >> m) & 1u) {
+      const Raw r = *reinterpret_cast<const Raw*>(stage + ((uint64_t)m * kTmaTile + off) * In::kBytes);
+      In::cvt4(r, x);
+    } else {
+      x[0] = x[1] = x[2] = x[3] = 0.0f;
+    }
+    if (first) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = x[i];
+      first = false;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], x[i]);
+    }
+  }
+}
+template <int N, class In>
+__device__ __forceinline__ float tma_fold_one(const char* stage, uint32_t off, int own, uint32_t contrib) {
+  float acc = 0.0f;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    int m = own + k;
+    if (m >= N) m -= N;
+    float x = 0.0f;
+    if ((contrib >> m) & 1u) {
+      if (In::kBytes == 4) x = *reinterpret_cast<const float*>(stage + ((uint64_t)m * kTmaTile + off) * 4);
+      else x = __uint_as_float((uint32_t)*reinterpret_cast<const uint16_t*>(stage + ((uint64_t)m * kTmaTile + off) * 2) << 16);
+    }
+    acc = k == 0 ? x : __fadd_rn(acc, x);
+  }
+  return acc;
+}
+
+// Reduce my slice [lo, hi) through the bulk-copy pipeline; results bulk-stored
+// to dsts[0..ndst) (each indexed by call-local element).  The < 8-element
+// ragged tail of the slice is folded by the last CTA with fold_range into
+// `tail_sink`.  Returns tiles done, or -1 when the fault hook stopped it.
+template <int N, class In, class Sink>
+__device__ int fold_tiles_tma(const LaunchParams& p, const typename In::T* const* src, float* const* dsts, int ndst,
+                              const Sink& tail_sink, uint64_t lo, uint64_t hi, bool do_scale, uint32_t& nf,
+                              HostCtl* ctl, int max_tiles, char* smem) {
+  const int tid = threadIdx.x;
+  const uint32_t S = p.tma_stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  const TmaMeta* meta = reinterpret_cast<const TmaMeta*>(smem + 256);
+  float* const outt = reinterpret_cast<float*>(smem + tma_out_off());
+  const uint64_t G = (p.rs_ctas > 0 && p.rs_ctas < (int)gridDim.x) ? (uint64_t)p.rs_ctas : gridDim.x;
+  if (blockIdx.x >= G) return 0;
+  const uint64_t len = hi > lo ? hi - lo : 0;
+  const uint64_t lenv = len & ~7ull;  // bulk-copied part (16-byte granules for bf16 and fp32)
+  const uint64_t ntiles = (lenv + kTmaTile - 1) / kTmaTile;
+  const uint64_t per = (ntiles + G - 1) / G;
+  const uint64_t t0 = umin(blockIdx.x * per, ntiles), t1 = umin(t0 + per, ntiles);
+  const uint64_t cnt = t1 - t0;
+  const float scale = p.scale;
+  if (tid == 0) {  // (the kernel initialised the mbarriers at entry)
+    for (uint64_t j = 0; j + 1 < S && j < cnt; ++j) tma_issue<N, In>(p, src, smem, S, lo, lenv, t0 + j, j);
+  }
+  __syncthreads();
+  int done = 0;
+  bool stopped = false;
+  for (uint64_t j = 0; j < cnt; ++j) {
+    const uint64_t t = t0 + j;
+    const uint32_t s = (uint32_t)(j % S);
+    if (done >= max_tiles) {
+      stopped = true;
+      break;
+    }
+    if (tid == 0) {
+      bulk_wait_read<1>();  // the store of tile j-2 has read out buffer (j & 1)
+      if (j + S - 1 < cnt) tma_issue<N, In>(p, src, smem, S, lo, lenv, t + S - 1, j + S - 1);  // tile j-1's stage
+    }
+    __syncthreads();
+    mbar_wait(&full[s], (uint32_t)((j / S) & 1));
+    const TmaMeta m = meta[s];
+    const char* stage = smem + tma_stage_off() + (uint64_t)s * N * kTmaTile * In::kBytes;
+    float* ot = outt + (j & 1) * kTmaTile;
+    const uint32_t off = (uint32_t)tid * 4;
+    if (off < m.cnt) {
+      float acc[4];
+      if (off + 4 <= m.bnd || off >= m.bnd) {
+        tma_fold_vec<N, In>(stage, off, off >= m.bnd ? m.s1 : m.s0, p.contrib, acc);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          acc[i] = tma_fold_one<N, In>(stage, off + i, off + i >= m.bnd ? m.s1 : m.s0, p.contrib);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        nf |= nonfinite_bits(acc[i]) ? 1u : 0u;
+        if (do_scale) acc[i] = __fmul_rn(acc[i], scale);
+      }
+      *reinterpret_cast<float4*>(ot + off) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      for (int d = 0; d < ndst; ++d) bulk_s2g(dsts[d] + m.a, ot, m.cnt * 4u);
+      bulk_commit();
+    }
+    ++done;
+    if (tid == 0 && (done & 63) == 0) ctl->progress = ((uint64_t)blockIdx.x << 32) | (uint64_t)done;
+  }
+  if (tid == 0) {
+    if (stopped) {  // drain the loads still landing in my stages before the CTA exits
+      for (uint64_t j = done; j < cnt && j < (uint64_t)done + S - 1; ++j)
+        mbar_wait(&full[j % S], (uint32_t)((j / S) & 1));
+    }
+    bulk_wait<0>();  // every bulk store performed (peers' outs included)
+    fence_proxy_async_global();
+  }
+  __syncthreads();
+  if (stopped) return -1;
+  if (lenv < len && blockIdx.x == G - 1) {  // ragged tail (< 8 elements): plain loads
+    int s0;
+    uint64_t send;
+    uint64_t cur = lo + lenv;
+    while (cur < hi) {
+      owner_of(cur, p, N, s0, send);
+      const uint64_t end = umin(send, hi);
+      fold_range<N, In, 1>(src, tail_sink, cur, end, s0, p.contrib, false, do_scale, scale, nf);
+      cur = end;
+    }
+  }
+  return done;
+}
+
+// All-gather pull of one member's fp32 slice with the TMA engine: the CTAs
+// split [0, cnt) into contiguous spans; thread 0 streams each span through
+// the smem stages (peer -> shared -> my out).  The < 4-element tail is copied
+// by plain loads.
+__device__ void tma_copy_span(float* dst, const float* src, uint64_t cnt, char* smem, uint32_t S_bytes_stages,
+                              uint32_t tile_bytes, uint32_t& phase_base) {
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  char* stages = smem + tma_stage_off();
+  const uint32_t S = S_bytes_stages;
+  const uint64_t te = tile_bytes / 4;
+  const uint64_t cntv = cnt & ~3ull;
+  const uint64_t ntiles = (cntv + te - 1) / te;
+  const uint64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const uint64_t t0 = umin((uint64_t)blockIdx.x * per, ntiles), t1 = umin(t0 + per, ntiles);
+  if (threadIdx.x == 0) {
+    const uint64_t n = t1 - t0;
+    const uint64_t L = S - 1;
+    for (uint64_t j = 0; j < n + L; ++j) {
+      if (j < n) {
+        const uint64_t g = phase_base + j;  // global sequence through the stage ring
+        const uint32_t s = (uint32_t)(g % S);
+        if (j >= S) bulk_wait_read<0>();
+        const uint64_t a = (t0 + j) * te;
+        const uint32_t bytes = (uint32_t)(umin(te, cntv - a) * 4);
+        mbar_expect_tx(&full[s], bytes);
+        bulk_g2s(stages + (uint64_t)s * tile_bytes, src + a, bytes, &full[s]);
+      }
+      if (j >= L) {
+        const uint64_t jj = j - L;
+        const uint64_t g = phase_base + jj;
+        const uint32_t s = (uint32_t)(g % S);
+        mbar_wait(&full[s], (uint32_t)((g / S) & 1));
+        const uint64_t a = (t0 + jj) * te;
+        const uint32_t bytes = (uint32_t)(umin(te, cntv - a) * 4);
+        bulk_s2g(dst + a, stages + (uint64_t)s * tile_bytes, bytes);
+        bulk_commit();
+      }
+    }
+    bulk_wait_read<0>();
+    phase_base += (uint32_t)n;
+    for (uint64_t e = cntv; e < cnt; ++e)
+      if (blockIdx.x == 0) dst[e] = src[e];
+  }
+}
+
 template <int N, class In>
 __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_constant__ LaunchParams p) {
   using T = typename In::T;
@@ -549,8 +845,8 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
   const uint64_t tag = p.tag;
   const uint64_t E = p.nelems;
   const int tid = threadIdx.x;
-  const uint64_t lo = umin((uint64_t)me * p.slice, E);
-  const uint64_t hi = umin(lo + p.slice, E);
+  uint64_t lo, hi;
+  slice_of(p, me, E, lo, hi);
   // direct: my reduced slice goes straight into `out` (out-of-place calls);
   // res_off then addresses element `lo` of my out inside my arena, so peers
   // pull my slice from there (p.res_off is already that when out is registered)
@@ -568,6 +864,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
 
   __shared__ uint64_t s_pin[N], s_pres[N], s_pout[N];  // CTA 0: entry results, staged for the fan-out
   __shared__ uint32_t s_pushok;
+  extern __shared__ __align__(1024) char dsmem[];  // bulk-copy stages (p.tma_stages > 0)
 
   if (tid == 0) {
     s_status = ST_OK;
@@ -575,6 +872,10 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
     s_nf = 0;
     s_push = 0;
     s_t0 = globaltimer_ns();
+    if (p.tma_stages) {
+      for (uint32_t s = 0; s < p.tma_stages; ++s) mbar_init(reinterpret_cast<uint64_t*>(dsmem) + s, 1);
+      fence_mbar_init();
+    }
   }
   if (blockIdx.x == 0 && tid < 32) {
     // ---- 1a. entry (may overlap the previous call's tail: PDL) ------------
@@ -607,7 +908,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
       // PCIe read, so it runs while the entry flags travel; a stale op that
       // already published is harmless: its tag matches no current peer call,
       // and it poisons itself below.)
-      if (ctl->epoch != tag_gen(tag)) {
+      if (ctl_mismatch(ctl, tag, N, p.contrib, !p.emulated, true)) {
         s_status = ST_PROTOCOL;
         s_blame = me;
       }
@@ -715,12 +1016,40 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
   // ---- 2. reduce-scatter of my slice: one contiguous span per CTA --------
   uint32_t nf = 0;
   int done = 0;
+  // the bulk-copy path runs when every buffer is 16-byte aligned (known only
+  // after the entry records) and the call is not a fused-optimizer one
+  const bool tma = p.tma_stages != 0 && s_vec_ok != 0 && (p.flags & kFlagSGD) == 0 && p.diag == 0;
+  uint32_t gseq = 0;  // thread 0: stage-ring sequence number (mbarrier phases) across RS and AG
   if (s_status == ST_OK) {
     const bool vec_ok = s_vec_ok != 0;
     const bool do_scale = (p.flags & FTAR_F_SCALE) != 0;
     const int max_tiles = (p.fault_member == me) ? p.fault_after_tiles : 0x7fffffff;
     float* const res = const_cast<float*>(s_res[me]) - lo;  // indexed by global element
-    if (p.diag == 1) {
+    if (tma) {
+      __shared__ float* s_dst[kMaxMembers + 1];
+      __shared__ int s_ndst;
+      if (tid == 0) {
+        int nd = 0;
+        if (s_push) {
+          for (int j = 0; j < N; ++j) s_dst[nd++] = s_out[j];
+        } else {
+          s_dst[nd++] = res;
+          if (direct && res != p.out[me]) s_dst[nd++] = p.out[me];
+        }
+        s_ndst = nd;
+      }
+      __syncthreads();
+      if (s_push)
+        done = fold_tiles_tma<N, In>(p, s_src, s_dst, s_ndst, SinkPush<N>{s_out}, lo, hi, do_scale, nf, ctl,
+                                     max_tiles, dsmem);
+      else if (direct && res != p.out[me])
+        done = fold_tiles_tma<N, In>(p, s_src, s_dst, s_ndst, SinkTwo{res, p.out[me]}, lo, hi, do_scale, nf, ctl,
+                                     max_tiles, dsmem);
+      else
+        done = fold_tiles_tma<N, In>(p, s_src, s_dst, s_ndst, SinkOne{res}, lo, hi, do_scale, nf, ctl, max_tiles,
+                                     dsmem);
+      gseq = done > 0 ? (uint32_t)done : 0u;
+    } else if (p.diag == 1) {
       done = fold_tiles<N, In>(p, s_src, SinkNone{res}, lo, hi, vec_ok, do_scale, nf, ctl, max_tiles);
     } else if (p.diag == 2) {
       __shared__ const T* s_loc[N];
@@ -879,13 +1208,19 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         __syncthreads();
         if (s_status != ST_OK) break;
       }
-      const uint64_t klo = umin((uint64_t)k * p.slice, E), khi = umin(klo + p.slice, E);
+      uint64_t klo, khi;
+      slice_of(p, k, E, klo, khi);
+      if (klo >= khi) continue;
       if (p.flags & kFlagSGD)
         pull_sgd<8>(direct ? out + klo : nullptr, s_res[k], SgdRefs{p.sgd_p[me], p.sgd_m[me], p.sgd_po[me], p.sgd_mo[me]}.at(klo),
                     khi - klo, vec_ok, p.sgd_lr, p.sgd_beta);
+      else if (tma)
+        tma_copy_span(out + klo, s_res[k], khi - klo, dsmem, p.tma_stages,
+                      (uint32_t)(N * kTmaTile * In::kBytes), gseq);
       else
         copy_f32<8>(out + klo, s_res[k], khi - klo, vec_ok);
     }
+    if (tma && tid == 0) bulk_wait<0>();  // my out is complete before the arrival below
   }
   __syncthreads();
   if (tid == 0 && blockIdx.x < 256) hdr->dbg_ag_end[blockIdx.x] = globaltimer_ns();
@@ -939,14 +1274,24 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
 
 // ---------------------------------------------------------------- small buckets
 // Push one-shot (input <= kSmallMax bytes): every member posts its whole
-// input into every peer's receive slot [seq parity][sender] and raises
-// sm_in[sender] (with a call fingerprint in sm_meta); then waits for the
-// N-1 peers' flags and folds all N copies LOCALLY in the reference order into
-// the result region, committing to `out` only if every sum is finite.  One
-// flag wait per call instead of entry + reduce-scatter barriers; nobody ever
-// reads a peer's memory, and the parity double buffer makes the receive
-// slots safe to reuse without an entry barrier (a member cannot start call
-// c+2 before every member finished call c+1, hence consumed call c).
+// input into every peer's receive slot [generation parity][seq parity][sender]
+// and raises sm_in[sender] (with a call fingerprint in sm_meta); then waits for
+// the N-1 peers' flags and folds all N copies LOCALLY in the reference order
+// into the result region, committing to `out` only if every sum is finite.
+// One flag wait per call instead of entry + reduce-scatter barriers; nobody
+// ever reads a peer's memory, and the seq-parity double buffer makes the
+// receive slots safe to reuse without an entry barrier (a member cannot start
+// call c+2 before every member finished call c+1, hence consumed call c).
+// The generation parity keeps a zombie of an abandoned generation (a member
+// dropped on timeout that resumes and pushes late, with its old ring index)
+// out of the slots the regrouped ring uses; after the fold every sender's
+// flag and fingerprint are re-read, so a late write that did land in time is
+// reported (PEER_RESET) instead of committed.
+
+__device__ __forceinline__ uint64_t small_slot(uint64_t tag, int sender) {
+  const uint64_t genp = tag_gen(tag) & 1ull, parity = tag & 1ull;
+  return kRecvOff + ((genp * 2 + parity) * kMaxMembers + (uint64_t)sender) * kSmallMax;
+}
 
 template <int N, class In>
 __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __grid_constant__ LaunchParams p) {
@@ -973,22 +1318,32 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
     s_blame = -1;
     s_t0 = globaltimer_ns();
     s_t1 = 0;
+    if (blockIdx.x == 0) {
+      // Epoch fence (a PCIe read, overlapping the previous kernel's tail):
+      // a stale op's pushes carry a tag no current peer call waits for, and
+      // it poisons itself.
+      if (ctl_mismatch(ctl, tag, N, p.contrib, !p.emulated, true)) {
+        s_status = ST_PROTOCOL;
+        s_blame = me;
+      }
+      ctl->started = tag;
+    }
   }
+  // The input may be the output of the previous kernel on this stream (an
+  // in-place chain, or an intra-replica reduce-scatter feeding this call):
+  // griddepcontrol.launch_dependents does not make that kernel's writes
+  // visible, so nothing reads my input before griddepcontrol.wait.
+  pdl_wait();
   __syncthreads();
   const uint64_t fp = call_fingerprint(p, N);
   const bool contributes = (p.contrib >> me) & 1u;
-  // 1. push my input to every peer (grid-stride 16-byte copies).  Under PDL
-  // this overlaps the previous call's tail: it writes only the peers' receive
-  // slots of THIS call's parity (the call before used the other one, and the
-  // call two back finished reading this one before the previous call could
-  // complete), a counter private to this parity, and the peers' arrival words.
+  // 1. push my input to every peer (grid-stride 16-byte copies)
   if (contributes && bytes) {
     const uint64_t stride = (uint64_t)gridDim.x * kThreads;
     const uint64_t first = (uint64_t)blockIdx.x * kThreads + tid;
     for (int jj = 1; jj < N; ++jj) {
       const int j = (me + jj) % N;
-      char* dst = p.base[j] + kRecvOff + (parity * 8 + (uint64_t)me) * kSmallMax;
-      copy_bytes_grid(dst, reinterpret_cast<const char*>(my_in), bytes, first, stride);
+      copy_bytes_grid(p.base[j] + small_slot(tag, me), reinterpret_cast<const char*>(my_in), bytes, first, stride);
     }
   }
   __syncthreads();
@@ -1004,18 +1359,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
         st_relaxed_sys(&reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->sm_in[me], mk_flag(tag, 0));
       s_t1 = globaltimer_ns();
     }
-    if (blockIdx.x == 0) {
-      // Epoch fence (a PCIe read, off the critical path): a stale op's pushes
-      // carry a tag no current peer call waits for, and it poisons itself.
-      if (ctl->epoch != tag_gen(tag)) {
-        s_status = ST_PROTOCOL;
-        s_blame = me;
-      }
-      ctl->started = tag;
-    }
   }
-  // the previous kernel on this stream has completed (no-op without PDL)
-  pdl_wait();
   __syncthreads();
   if (tid == 0 && blockIdx.x == 0) {
     hdr->tph[0] = s_t0;
@@ -1035,8 +1379,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
       }
     }
     for (int j = 0; j < N; ++j)
-      s_src[j] = j == me ? my_in
-                         : reinterpret_cast<const T*>(mybase + kRecvOff + (parity * 8 + (uint64_t)j) * kSmallMax);
+      s_src[j] = j == me ? my_in : reinterpret_cast<const T*>(mybase + small_slot(tag, j));
     if (blockIdx.x == 0) hdr->tph[2] = globaltimer_ns();
   }
   __syncthreads();
@@ -1053,6 +1396,19 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
     g.rs_layout = 1;
     g.rs_ctas = 0;
     fold_tiles<N, In>(g, s_src, SinkOne{res}, 0, E, vec_ok, (p.flags & FTAR_F_SCALE) != 0, nf, ctl, 0x7fffffff);
+  }
+  __syncthreads();
+  if (tid == 0 && s_status == ST_OK) {
+    // every copy I folded must still be the one its sender flagged for this
+    // call: a zombie's late push is followed by its (older) flag
+    for (int jj = 1; jj < N; ++jj) {
+      const int j = (me + jj) % N;
+      if (flag_tag(ld_acquire_sys(&hdr->sm_in[j])) != tag || ld_relaxed_sys(&hdr->sm_meta[j]) != fp) {
+        s_status = ST_PEER_RESET;
+        s_blame = j;
+        break;
+      }
+    }
   }
   if (__any_sync(0xffffffffu, nf != 0) && (tid & 31) == 0) atomicOr(&s_nf, 1u);
   __syncthreads();
@@ -1170,7 +1526,7 @@ __global__ void __launch_bounds__(kThreads, 1) intra_kernel(const __grid_constan
       if (N > 1) fence_acq_rel_sys();
       for (int jj = 1; jj < N; ++jj)
         st_relaxed_sys(&reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->ent_in[me].flag, mk_flag(tag, 0));
-      if (ctl->epoch != tag_gen(tag)) {
+      if (ctl_mismatch(ctl, tag, N, p.contrib, !p.emulated, false)) {
         s_status = ST_PROTOCOL;
         s_blame = me;
       }
@@ -1603,6 +1959,42 @@ __global__ void __launch_bounds__(kThreads) probe_copy_kernel(char* dst, const c
   copy_bytes_grid(dst, src, bytes, first, stride);
 }
 
+// Bulk-copy probe (diagnostic): the same copy moved by the TMA engine, one
+// thread per CTA driving an S-stage pipeline of `tile`-byte bulk loads
+// (global -> shared, mbarrier tx) and bulk stores (shared -> global), one
+// contiguous span per CTA.  src or dst may be a peer address.
+template <int S>
+__global__ void __launch_bounds__(32, 1) probe_bulk_kernel(char* dst, const char* src, uint64_t bytes,
+                                                           uint32_t tile) {
+  extern __shared__ __align__(1024) char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  char* buf = smem + 1024;
+  if (threadIdx.x != 0) return;
+  const uint64_t ntiles = bytes / tile;
+  const uint64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const uint64_t t0 = umin((uint64_t)blockIdx.x * per, ntiles), t1 = umin(t0 + per, ntiles);
+  for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+  fence_mbar_init();
+  const uint64_t cnt = t1 - t0;
+  constexpr uint64_t L = S - 1;  // loads lead stores by S-1 tiles
+  for (uint64_t j = 0; j < cnt + L; ++j) {
+    if (j < cnt) {
+      const int s = (int)(j % S);
+      if (j >= S) bulk_wait_read<0>();  // the store of tile j-S has read slot s
+      mbar_expect_tx(&full[s], tile);
+      bulk_g2s(buf + (uint64_t)s * tile, src + (t0 + j) * tile, tile, &full[s]);
+    }
+    if (j >= L) {
+      const uint64_t t = j - L;
+      const int s = (int)(t % S);
+      mbar_wait(&full[s], (uint32_t)((t / S) & 1));
+      bulk_s2g(dst + (t0 + t) * tile, buf + (uint64_t)s * tile, tile);
+      bulk_commit();
+    }
+  }
+  bulk_wait<0>();
+}
+
 // Access-pattern probe (diagnostic): elements are fp32; a = local, b = remote.
 //  mode 0: c[i] = a[i] + b[i]    (reduce-scatter-like, N = 2)
 //  mode 1: c[i] = b[i]           (all-gather-like)
@@ -1782,6 +2174,15 @@ uint64_t small_bytes() {
 }
 // programmatic dependent launch of the two-shot kernel (FTAR_PDL=0 disables)
 bool pdl_on() { return env_int("FTAR_PDL", 1) != 0; }
+// bulk-copy (TMA) data path for the two-shot kernel (FTAR_TMA=0 disables)
+bool tma_on() { return env_int("FTAR_TMA", 1) != 0; }
+// CTAs of the bulk-copy path: ~128 KB of my slice per CTA, at most
+// FTAR_CTAS_TMA (default 32: tools/tma_probe.py saturates a link with 16-32)
+int tma_ctas(uint64_t slice_bytes) {
+  const int cap = g_ctas > 0 ? g_ctas : env_int("FTAR_CTAS_TMA", 32);
+  const uint64_t per = (uint64_t)env_int("FTAR_TMA_BYTES_PER_CTA", 128 << 10);
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)std::max(cap, 1), (slice_bytes + per - 1) / per));
+}
 int small_ctas(uint64_t bytes) { return (int)std::max<uint64_t>(1, std::min<uint64_t>(16, (bytes + (32u << 10) - 1) >> 15)); }
 int rs_layout() { return env_int("FTAR_RS_LAYOUT", 0); }
 int diag_mode() { return env_int("FTAR_DIAG", 0); }
@@ -1825,6 +2226,7 @@ struct ftar_ctx {
   uint64_t q_tag[kQueue] = {};
   int q_head = 0, q_count = 0;
   char* peer[kMaxSlots] = {};
+  cudaIpcMemHandle_t peer_handle[kMaxSlots] = {};  // what each slot maps (import refuses a different one)
   uint64_t peer_bytes[kMaxSlots] = {};
   bool peer_local[kMaxSlots] = {};  // linked in-process (no IPC handle to close)
   int ring_slots[kMaxMembers] = {};
@@ -1872,6 +2274,7 @@ struct ftar_snap {
   HostCtl* ctl_h = nullptr;
   HostCtl* ctl_d = nullptr;
   char* peer[kMaxSlots] = {};
+  cudaIpcMemHandle_t peer_handle[kMaxSlots] = {};
   uint64_t seq = 0;
   uint64_t cur_tag = 0;
   bool inflight = false;
@@ -1882,9 +2285,21 @@ namespace {
 template <int N, class In>
 cudaError_t launch_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bool coop, bool pdl) {
   auto fn = allreduce_kernel<N, In>;
+  size_t dyn = 0;
+  if (p.tma_stages) {
+    dyn = (size_t)tma_smem_bytes(N, In::kBytes, p.tma_stages);
+    static bool attr_set[64] = {};  // per template instance and device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemMax);
+      if (e != cudaSuccess) return e;
+      if (dev >= 0 && dev < 64) attr_set[dev] = true;
+    }
+  }
   if (coop) {
     void* args[] = {const_cast<LaunchParams*>(&p)};
-    return cudaLaunchCooperativeKernel((const void*)fn, grid, dim3(kThreads), args, 0, st);
+    return cudaLaunchCooperativeKernel((const void*)fn, grid, dim3(kThreads), args, dyn, st);
   }
   if (pdl) {
     // programmatic dependent launch: when the previous kernel on the stream
@@ -1892,7 +2307,7 @@ cudaError_t launch_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bool coo
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = dyn;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1901,7 +2316,7 @@ cudaError_t launch_n(const LaunchParams& p, dim3 grid, cudaStream_t st, bool coo
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, fn, p);
   }
-  fn<<<grid, kThreads, 0, st>>>(p);
+  fn<<<grid, kThreads, dyn, st>>>(p);
   return cudaGetLastError();
 }
 
@@ -2059,6 +2474,17 @@ void fill_geometry(LaunchParams& p, uint64_t E, uint64_t chunk_bytes, int C, int
 
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
+// Workers = the contributors (every member if none): the reduce-scatter
+// slices are split among them only, so a behind replica does no RS work.
+void set_workers(LaunchParams& p, int n, uint64_t E) {
+  const uint32_t all = (n >= 32) ? 0xffffffffu : ((1u << n) - 1u);
+  p.workers = (p.contrib & all) ? (p.contrib & all) : all;
+  const uint64_t h = (uint64_t)__builtin_popcount(p.workers);
+  const uint64_t per = (E + h - 1) / h;
+  p.slice = (per + 7) & ~7ull;
+  if (p.slice == 0) p.slice = 8;
+}
+
 int validate_common(int in_dtype, int n, uint64_t chunk_bytes, int max_in_flight) {
   if (in_dtype != FTAR_DT_F32 && in_dtype != FTAR_DT_BF16)
     return fail(FTAR_ST_INVARIANT, "all-reduce input must be float32 or bfloat16");
@@ -2178,9 +2604,15 @@ int ftar_ctx_import(ftar_ctx* c, int slot, const void* handle, size_t len, uint6
   if (!c || slot < 0 || slot >= kMaxSlots || !handle || len < sizeof(cudaIpcMemHandle_t))
     return fail(FTAR_ST_INVARIANT, "bad import args");
   DeviceGuard g(c->device);
-  if (c->peer[slot]) return FTAR_OK;  // cached mapping
   cudaIpcMemHandle_t h;
   std::memcpy(&h, handle, sizeof(h));
+  if (c->peer[slot]) {
+    // cached mapping of the SAME arena only: a slot still holding another
+    // member's (or a dead incarnation's) arena must be unmapped first, never
+    // silently reused for a different handle
+    if (!c->peer_local[slot] && std::memcmp(&c->peer_handle[slot], &h, sizeof(h)) == 0) return FTAR_OK;
+    return fail(FTAR_ST_INVARIANT, "slot " + std::to_string(slot) + " maps a different arena (unmap it first)");
+  }
   void* p = nullptr;
   cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
   if (e != cudaSuccess) {
@@ -2189,6 +2621,7 @@ int ftar_ctx_import(ftar_ctx* c, int slot, const void* handle, size_t len, uint6
     return FTAR_ST_PEER_DOWN;
   }
   c->peer[slot] = static_cast<char*>(p);
+  c->peer_handle[slot] = h;
   c->peer_bytes[slot] = arena_bytes;
   return FTAR_OK;
 }
@@ -2211,11 +2644,15 @@ int ftar_ctx_link_local(ftar_ctx* c, int slot, ftar_ctx* other) {
 
 int ftar_ctx_unmap(ftar_ctx* c, int slot) {
   if (!c || slot < 0 || slot >= kMaxSlots) return fail(FTAR_ST_INVARIANT, "bad unmap args");
+  for (int i = 0; i < c->n; ++i)
+    if (i != c->self && c->ring_slots[i] == slot)
+      return fail(FTAR_ST_INVARIANT, "slot " + std::to_string(slot) + " belongs to the current ring");
   DeviceGuard g(c->device);
   if (c->peer[slot]) {
     if (!c->peer_local[slot]) cudaIpcCloseMemHandle(c->peer[slot]);
     c->peer[slot] = nullptr;
     c->peer_local[slot] = false;
+    std::memset(&c->peer_handle[slot], 0, sizeof(cudaIpcMemHandle_t));
   }
   return FTAR_OK;
 }
@@ -2365,6 +2802,7 @@ static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, ui
     }
   }
   p.contrib = c->contrib;
+  set_workers(p, c->n, n_elems);
   p.dtype = (uint32_t)in_dtype;
   p.self = c->self;
   p.emulated = 0;
@@ -2386,6 +2824,10 @@ static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, ui
     if (p.flags & kFlagDirect) p.flags |= kFlagSmallDirect;
     p.flags &= ~(kFlagPush | kFlagDirect);
     G = g_ctas > 0 ? g_ctas : small_ctas(in_bytes);
+  } else if (!sgd && c->n >= 2 && tma_on() && p.p_base / (uint64_t)c->n >= kTmaTile) {
+    // every segment spans >= one tile: the bulk-copy data path
+    p.tma_stages = tma_stages_for(c->n, (int)esz);
+    G = tma_ctas(p.slice * esz);
   }
   const dim3 grid(G, 1);
   cudaError_t e = small ? (in_dtype == FTAR_DT_BF16 ? launch_small<BF16In>(c->n, p, grid, st, false, pdl_on())
@@ -2498,6 +2940,7 @@ static int launch_local(ftar_ctx** ctxs, int n, const void* const* ins, int in_d
     }
   }
   p.contrib = contrib_mask & ((1u << n) - 1u);
+  set_workers(p, n, n_elems);
   p.dtype = (uint32_t)in_dtype;
   p.self = 0;
   p.emulated = 1;
@@ -2562,6 +3005,10 @@ static int launch_local(ftar_ctx** ctxs, int n, const void* const* ins, int in_d
       return cuda_fail(e, "local small-bucket cooperative launch");
     }
     return FTAR_OK;
+  }
+  if (!sgd_p && n >= 2 && tma_on() && p.p_base / (uint64_t)n >= kTmaTile) {
+    p.tma_stages = tma_stages_for(n, in_dtype == FTAR_DT_BF16 ? 2 : 4);
+    if (g_local_ctas <= 0) G = std::min(G, tma_ctas(p.slice * (in_dtype == FTAR_DT_BF16 ? 2 : 4)));
   }
   const dim3 grid(G, n);
   cudaError_t e = in_dtype == FTAR_DT_BF16 ? launch_dispatch<BF16In>(n, p, grid, st, true)
@@ -2949,6 +3396,29 @@ int ftar_probe_copy(void* dst, const void* src, uint64_t bytes, int ctas, void* 
   return FTAR_OK;
 }
 
+int ftar_probe_bulk(void* dst, const void* src, uint64_t bytes, int ctas, int tile, int stages, void* stream) {
+  if (tile < 16 || (tile & 15) || stages < 2 || (uint64_t)tile * stages + 1024 > 227 * 1024)
+    return fail(FTAR_ST_INVARIANT, "bad bulk probe shape");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t sm = 1024 + (size_t)tile * stages;
+  const int g = std::max(1, ctas);
+  char* d = static_cast<char*>(dst);
+  const char* s = static_cast<const char*>(src);
+#define BULK_CASE(K)                                                                           \
+  case K:                                                                                      \
+    CK(cudaFuncSetAttribute(probe_bulk_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                            (int)sm));                                                         \
+    probe_bulk_kernel<K><<<g, 32, sm, st>>>(d, s, bytes, (uint32_t)tile);                      \
+    break;
+  switch (stages) {
+    BULK_CASE(2) BULK_CASE(4) BULK_CASE(6) BULK_CASE(8) BULK_CASE(12) BULK_CASE(16)
+    default: return fail(FTAR_ST_INVARIANT, "stages must be 2, 4, 6, 8, 12 or 16");
+  }
+#undef BULK_CASE
+  CK(cudaGetLastError());
+  return FTAR_OK;
+}
+
 int ftar_peer_enable(int device, int peer) {
   DeviceGuard g(device);
   cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
@@ -3092,9 +3562,12 @@ int ftar_snap_import(ftar_snap* s, int slot, const void* handle, size_t len, uin
   if (!s || slot < 0 || slot >= kMaxSlots || !handle || len < sizeof(cudaIpcMemHandle_t))
     return fail(FTAR_ST_INVARIANT, "bad import args");
   DeviceGuard g(s->device);
-  if (s->peer[slot]) return FTAR_OK;
   cudaIpcMemHandle_t h;
   std::memcpy(&h, handle, sizeof(h));
+  if (s->peer[slot]) {
+    if (std::memcmp(&s->peer_handle[slot], &h, sizeof(h)) == 0) return FTAR_OK;
+    return fail(FTAR_ST_INVARIANT, "snapshot slot " + std::to_string(slot) + " maps a different donor (unmap it first)");
+  }
   void* p = nullptr;
   cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
   if (e != cudaSuccess) {
@@ -3103,6 +3576,33 @@ int ftar_snap_import(ftar_snap* s, int slot, const void* handle, size_t len, uin
     return FTAR_ST_PEER_DOWN;
   }
   s->peer[slot] = static_cast<char*>(p);
+  s->peer_handle[slot] = h;
+  return FTAR_OK;
+}
+
+int ftar_snap_unmap(ftar_snap* s, int slot) {
+  if (!s || slot < 0 || slot >= kMaxSlots) return fail(FTAR_ST_INVARIANT, "bad unmap args");
+  if (s->inflight && flag_tag(s->ctl_h->done) != s->cur_tag)
+    return fail(FTAR_ST_INVARIANT, "unmap with a pull in flight");
+  DeviceGuard g(s->device);
+  if (s->peer[slot]) {
+    cudaIpcCloseMemHandle(s->peer[slot]);
+    s->peer[slot] = nullptr;
+    std::memset(&s->peer_handle[slot], 0, sizeof(cudaIpcMemHandle_t));
+  }
+  return FTAR_OK;
+}
+
+int ftar_snap_peer_info(ftar_snap* s, int slot, int64_t* step, uint64_t* pbytes, uint64_t* mbytes) {
+  // the donor's snapshot header read over NVLink (a 32-byte peer copy): what
+  // step it holds (-1: nothing, or a capture in progress) and its lengths
+  if (!s || slot < 0 || slot >= kMaxSlots || !s->peer[slot]) return fail(FTAR_ST_INVARIANT, "donor not mapped");
+  DeviceGuard g(s->device);
+  SnapHdr h;
+  CK(cudaMemcpy(&h, s->peer[slot], 32, cudaMemcpyDefault));
+  if (step) *step = (h.seq & 1u) ? -1 : h.step;
+  if (pbytes) *pbytes = h.pbytes;
+  if (mbytes) *mbytes = h.mbytes;
   return FTAR_OK;
 }
 

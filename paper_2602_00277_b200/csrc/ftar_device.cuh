@@ -24,10 +24,11 @@ constexpr int kMaxMembers = 8;
 constexpr int kThreads = 512;          // one CTA per SM (launch_bounds(512,1))
 constexpr uint64_t kHdrBytes = 64 * 1024;
 // small-bucket push one-shot: receive slots right after the header, at the
-// same offset in every member's arena: [parity][sender] x kSmallMax bytes
+// same offset in every member's arena:
+// [generation parity][call parity][sender] x kSmallMax bytes
 constexpr uint64_t kSmallMax = 1ull << 20;
 constexpr uint64_t kRecvOff = kHdrBytes;
-constexpr uint64_t kRecvBytes = 2 * 8 * kSmallMax;
+constexpr uint64_t kRecvBytes = 2 * 2 * 8 * kSmallMax;
 constexpr uint32_t kBitNonFinite = 1u;
 
 // status codes (mirror include/ftar_b200.h)
@@ -105,6 +106,8 @@ struct alignas(128) ArenaHdr {
 static_assert(sizeof(ArenaHdr) <= kHdrBytes, "header too large");
 
 // Pinned host memory mapped into the device: the control plane's words.
+// epoch, live_mask and contrib_mask are read by every kernel at entry (one
+// 16-byte load, ctl_mismatch): a mismatch with the launch is PROTOCOL.
 struct alignas(64) HostCtl {
   volatile uint64_t epoch;         // host: current generation (quorum.py Decision.generation)
   volatile uint32_t live_mask;     // host: ring members (bit = ring index)
@@ -197,6 +200,82 @@ __device__ __forceinline__ void st_stream(void* p, uint4 v) {
                :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
+// ---- bulk async copies (TMA engine, non-tensor: cp.async.bulk) + mbarriers.
+// Peer (NVLink) addresses are ordinary global addresses to the copy engine:
+// one thread moves a whole tile (peer global -> shared, shared -> peer
+// global), so the SM's threads only fold; the bytes in flight per SM are the
+// pipeline's stages, not its registers.  SASS: UBLKCP / SYNCS.*.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+// Bulk copies always complete (local or peer memory that stays mapped), so
+// this wait is bounded only as a safety net: a copy that never lands is a
+// programming error and traps the kernel instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (uint32_t it = 1;; ++it) {
+    if (mbar_try_wait(bar, parity)) return;
+    if ((it & 1023u) == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 30ull * 1000000000ull) __trap();
+    }
+  }
+}
+// global (local or peer) -> shared; completes `bytes` of tx on `bar`
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// shared -> global (local or peer), tracked by bulk groups
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// at most N committed groups may still be READING shared memory
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// at most N committed groups may still be incomplete (writes not yet performed)
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+// generic-proxy smem writes -> visible to the async proxy (before a bulk store)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// named barrier over `nthreads` threads (the consumer warps of a CTA)
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 __device__ __forceinline__ bool nonfinite_bits(float x) {
   return (__float_as_uint(x) & 0x7f800000u) == 0x7f800000u;
 }
@@ -211,12 +290,34 @@ __device__ __forceinline__ uint2 ld_stream64(const void* p) {
   return r;
 }
 
+// Predicated forms: `on` false issues no load at all (zeros), so a
+// non-contributor's buffer costs no NVLink traffic and needs no branch
+// between the batched loads.
+__device__ __forceinline__ uint4 ld_stream_if(const void* p, bool on) {
+  uint4 r;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n"
+      " mov.b32 %0, 0;\n mov.b32 %1, 0;\n mov.b32 %2, 0;\n mov.b32 %3, 0;\n"
+      " @q ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n}\n"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "r"((int)on));
+  return r;
+}
+__device__ __forceinline__ uint2 ld_stream64_if(const void* p, bool on) {
+  uint2 r;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n mov.b32 %0, 0;\n mov.b32 %1, 0;\n"
+      " @q ld.global.L1::no_allocate.v2.u32 {%0,%1}, [%2];\n}\n"
+      : "=r"(r.x), "=r"(r.y) : "l"(p), "r"((int)on));
+  return r;
+}
+
 struct F32In {
   using T = float;
   using Raw = uint4;
   static constexpr int kBytes = 4;
   __device__ __forceinline__ static float scalar(const float* p, uint64_t e) { return p[e]; }
   __device__ __forceinline__ static Raw load4(const float* p, uint64_t e) { return ld_stream(p + e); }
+  __device__ __forceinline__ static Raw load4_if(const float* p, uint64_t e, bool on) { return ld_stream_if(p + e, on); }
   __device__ __forceinline__ static Raw zero() { return make_uint4(0u, 0u, 0u, 0u); }
   __device__ __forceinline__ static void cvt4(const Raw& r, float (&v)[4]) {
     v[0] = __uint_as_float(r.x); v[1] = __uint_as_float(r.y);
@@ -232,6 +333,9 @@ struct BF16In {
     return up(reinterpret_cast<const uint16_t*>(p)[e]);
   }
   __device__ __forceinline__ static Raw load4(const __nv_bfloat16* p, uint64_t e) { return ld_stream64(p + e); }
+  __device__ __forceinline__ static Raw load4_if(const __nv_bfloat16* p, uint64_t e, bool on) {
+    return ld_stream64_if(p + e, on);
+  }
   __device__ __forceinline__ static Raw zero() { return make_uint2(0u, 0u); }
   __device__ __forceinline__ static void cvt4(const Raw& r, float (&v)[4]) {
     v[0] = __uint_as_float(r.x << 16); v[1] = __uint_as_float(r.x & 0xffff0000u);

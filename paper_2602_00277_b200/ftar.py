@@ -239,7 +239,10 @@ class RingGroup:
         self.max_bucket_bytes = max_bucket_bytes
         self._links_up = False
         self._seq = 0
+        # peer arena mappings by (replica, incarnation); slots come from a
+        # free list and return to it when reconfig unmaps a departed member
         self._slots: dict[tuple[int, int], int] = {}
+        self._free_slots: list[int] = list(range(255, -1, -1))
         self._pool_next = 0
         ptr, nbytes = C.c_uint64(), C.c_uint64()
         _lib.lib.ftar_ctx_pool(ctx, C.byref(ptr), C.byref(nbytes))
@@ -294,8 +297,24 @@ class RingGroup:
     def _slot(self, replica_id: int, incarnation: int) -> int:
         key = (replica_id, incarnation)
         if key not in self._slots:
-            self._slots[key] = len(self._slots) % 256
+            if not self._free_slots:
+                raise Fatal(INTERNAL_INVARIANT, "no free peer-arena slots (256 mapped)")
+            self._slots[key] = self._free_slots.pop()
         return self._slots[key]
+
+    def _release_stale(self, keep: set) -> None:
+        """Unmap every peer arena whose (replica, incarnation) is not in
+        `keep` (the current ring): a departed member or a dead incarnation
+        must not stay pinned in its GPU's memory (close_links, ftar.py:226-230)."""
+        for key in [k for k in self._slots if k not in keep]:
+            slot = self._slots.pop(key)
+            _lib.check(_lib.lib.ftar_ctx_unmap(self._ctx, slot), f"unmap arena of replica {key[0]}")
+            self._free_slots.append(slot)
+
+    @property
+    def mapped_peers(self) -> list[tuple[int, int]]:
+        """(replica, incarnation) of every peer arena currently mapped."""
+        return sorted(self._slots)
 
     def _set_membership(self, infos: dict | None = None) -> None:
         n = self.n
@@ -357,6 +376,9 @@ class RingGroup:
                         self.close_links()
                         _lib.check(rc, f"map arena of replica {m}")
         self._set_membership(infos)
+        if not self._local:
+            keep = {(m, infos[m].incarnation) for m in self.members if m != self.self_replica} if infos else set()
+            self._release_stale(keep)
         self._links_up = True
 
     def close_links(self) -> None:

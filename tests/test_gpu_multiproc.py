@@ -361,6 +361,118 @@ def _worker(rank, world, port, scenario, outdir):
                 and np.array_equal(f2.cpu().numpy(), orc.intra_all_gather(want, bounds, total))
             (res["ok"] if good else res["errors"]).append("intra_queued")
             ir.close()
+        elif scenario == "churn":
+            # 300 kill/rejoin reconfigs of one member (verdict r1 item 6): the
+            # victim drops its ring group (arena freed) and rejoins as a new
+            # incarnation; survivors map the new arena and unmap the dead
+            # one, so the victim GPU's memory stays flat and every call is exact
+            victim = world - 1
+            e = 70_001
+            arrays = member_inputs(world, e, seed=77)
+            want = orc.oracle_reduce(arrays, 8 << 20, 4)
+            group.close()
+            group = ftar.RingGroup(rank, 0, fabric, device=dev, max_bucket_bytes=1 << 20, incarnation=0)
+            free_at, bad, maxmapped = {}, 0, 0
+            for it in range(300):
+                if rank == victim and it > 0:
+                    group.close()
+                    group = ftar.RingGroup(rank, 0, fabric, device=dev, max_bucket_bytes=1 << 20, incarnation=it)
+                group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, it + 1, deadline_s=60)
+                buf = torch.from_numpy(arrays[rank]).to(dev)
+                ftar.ftar_all_reduce(group, buf, it)
+                bad += int(not np.array_equal(buf.cpu().numpy(), want))
+                maxmapped = max(maxmapped, len(group.mapped_peers))
+                if it in (20, 299):
+                    torch.cuda.synchronize()
+                    free_at[it] = torch.cuda.mem_get_info(dev)[0]
+            (res["ok"] if bad == 0 else res["errors"]).append(f"churn_exact:{bad}")
+            (res["ok"] if maxmapped <= world - 1 else res["errors"]).append(f"mapped:{maxmapped}")
+            drift = free_at[20] - free_at[299]
+            res["free_drift_mib"] = drift / 2**20
+            (res["ok"] if drift < (64 << 20) else res["errors"]).append(f"memory_flat:{drift >> 20}MiB")
+        elif scenario == "bench":
+            # bench.py's bucket over NVLink: 64 Mi fp32 per replica, default
+            # geometry, x f32(1/n); registered out-of-place (push all-gather),
+            # registered in place, and ordinary torch tensors (the reference
+            # call shape), three calls queued before the first wait
+            e = 64 << 20
+            group.close()
+            group = ftar.RingGroup(rank, 0, fabric, device=dev, max_bucket_bytes=e * 4, pool_bytes=2 * e * 4 + 4096)
+            group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, 1, deadline_s=60)
+            hosts = [np.random.default_rng((0, r)).standard_normal(e).astype(np.float32) for r in range(world)]
+            want = orc.normalize(orc.oracle_reduce(hosts, 8 << 20, 4), world)
+            cfg = ftar.PipelineConfig(per_chunk_timeout_s=10)
+            x = group.alloc_bucket(e)
+            o = group.alloc_bucket(e)
+            x.copy_(torch.from_numpy(hosts[rank]))
+            pend = [ftar.ftar_all_reduce_async(group, x, k, cfg, out=o, scale=1.0 / world) for k in range(3)]
+            for p_ in pend:
+                p_.wait()
+            (res["ok"] if np.array_equal(o.cpu().numpy(), want) else res["errors"]).append("bench_push")
+            ftar.ftar_all_reduce(group, x, 3, cfg, scale=1.0 / world)
+            (res["ok"] if np.array_equal(x.cpu().numpy(), want) else res["errors"]).append("bench_inplace")
+            u = torch.from_numpy(hosts[rank]).to(dev)
+            uo = torch.empty(e, device=dev)
+            pend = [ftar.ftar_all_reduce_async(group, u, 4 + k, cfg, out=uo, scale=1.0 / world) for k in range(3)]
+            for p_ in pend:
+                p_.wait()
+            (res["ok"] if np.array_equal(uo.cpu().numpy(), want) else res["errors"]).append("bench_unregistered")
+            ftar.ftar_all_reduce(group, u, 7, cfg, scale=1.0 / world)
+            (res["ok"] if np.array_equal(u.cpu().numpy(), want) else res["errors"]).append("bench_unreg_inplace")
+        elif scenario == "fetch":
+            # the reference's fetch_shard(addr, step, rank, replica_id,
+            # incarnation, timeout_s) shape across processes
+            # (tests/test_checkpoint.py:41-95 with tensor buffers)
+            from paper_2602_00277_b200 import checkpoint as ck
+            snap = ck.SnapshotStore(capacity_bytes=16 << 20, device=dev, fabric=fabric, rank=0, replica_id=rank,
+                                    incarnation=1)
+            rec = world - 1
+            donors = list(range(world - 1))
+            params = torch.arange(10, dtype=torch.float32, device=dev)
+            momentum = torch.ones(5, dtype=torch.float32, device=dev)
+            big = torch.randn(3 << 20, device=dev, generator=torch.Generator(device=dev).manual_seed(9))
+            if rank != rec:
+                snap.capture(7, params, momentum)
+                torch.cuda.synchronize()
+            store.set(f"f_captured{rank}", b"1")
+            store.wait([f"f_captured{r}" for r in donors])
+            if rank == rec:
+                got = []
+                for attempt in range(len(donors)):
+                    d = ck.pick_donor(donors + [rec], rec, 0, attempt)
+                    got.append(d)
+                    gp, gm = ck.fetch_shard(ftar.PeerAddress(d), 7, rank=0, replica_id=rec, incarnation=1,
+                                            timeout_s=10)
+                    good = torch.equal(gp.view(torch.float32), params) and torch.equal(gm.view(torch.float32), momentum)
+                    (res["ok"] if good else res["errors"]).append(f"roundtrip_from_{d}")
+                (res["ok"] if sorted(got) == donors else res["errors"]).append("rotation")
+                try:
+                    ck.fetch_shard(ftar.PeerAddress(0), 6, rank=0, replica_id=rec, incarnation=1, timeout_s=10)
+                    res["errors"].append("stale step served")
+                except ck.SnapshotUnavailable as exc:
+                    (res["ok"] if exc.available == 7 else res["errors"]).append("unavailable")
+                try:
+                    ck.fetch_shard(ftar.PeerAddress(99), 1, rank=0, replica_id=rec, incarnation=1, timeout_s=0.4)
+                    res["errors"].append("dead donor served")
+                except errors.Recoverable:
+                    res["ok"].append("dead_donor_recoverable")
+                store.set("f_fetched", b"1")
+                store.wait(["f_recaptured"])
+                try:
+                    ck.fetch_shard(ftar.PeerAddress(0), 7, rank=0, replica_id=rec, incarnation=1, timeout_s=10)
+                    res["errors"].append("overwritten step served")
+                except ck.SnapshotUnavailable as exc:
+                    (res["ok"] if exc.available == 8 else res["errors"]).append("moved_on")
+                gp, gm = ck.fetch_shard(ftar.PeerAddress(0), 8, rank=0, replica_id=rec, incarnation=1, timeout_s=10)
+                (res["ok"] if torch.equal(gp.view(torch.float32), big) else res["errors"]).append("big_shard")
+            elif rank == 0:
+                store.wait(["f_fetched"])
+                snap.capture(8, big, momentum)
+                torch.cuda.synchronize()
+                store.set("f_recaptured", b"1")
+            store.set(f"f_done{rank}", b"1")
+            store.wait([f"f_done{r}" for r in range(world)])
+            snap.close()
         elif scenario == "catchup":
             from paper_2602_00277_b200 import checkpoint as ck
             snap = ck.SnapshotStore(capacity_bytes=64 << 20, device=dev, fabric=fabric, rank=0, replica_id=rank)
@@ -498,6 +610,31 @@ def test_catchup_pull_over_nvlink():
     rec = res[world - 1]
     assert not rec["errors"], rec["errors"]
     assert {"connected", "pull", "striped", "unavailable"} <= set(rec["ok"])
+
+
+def test_kill_rejoin_churn_keeps_memory_flat():
+    """300 kill/rejoin reconfigs of one member: bit-exact every time, at most
+    world-1 peer arenas mapped, and the victim GPU's free memory flat (dead
+    incarnations' arenas are unmapped, so their memory is released)."""
+    res = run("churn", world_size())
+    for r in res:
+        assert not r["errors"], (r["errors"], r.get("free_drift_mib"))
+        assert "churn_exact:0" in r["ok"]
+
+
+def test_bench_workload_over_nvlink():
+    res = run("bench", world_size())
+    for r in res:
+        assert not r["errors"], r["errors"]
+        assert {"bench_push", "bench_inplace", "bench_unregistered", "bench_unreg_inplace"} <= set(r["ok"])
+
+
+def test_reference_shaped_fetch_shard():
+    world = world_size()
+    res = run("fetch", world)
+    rec = res[world - 1]
+    assert not rec["errors"], rec["errors"]
+    assert {"rotation", "unavailable", "dead_donor_recoverable", "moved_on", "big_shard"} <= set(rec["ok"])
 
 
 def _async_worker(rank, world, port, outdir):

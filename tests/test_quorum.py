@@ -191,3 +191,76 @@ def test_store_quorum_vote_outcome_is_shared():
     # a vote that lands after the decider's deadline aborts the step everywhere,
     # including on the late voter itself
     assert _run_threads([voter(0, 3, True, 0), voter(1, 3, True, 0), voter(2, 3, True, 0.8)]) == [False] * 3
+
+
+def _dead_heartbeat(store, prefix, rid):
+    import time
+    store.set(f"{prefix}/hb/{rid}", repr(time.time() - 60.0).encode())
+
+
+def test_store_quorum_outage_round_ends_when_live_reporters_posted():
+    """With heartbeats, a round in which a replica is dead closes as soon as
+    every live replica posted, not at the round deadline."""
+    import time
+
+    from paper_2602_00277_b200.quorum import StoreQuorum
+    master, cl = _stores(3)
+    qs = [StoreQuorum(cl[i], [0, 1, 2], prefix="tl", liveness_s=0.5) for i in range(3)]
+    qs[0].start_heartbeat(0)
+    qs[1].start_heartbeat(1)
+    _dead_heartbeat(cl[2], "tl", 2)
+    t0 = time.monotonic()
+    ds = _run_threads([lambda: qs[0].exchange(1, 0, Report(4, 0), round_deadline_s=20.0),
+                       lambda: qs[1].exchange(1, 1, Report(4, 0), round_deadline_s=20.0)])
+    took = time.monotonic() - t0
+    for q in qs:
+        q.stop_heartbeat()
+    assert ds[0] == ds[1] and ds[0].healthy == (0, 1)
+    assert took < 5.0, took
+
+
+def test_store_quorum_coordinator_failover():
+    """The coordinator (lowest id) is dead: the lowest LIVE replica runs the
+    round, everyone adopts its decision and engine state, and the next round
+    continues the same epoch/generation sequence."""
+    import time
+
+    from paper_2602_00277_b200.quorum import StoreQuorum
+    master, cl = _stores(3)
+    qs = [StoreQuorum(cl[i], [0, 1, 2], prefix="tf", liveness_s=0.5) for i in range(3)]
+    qs[1].start_heartbeat(1)
+    qs[2].start_heartbeat(2)
+    _dead_heartbeat(cl[0], "tf", 0)
+    t0 = time.monotonic()
+    ds = _run_threads([lambda: qs[1].exchange(1, 1, Report(3, 0), round_deadline_s=20.0, decide_timeout_s=30.0),
+                       lambda: qs[2].exchange(1, 2, Report(3, 0), round_deadline_s=20.0, decide_timeout_s=30.0)])
+    assert time.monotonic() - t0 < 5.0
+    assert ds[0] == ds[1] and ds[0].healthy == (1, 2) and ds[0].epoch == 1
+    ds2 = _run_threads([lambda: qs[1].exchange(2, 1, Report(4, 0), round_deadline_s=20.0),
+                        lambda: qs[2].exchange(2, 2, Report(4, 0), round_deadline_s=20.0)])
+    for q in qs:
+        q.stop_heartbeat()
+    assert ds2[0] == ds2[1] and ds2[0].epoch == 2 and ds2[0].generation == ds[0].generation
+    assert qs[2].engine.state() == qs[1].engine.state()
+
+
+def test_store_quorum_vote_decider_failover():
+    """The decision's lowest member died before voting: the next live member
+    decides the outcome (abort: a vote is missing) without waiting out the
+    deadline, and every live voter applies the same outcome."""
+    import time
+
+    from paper_2602_00277_b200.quorum import StoreQuorum
+    master, cl = _stores(3)
+    qs = [StoreQuorum(cl[i], [0, 1, 2], prefix="tvf", liveness_s=0.5) for i in range(3)]
+    qs[1].start_heartbeat(1)
+    qs[2].start_heartbeat(2)
+    _dead_heartbeat(cl[0], "tvf", 0)
+    d = Decision(1, 5, 1, (0, 1, 2), {})
+    t0 = time.monotonic()
+    out = _run_threads([lambda: qs[1].vote(1, d, 1, True, deadline_s=20.0),
+                        lambda: qs[2].vote(1, d, 2, True, deadline_s=20.0)])
+    for q in qs:
+        q.stop_heartbeat()
+    assert out == [False, False]
+    assert time.monotonic() - t0 < 5.0
