@@ -491,14 +491,14 @@ def run_multi(args, rank, world, local_rank):
     dist.barrier()
     nvl = NvlinkBytes(local_rank)
     with ClockSampler(local_rank) as clk:
+        c0 = nvl.read()  # (the counters cover the untimed collective below too: steps + 1 calls)
         # One untimed collective right before the window: it is a device-side
         # barrier, so the timed region starts on every rank when all streams
         # reach the same point, instead of absorbing the ranks' host-side exit
         # skew from dist.barrier() (and the sampler's start) into the first
-        # timed launch (measured: 0.7-1.5 ms vs 0.64 ms steady at 256 MiB, N=4).
+        # timed launch (measured: 0.7-1.5 ms vs 0.64 ms steady at 256 MiB, N=4;
+        # host work between this call and the window would reopen the skew).
         step()
-        drain()
-        c0 = nvl.read()
         total, per_launch = timed_loop(step, args.steps, stream, torch, drain)
         c1 = nvl.read()
     dist.barrier()
@@ -511,7 +511,7 @@ def run_multi(args, rank, world, local_rank):
     dist.all_gather_object(oks, bool(want is not None and got == want and (after is None or after == got)))
     nv_meas = None
     if c0 is not None and c1 is not None:
-        nv_meas = [(b - a) / args.steps for a, b in zip(c0, c1)]
+        nv_meas = [(b - a) / (args.steps + 1) for a, b in zip(c0, c1)]
     all_nv = [None] * n
     dist.all_gather_object(all_nv, nv_meas)
     t_step = total / args.steps

@@ -277,6 +277,10 @@ int ftar_probe_bulk(void* dst, const void* src, uint64_t bytes, int ctas, int ti
 /* %globaltimer stamps of the last call's phases (start, entry passed,
  * reduce-scatter published, all-gather barrier passed, end). */
 int ftar_phase_times(ftar_ctx* ctx, uint64_t* out, int n);
+/* Diagnostic build: CTA 0's bulk-copy pipeline stamps of the last call
+ * ([0,128) refill start, [128,256) refill issued, [256,384) tile landed for
+ * warp 0, [384,512) for warp 1). */
+int ftar_debug_trace(ftar_ctx* ctx, uint64_t* out, int n);
 /* Per-CTA %globaltimer at the end of reduce-scatter / all-gather (last call). */
 int ftar_debug_cta_times(ftar_ctx* ctx, uint64_t* rs_end, uint64_t* ag_end, int n);
 int ftar_peer_enable(int device, int peer);

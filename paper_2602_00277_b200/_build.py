@@ -16,6 +16,10 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libftar_b200.so")
+# timing-diagnostic variant (-DFTAR_DIAGNOSTICS: FTAR_DIAG modes that skip
+# stores or read local data only); built on request for tools, never loaded
+# by the package unless FTAR_LIB_VARIANT=diag
+LIB_DIAG = os.path.join(OUT_DIR, "libftar_b200_diag.so")
 SOURCES = [os.path.join(CSRC, "ftar_b200.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "ftar_device.cuh"),
                   os.path.join(os.path.dirname(PKG), "include", "ftar_b200.h")]
@@ -35,26 +39,27 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found: cannot build libftar_b200.so")
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def up_to_date(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(d) <= t for d in DEPS if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
+def build(force: bool = False, verbose: bool = False, diag: bool = False) -> str:
+    lib = LIB_DIAG if diag else LIB
+    if not force and up_to_date(lib):
+        return lib
     os.makedirs(OUT_DIR, exist_ok=True)
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, *SOURCES]
+    tmp = lib + ".tmp"
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-DFTAR_DIAGNOSTICS"] if diag else []), "-o", tmp, *SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr[-4000:]}")
     if verbose and res.stderr:
         print(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

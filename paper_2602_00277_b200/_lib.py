@@ -82,6 +82,7 @@ SIGNATURES = {
     "ftar_probe_fence": (i32, [vp, vp, vp, u64, i32, i32, vp, i32, vp]),
     "ftar_phase_times": (i32, [c_ctx_p, C.POINTER(u64), i32]),
     "ftar_debug_cta_times": (i32, [c_ctx_p, C.POINTER(u64), C.POINTER(u64), i32]),
+    "ftar_debug_trace": (i32, [c_ctx_p, C.POINTER(u64), i32]),
     "ftar_probe_pattern": (i32, [vp, vp, vp, u64, i32, i32, i32, i32, i32, vp]),
 }
 
@@ -100,7 +101,7 @@ def header_symbols(path: str = _HDR) -> list[str]:
 
 
 def _load() -> C.CDLL:
-    path = _build.LIB
+    path = _build.LIB_DIAG if os.environ.get("FTAR_LIB_VARIANT") == "diag" else _build.LIB
     if not os.path.exists(path):
         raise ImportError(
             f"{path} is missing: build it with paper_2602_00277_b200._build.build() "

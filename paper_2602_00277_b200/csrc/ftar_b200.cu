@@ -126,6 +126,19 @@ __device__ __forceinline__ bool ctl_mismatch(const HostCtl* ctl, uint64_t tag, i
   return check_contrib && (uint32_t)(m >> 32) != contrib;
 }
 
+// Zombie guard for kernels that PUSH data into peers' memory: lane j of warp
+// 0 reads member j's gen_word (installed by its host at reconfig); a peer
+// that has already moved to a newer generation means this call belongs to an
+// abandoned ring (this member was dropped on timeout and is running late), so
+// it must not write anything there.  Returns the mask of such peers.
+__device__ __forceinline__ uint32_t newer_peers(const LaunchParams& p, int n, int me, uint64_t tag) {
+  bool newer = false;
+  const int j = threadIdx.x;
+  if (j < n && j != me)
+    newer = ld_relaxed_sys(&reinterpret_cast<const ArenaHdr*>(p.base[j])->gen_word) > tag_gen(tag);
+  return __ballot_sync(0xffffffffu, newer);
+}
+
 // Member i's reduce-scatter slice.  Only contributors (the workers) reduce:
 // a behind replica (replica.py:574-577) owns no slice, issues no loads and
 // is served by the others; the fold order is set by the segment owner, not
@@ -573,26 +586,50 @@ __device__ __forceinline__ void copy_f32(float* dst, const float* src, uint64_t 
 }
 
 // ---------------------------------------------------------------- bulk-copy (TMA) data path
-// The reduce-scatter with the TMA engine moving every byte.  Per CTA, a ring
-// of S smem stages; stage s holds one tile (kTmaTile elements) of every
-// contributing member's input, landed by cp.async.bulk (peer -> shared) on
-// mbarrier full[s].  Thread 0 keeps S-1 tiles of loads in flight (issued one
-// tile ahead of the fold that frees their stage), so the bytes in flight per
-// SM are ~(S-1) x (N-1) x tile, not a register budget: 16-32 CTAs saturate
-// NVLink where the register-staged loop needed 64-128 (tools/tma_probe.py).
-// All 512 threads fold the tile from shared memory (one 4-element vector
-// each, reference order from the segment owner, fused cast / scale /
-// non-finite vote) into an fp32 out tile, which thread 0 bulk-stores to every
-// destination: the result region, my `out`, and in push mode every peer's
-// `out` (the all-gather fused in: one smem tile, N posted bulk writes).
-// Non-contributors' tiles are never loaded (their +0.0 is folded from a
-// register).  Needs every segment to be >= one tile (at most one owner change
-// per tile) and 16-byte aligned buffers; anything else takes fold_tiles.
-constexpr uint32_t kTmaTile = kThreads * 4;           // elements per tile
+// The reduce-scatter with the TMA engine moving every remote input byte.  Per
+// CTA, a ring of S smem stages; stage s holds one tile (tma_tile(N, in)
+// elements) of every contributing PEER's input, landed by cp.async.bulk
+// (peer -> shared) on mbarrier full[s].  Warp 15 is the producer: its lane 0
+// keeps S-1 tiles of loads in flight, reloading a stage as soon as the 15
+// consumer warps have arrived on its empty[s] mbarrier, so the bytes in
+// flight per SM are ~(S-1) x (N-1) x tile, not a register budget: 16-32 CTAs
+// saturate NVLink where the register-staged loop needed 64-128
+// (tools/tma_probe.py: 47 vs 28 GB/s per CTA).  The producer is a warp of its
+// own because issuing a bulk copy blocks the issuing thread ~0.2 us; folded
+// into a consumer it set the whole CTA's pace (1.3 us per tile,
+// tools/tma_fold_probe.py trace).  The 15 consumer warps fold V 4-element
+// vectors each per tile: this member's own copy is read straight from its
+// buffer (local HBM, prefetched into registers before the tile lands), the
+// peers' from shared memory, in the reference order from the segment owner
+// with the fused cast / scale / non-finite vote, and the result goes from
+// registers by posted 16-byte stores to every destination: the result
+// region, my `out`, and in push mode every peer's `out` (the all-gather fused
+// in; a bulk store to a peer only releases its smem after the remote write).
+// The producer tracks the segment owner incrementally (owner_of's 64-bit
+// divisions only when a tile crosses a segment end).  Non-contributors' tiles
+// are never loaded (their +0.0 is folded from a register).  Needs every
+// segment to be >= one tile (at most one owner change per tile) and 16-byte
+// aligned buffers; anything else takes fold_tiles.
 constexpr uint32_t kTmaMetaBytes = 1024;              // mbarriers + per-stage tile metadata
 // dynamic smem per CTA (1 CTA / SM): 227 KB less room for the kernel's
 // static shared variables and the 1 KB alignment of the dynamic window
 constexpr uint32_t kTmaSmemMax = 227 * 1024 - 2048;
+constexpr uint32_t kTmaMaxStages = 16;
+constexpr uint32_t kTmaConsumers = kThreads - 32;     // warps 0..14 fold, warp 15 produces
+constexpr int kTmaProducer = kThreads - 32;           // thread that issues the bulk copies
+
+// vectors per consumer thread per tile: ~24 KB of peer data per stage, so
+// that >= 8 stages (>= 8 bulk copies) are in flight per SM where the ring is
+// small — one copy lands at ~10 GB/s and an SM's copy engine needs several
+// in flight to reach its ~47 GB/s (tools/tma_probe.py, tma_fold_probe.py)
+__host__ __device__ constexpr uint32_t tma_vecs(int n, int in_bytes) {
+  const uint32_t per_vec = (uint32_t)(n > 1 ? n - 1 : 1) * kTmaConsumers * 4u * (uint32_t)in_bytes;
+  const uint32_t v = 24576u / per_vec;
+  return v < 1 ? 1u : (v > 4 ? 4u : v);
+}
+__host__ __device__ constexpr uint32_t tma_tile(int n, int in_bytes) {
+  return kTmaConsumers * 4u * tma_vecs(n, in_bytes);
+}
 
 struct TmaMeta {            // what the producer recorded for the tile in a stage
   uint64_t a;               // first element (call-local)
@@ -600,79 +637,95 @@ struct TmaMeta {            // what the producer recorded for the tile in a stag
   int s0, s1;               // owner of [a, bnd) and of [bnd, a + cnt)
   uint32_t bnd;             // boundary offset within the tile (>= cnt: none)
 };
+// smem map: [0,128) full[16] | [128,256) empty[16] | [256,640) meta[16] | stages
+__device__ __forceinline__ uint64_t* tma_full(char* smem) { return reinterpret_cast<uint64_t*>(smem); }
+__device__ __forceinline__ uint64_t* tma_empty(char* smem) { return reinterpret_cast<uint64_t*>(smem + 128); }
+__device__ __forceinline__ TmaMeta* tma_meta(char* smem) { return reinterpret_cast<TmaMeta*>(smem + 256); }
 
-__host__ __device__ __forceinline__ uint64_t tma_out_off() { return kTmaMetaBytes; }
-__host__ __device__ __forceinline__ uint64_t tma_stage_off() { return kTmaMetaBytes + 2ull * kTmaTile * 4; }
+__host__ __device__ __forceinline__ uint64_t tma_stage_off() { return kTmaMetaBytes; }
+// one stage = a tile of every PEER's input (this member's own copy is read
+// from global memory): peer k sits in slot k - (k > me)
+__host__ __device__ __forceinline__ uint64_t tma_stage_bytes(int n, int in_bytes) {
+  return (uint64_t)(n > 1 ? n - 1 : 1) * tma_tile(n, in_bytes) * (uint64_t)in_bytes;
+}
+__device__ __forceinline__ uint32_t tma_slot(int k, int me) { return (uint32_t)(k - (k > me ? 1 : 0)); }
 __host__ __device__ __forceinline__ uint32_t tma_stages_for(int n, int in_bytes) {
-  const uint64_t stage = (uint64_t)n * kTmaTile * (uint64_t)in_bytes;
-  const uint64_t s = (kTmaSmemMax - tma_stage_off()) / stage;
-  return (uint32_t)(s > 16 ? 16 : s);
+  const uint64_t s = (kTmaSmemMax - tma_stage_off()) / tma_stage_bytes(n, in_bytes);
+  return (uint32_t)(s > kTmaMaxStages ? kTmaMaxStages : s);
 }
 __host__ __device__ __forceinline__ uint64_t tma_smem_bytes(int n, int in_bytes, uint32_t stages) {
-  return tma_stage_off() + (uint64_t)stages * n * kTmaTile * (uint64_t)in_bytes;
+  return tma_stage_off() + (uint64_t)stages * tma_stage_bytes(n, in_bytes);
 }
 
-// Issue the bulk loads of tile t (elements [lo + t*TE, ...)) into stage s.
+// The producer's cached owner run [sbeg, send) -> owner (fold_tiles does the same).
+struct OwnerRun {
+  uint64_t sbeg = 1, send = 0;
+  int owner = 0;
+};
+
+// Issue the bulk loads of the tile at element `a` (cnt elements) into stage
+// j % S (j = the CTA-local sequence number, which also sets the phases).
 template <int N, class In>
-__device__ __forceinline__ void tma_issue(const LaunchParams& p, const typename In::T* const* src, char* smem,
-                                          uint32_t S, uint64_t lo, uint64_t lenv, uint64_t t, uint64_t j) {
-  // stage (and mbarrier phase) by the CTA-local sequence number j
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  TmaMeta* meta = reinterpret_cast<TmaMeta*>(smem + 256);
+__device__ __forceinline__ void tma_issue(const LaunchParams& p, const typename In::T* const* src, int me, char* smem,
+                                          uint32_t S, uint64_t a, uint32_t cnt, uint64_t j, OwnerRun& run) {
+  constexpr uint32_t TE = tma_tile(N, In::kBytes);
+  uint64_t* full = tma_full(smem);
+  TmaMeta* meta = tma_meta(smem);
   const uint32_t s = (uint32_t)(j % S);
-  const uint64_t a = lo + t * kTmaTile;
-  const uint32_t cnt = (uint32_t)umin(kTmaTile, lo + lenv - a);
-  int s0;
-  uint64_t send;
-  owner_of(a, p, N, s0, send);
+  if (a < run.sbeg || a >= run.send) {
+    owner_of(a, p, N, run.owner, run.send);
+    run.sbeg = a;
+  }
   TmaMeta m;
   m.a = a;
   m.cnt = cnt;
-  m.s0 = s0;
-  m.s1 = s0;
+  m.s0 = run.owner;
+  m.s1 = run.owner;
   m.bnd = 0xffffffffu;
-  if (send < a + cnt) {  // one owner change inside the tile (segments >= a tile)
-    uint64_t send2;
-    owner_of(send, p, N, m.s1, send2);
-    m.bnd = (uint32_t)(send - a);
+  if (run.send < a + cnt) {  // one owner change inside the tile (segments >= a tile)
+    const uint64_t b = run.send;
+    owner_of(b, p, N, run.owner, run.send);
+    run.sbeg = b;
+    m.s1 = run.owner;
+    m.bnd = (uint32_t)(b - a);
   }
   meta[s] = m;
   const uint32_t bytes = cnt * (uint32_t)In::kBytes;
-  const uint32_t nsrc = __popc(p.contrib & ((1u << N) - 1u));
-  char* stage = smem + tma_stage_off() + (uint64_t)s * N * kTmaTile * In::kBytes;
-  if (nsrc == 0) {
+  const uint32_t peers = p.contrib & ((1u << N) - 1u) & ~(1u << me);
+  char* stage = smem + tma_stage_off() + (uint64_t)s * tma_stage_bytes(N, In::kBytes);
+  if (peers == 0) {
     mbar_arrive(&full[s]);
     return;
   }
-  mbar_expect_tx(&full[s], bytes * nsrc);
+  mbar_expect_tx(&full[s], bytes * (uint32_t)__popc(peers));
 #pragma unroll
-  for (int j = 0; j < N; ++j)
-    if ((p.contrib >> j) & 1u) bulk_g2s(stage + (uint64_t)j * kTmaTile * In::kBytes, src[j] + a, bytes, &full[s]);
+  for (int k = 0; k < N; ++k)
+    if ((peers >> k) & 1u) bulk_g2s(stage + (uint64_t)tma_slot(k, me) * TE * In::kBytes, src[k] + a, bytes, &full[s]);
 }
 
-// Fold one 4-element vector (elements e..e+3 of the tile at offset `off`)
-// whose fold starts at ring index `own`, reading every contributor's copy
-// from the stage.
+// Fold one 4-element vector (elements off..off+3 of the tile) whose fold
+// starts at ring index `own`: member `me`'s copy from registers (`mine`),
+// every other contributor's from the stage.
 template <int N, class In>
-__device__ __forceinline__ void tma_fold_vec(const char* stage, uint32_t off, int own, uint32_t contrib,
-                                             float (&acc)[4]) {
+__device__ __forceinline__ void tma_fold_vec(const char* stage, uint32_t off, int own, int me, uint32_t contrib,
+                                             const typename In::Raw& mine, float (&acc)[4]) {
   using Raw = typename In::Raw;
-  bool first = true;
+  constexpr uint32_t TE = tma_tile(N, In::kBytes);
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     int m = own + k;
     if (m >= N) m -= N;
     float x[4];
-    if ((contrib >> m) & 1u) {
-      const Raw r = *reinterpret_cast<const Raw*>(stage + ((uint64_t)m * kTmaTile + off) * In::kBytes);
-      In::cvt4(r, x);
-    } else {
+    if (!((contrib >> m) & 1u)) {
       x[0] = x[1] = x[2] = x[3] = 0.0f;
+    } else if (m == me) {
+      In::cvt4(mine, x);
+    } else {
+      In::cvt4(*reinterpret_cast<const Raw*>(stage + ((uint64_t)tma_slot(m, me) * TE + off) * In::kBytes), x);
     }
-    if (first) {
+    if (k == 0) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[i] = x[i];
-      first = false;
     } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], x[i]);
@@ -680,7 +733,9 @@ __device__ __forceinline__ void tma_fold_vec(const char* stage, uint32_t off, in
   }
 }
 template <int N, class In>
-__device__ __forceinline__ float tma_fold_one(const char* stage, uint32_t off, int own, uint32_t contrib) {
+__device__ __forceinline__ float tma_fold_one(const char* stage, uint32_t off, int own, int me, uint32_t contrib,
+                                              const typename In::T* mine_g, uint64_t e) {
+  constexpr uint32_t TE = tma_tile(N, In::kBytes);
   float acc = 0.0f;
 #pragma unroll
   for (int k = 0; k < N; ++k) {
@@ -688,106 +743,144 @@ __device__ __forceinline__ float tma_fold_one(const char* stage, uint32_t off, i
     if (m >= N) m -= N;
     float x = 0.0f;
     if ((contrib >> m) & 1u) {
-      if (In::kBytes == 4) x = *reinterpret_cast<const float*>(stage + ((uint64_t)m * kTmaTile + off) * 4);
-      else x = __uint_as_float((uint32_t)*reinterpret_cast<const uint16_t*>(stage + ((uint64_t)m * kTmaTile + off) * 2) << 16);
+      const uint64_t at = (uint64_t)tma_slot(m, me) * TE + off;
+      if (m == me) x = In::scalar(mine_g, e);
+      else if (In::kBytes == 4) x = *reinterpret_cast<const float*>(stage + at * 4);
+      else x = __uint_as_float((uint32_t)*reinterpret_cast<const uint16_t*>(stage + at * 2) << 16);
     }
     acc = k == 0 ? x : __fadd_rn(acc, x);
   }
   return acc;
 }
 
-// Reduce my slice [lo, hi) through the bulk-copy pipeline; results bulk-stored
-// to dsts[0..ndst) (each indexed by call-local element).  The < 8-element
-// ragged tail of the slice is folded by the last CTA with fold_range into
-// `tail_sink`.  Returns tiles done, or -1 when the fault hook stopped it.
+// Reduce my slice [lo, hi) through the bulk-copy pipeline; every result
+// vector goes to `sink` (put4 / put1 by call-local element).  The < 8-element
+// ragged tail of the slice is folded by the last CTA with fold_range.
+// Returns tiles done, or -1 when the fault hook stopped it.
 template <int N, class In, class Sink>
-__device__ int fold_tiles_tma(const LaunchParams& p, const typename In::T* const* src, float* const* dsts, int ndst,
-                              const Sink& tail_sink, uint64_t lo, uint64_t hi, bool do_scale, uint32_t& nf,
-                              HostCtl* ctl, int max_tiles, char* smem) {
+__device__ int fold_tiles_tma(const LaunchParams& p, const typename In::T* const* src, int me, const Sink& sink,
+                              uint64_t lo, uint64_t hi, bool do_scale, uint32_t& nf, HostCtl* ctl, int max_tiles,
+                              char* smem) {
+  using Raw = typename In::Raw;
+  constexpr uint32_t TE = tma_tile(N, In::kBytes);
+  constexpr uint32_t V = tma_vecs(N, In::kBytes);
   const int tid = threadIdx.x;
   const uint32_t S = p.tma_stages;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  const TmaMeta* meta = reinterpret_cast<const TmaMeta*>(smem + 256);
-  float* const outt = reinterpret_cast<float*>(smem + tma_out_off());
+  uint64_t* full = tma_full(smem);
+  uint64_t* empty = tma_empty(smem);
+  const TmaMeta* meta = tma_meta(smem);
   const uint64_t G = (p.rs_ctas > 0 && p.rs_ctas < (int)gridDim.x) ? (uint64_t)p.rs_ctas : gridDim.x;
   if (blockIdx.x >= G) return 0;
   const uint64_t len = hi > lo ? hi - lo : 0;
   const uint64_t lenv = len & ~7ull;  // bulk-copied part (16-byte granules for bf16 and fp32)
-  const uint64_t ntiles = (lenv + kTmaTile - 1) / kTmaTile;
+  const uint64_t ntiles = (lenv + TE - 1) / TE;
   const uint64_t per = (ntiles + G - 1) / G;
   const uint64_t t0 = umin(blockIdx.x * per, ntiles), t1 = umin(t0 + per, ntiles);
   const uint64_t cnt = t1 - t0;
   const float scale = p.scale;
-  if (tid == 0) {  // (the kernel initialised the mbarriers at entry)
-    for (uint64_t j = 0; j + 1 < S && j < cnt; ++j) tma_issue<N, In>(p, src, smem, S, lo, lenv, t0 + j, j);
-  }
-  __syncthreads();
-  int done = 0;
-  bool stopped = false;
-  for (uint64_t j = 0; j < cnt; ++j) {
-    const uint64_t t = t0 + j;
-    const uint32_t s = (uint32_t)(j % S);
-    if (done >= max_tiles) {
-      stopped = true;
-      break;
-    }
-    if (tid == 0) {
-      bulk_wait_read<1>();  // the store of tile j-2 has read out buffer (j & 1)
-      if (j + S - 1 < cnt) tma_issue<N, In>(p, src, smem, S, lo, lenv, t + S - 1, j + S - 1);  // tile j-1's stage
-    }
-    __syncthreads();
-    mbar_wait(&full[s], (uint32_t)((j / S) & 1));
-    const TmaMeta m = meta[s];
-    const char* stage = smem + tma_stage_off() + (uint64_t)s * N * kTmaTile * In::kBytes;
-    float* ot = outt + (j & 1) * kTmaTile;
-    const uint32_t off = (uint32_t)tid * 4;
-    if (off < m.cnt) {
-      float acc[4];
-      if (off + 4 <= m.bnd || off >= m.bnd) {
-        tma_fold_vec<N, In>(stage, off, off >= m.bnd ? m.s1 : m.s0, p.contrib, acc);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          acc[i] = tma_fold_one<N, In>(stage, off + i, off + i >= m.bnd ? m.s1 : m.s0, p.contrib);
+  const uint64_t run = umin(cnt, (uint64_t)(max_tiles < 0 ? 0 : max_tiles));  // the fault hook stops early
+  const uint64_t end = lo + lenv;
+  const bool i_contribute = (p.contrib >> me) & 1u;
+  const typename In::T* const mine_g = src[me];
+#ifdef FTAR_DIAGNOSTICS
+  uint64_t* trace = (p.diag >= 3 && blockIdx.x == 0 && (p.emulated == 0 || blockIdx.y == 0))
+                        ? reinterpret_cast<ArenaHdr*>(p.base[p.emulated ? blockIdx.y : p.self])->dbg_trace
+                        : nullptr;
+#endif
+  if (tid >= (int)kTmaConsumers) {
+    // ---- producer warp (the kernel initialised the mbarriers at entry)
+    if (tid == kTmaProducer) {
+      OwnerRun orun;
+      for (uint64_t j = 0; j < run; ++j) {
+        if (j >= S) mbar_wait(&empty[j % S], (uint32_t)(((j / S) - 1) & 1));  // tile j-S left the stage
+#ifdef FTAR_DIAGNOSTICS
+        if (trace && j < 128) trace[j] = globaltimer_ns();
+#endif
+        const uint64_t a = lo + (t0 + j) * TE;
+        tma_issue<N, In>(p, src, me, smem, S, a, (uint32_t)umin(TE, end - a), j, orun);
+#ifdef FTAR_DIAGNOSTICS
+        if (trace && j < 128) trace[128 + j] = globaltimer_ns();
+#endif
       }
+    }
+  } else {
+    // ---- consumer warps
+    for (uint64_t j = 0; j < run; ++j) {
+      const uint32_t s = (uint32_t)(j % S);
+      // this member's own copy: local HBM, loaded before the tile lands
+      const uint64_t a = lo + (t0 + j) * TE;
+      const uint32_t tcnt = (uint32_t)umin(TE, end - a);
+      Raw mine[V];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        nf |= nonfinite_bits(acc[i]) ? 1u : 0u;
-        if (do_scale) acc[i] = __fmul_rn(acc[i], scale);
+      for (uint32_t v = 0; v < V; ++v) {
+        const uint32_t off = (v * kTmaConsumers + (uint32_t)tid) * 4;
+        mine[v] = In::load4_if(mine_g, a + (off < tcnt ? off : 0), i_contribute);
       }
-      *reinterpret_cast<float4*>(ot + off) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      mbar_wait(&full[s], (uint32_t)((j / S) & 1));
+#ifdef FTAR_DIAGNOSTICS
+      if (trace && tid == 0 && j < 128) trace[256 + j] = globaltimer_ns();
+      if (trace && tid == 32 && j < 128) trace[384 + j] = globaltimer_ns();
+#endif
+      const TmaMeta m = meta[s];
+      const char* stage = smem + tma_stage_off() + (uint64_t)s * tma_stage_bytes(N, In::kBytes);
+      float acc[V][4];
+#pragma unroll
+      for (uint32_t v = 0; v < V; ++v) {
+        const uint32_t off = (v * kTmaConsumers + (uint32_t)tid) * 4;
+        acc[v][0] = acc[v][1] = acc[v][2] = acc[v][3] = 0.f;
+#ifdef FTAR_DIAGNOSTICS
+        if (off < m.cnt && p.diag != 4) {  // diag 4: loads only
+#else
+        if (off < m.cnt) {
+#endif
+          if (off + 4 <= m.bnd || off >= m.bnd) {
+            tma_fold_vec<N, In>(stage, off, off >= m.bnd ? m.s1 : m.s0, me, p.contrib, mine[v], acc[v]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              acc[v][i] = tma_fold_one<N, In>(stage, off + i, off + i >= m.bnd ? m.s1 : m.s0, me, p.contrib,
+                                              mine_g, m.a + off + i);
+          }
+        }
+      }
+      // this warp is done with the stage: let the producer reload it
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+      for (uint32_t v = 0; v < V; ++v) {
+        const uint32_t off = (v * kTmaConsumers + (uint32_t)tid) * 4;
+        if (off < m.cnt) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            nf |= nonfinite_bits(acc[v][i]) ? 1u : 0u;
+            if (do_scale) acc[v][i] = __fmul_rn(acc[v][i], scale);
+          }
+#ifdef FTAR_DIAGNOSTICS
+          if (p.diag != 3)  // diag 3: no stores
+#endif
+            sink.put4(m.a + off, make_uint4(__float_as_uint(acc[v][0]), __float_as_uint(acc[v][1]),
+                                            __float_as_uint(acc[v][2]), __float_as_uint(acc[v][3])));
+        }
+      }
+      if (tid == 0 && ((j + 1) & 63) == 0) ctl->progress = ((uint64_t)blockIdx.x << 32) | (uint64_t)(j + 1);
     }
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      for (int d = 0; d < ndst; ++d) bulk_s2g(dsts[d] + m.a, ot, m.cnt * 4u);
-      bulk_commit();
-    }
-    ++done;
-    if (tid == 0 && (done & 63) == 0) ctl->progress = ((uint64_t)blockIdx.x << 32) | (uint64_t)done;
   }
-  if (tid == 0) {
-    if (stopped) {  // drain the loads still landing in my stages before the CTA exits
-      for (uint64_t j = done; j < cnt && j < (uint64_t)done + S - 1; ++j)
-        mbar_wait(&full[j % S], (uint32_t)((j / S) & 1));
-    }
-    bulk_wait<0>();  // every bulk store performed (peers' outs included)
-    fence_proxy_async_global();
-  }
+  // every stage is consumed (the all-gather copies reuse the ring with the
+  // sequence continuing at `run`)
   __syncthreads();
-  if (stopped) return -1;
+  if (run < cnt) return -1;
   if (lenv < len && blockIdx.x == G - 1) {  // ragged tail (< 8 elements): plain loads
     int s0;
     uint64_t send;
     uint64_t cur = lo + lenv;
     while (cur < hi) {
       owner_of(cur, p, N, s0, send);
-      const uint64_t end = umin(send, hi);
-      fold_range<N, In, 1>(src, tail_sink, cur, end, s0, p.contrib, false, do_scale, scale, nf);
-      cur = end;
+      const uint64_t e2 = umin(send, hi);
+      fold_range<N, In, 1>(src, sink, cur, e2, s0, p.contrib, false, do_scale, scale, nf);
+      cur = e2;
     }
   }
-  return done;
+  return (int)cnt;
 }
 
 // All-gather pull of one member's fp32 slice with the TMA engine: the CTAs
@@ -796,7 +889,7 @@ __device__ int fold_tiles_tma(const LaunchParams& p, const typename In::T* const
 // by plain loads.
 __device__ void tma_copy_span(float* dst, const float* src, uint64_t cnt, char* smem, uint32_t S_bytes_stages,
                               uint32_t tile_bytes, uint32_t& phase_base) {
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* full = tma_full(smem);
   char* stages = smem + tma_stage_off();
   const uint32_t S = S_bytes_stages;
   const uint64_t te = tile_bytes / 4;
@@ -864,6 +957,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
 
   __shared__ uint64_t s_pin[N], s_pres[N], s_pout[N];  // CTA 0: entry results, staged for the fan-out
   __shared__ uint32_t s_pushok;
+  __shared__ uint32_t s_newer;
   extern __shared__ __align__(1024) char dsmem[];  // bulk-copy stages (p.tma_stages > 0)
 
   if (tid == 0) {
@@ -873,9 +967,19 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
     s_push = 0;
     s_t0 = globaltimer_ns();
     if (p.tma_stages) {
-      for (uint32_t s = 0; s < p.tma_stages; ++s) mbar_init(reinterpret_cast<uint64_t*>(dsmem) + s, 1);
+      for (uint32_t s = 0; s < p.tma_stages; ++s) {
+        mbar_init(tma_full(dsmem) + s, 1);
+        mbar_init(tma_empty(dsmem) + s, kTmaConsumers / 32);
+      }
       fence_mbar_init();
     }
+  }
+  if (tid < 32 && !p.emulated && (p.flags & kFlagPush)) {
+    // push mode writes into peers' outputs: never from an abandoned generation
+    const uint32_t m = newer_peers(p, N, me, tag);
+    if (tid == 0) s_newer = m;
+  } else if (tid == 0) {
+    s_newer = 0;
   }
   if (blockIdx.x == 0 && tid < 32) {
     // ---- 1a. entry (may overlap the previous call's tail: PDL) ------------
@@ -1013,12 +1117,17 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
   }
   __syncthreads();
 
+  if (tid == 0 && s_newer && s_status == ST_OK) {  // I am a zombie of an older ring: push nothing
+    s_status = ST_PEER_RESET;
+    s_blame = __ffs(s_newer) - 1;
+  }
+  __syncthreads();
   // ---- 2. reduce-scatter of my slice: one contiguous span per CTA --------
   uint32_t nf = 0;
   int done = 0;
   // the bulk-copy path runs when every buffer is 16-byte aligned (known only
   // after the entry records) and the call is not a fused-optimizer one
-  const bool tma = p.tma_stages != 0 && s_vec_ok != 0 && (p.flags & kFlagSGD) == 0 && p.diag == 0;
+  const bool tma = p.tma_stages != 0 && s_vec_ok != 0 && (p.flags & kFlagSGD) == 0 && (p.diag == 0 || p.diag >= 3);
   uint32_t gseq = 0;  // thread 0: stage-ring sequence number (mbarrier phases) across RS and AG
   if (s_status == ST_OK) {
     const bool vec_ok = s_vec_ok != 0;
@@ -1026,29 +1135,16 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
     const int max_tiles = (p.fault_member == me) ? p.fault_after_tiles : 0x7fffffff;
     float* const res = const_cast<float*>(s_res[me]) - lo;  // indexed by global element
     if (tma) {
-      __shared__ float* s_dst[kMaxMembers + 1];
-      __shared__ int s_ndst;
-      if (tid == 0) {
-        int nd = 0;
-        if (s_push) {
-          for (int j = 0; j < N; ++j) s_dst[nd++] = s_out[j];
-        } else {
-          s_dst[nd++] = res;
-          if (direct && res != p.out[me]) s_dst[nd++] = p.out[me];
-        }
-        s_ndst = nd;
-      }
-      __syncthreads();
       if (s_push)
-        done = fold_tiles_tma<N, In>(p, s_src, s_dst, s_ndst, SinkPush<N>{s_out}, lo, hi, do_scale, nf, ctl,
-                                     max_tiles, dsmem);
+        done = fold_tiles_tma<N, In>(p, s_src, me, SinkPush<N>{s_out}, lo, hi, do_scale, nf, ctl, max_tiles, dsmem);
       else if (direct && res != p.out[me])
-        done = fold_tiles_tma<N, In>(p, s_src, s_dst, s_ndst, SinkTwo{res, p.out[me]}, lo, hi, do_scale, nf, ctl,
-                                     max_tiles, dsmem);
+        done = fold_tiles_tma<N, In>(p, s_src, me, SinkTwo{res, p.out[me]}, lo, hi, do_scale, nf, ctl, max_tiles, dsmem);
       else
-        done = fold_tiles_tma<N, In>(p, s_src, s_dst, s_ndst, SinkOne{res}, lo, hi, do_scale, nf, ctl, max_tiles,
-                                     dsmem);
+        done = fold_tiles_tma<N, In>(p, s_src, me, SinkOne{res}, lo, hi, do_scale, nf, ctl, max_tiles, dsmem);
       gseq = done > 0 ? (uint32_t)done : 0u;
+#ifdef FTAR_DIAGNOSTICS
+      // timing diagnostics that change results (the diagnostic library
+      // variant only, built by _build.build(diag=True); never the product)
     } else if (p.diag == 1) {
       done = fold_tiles<N, In>(p, s_src, SinkNone{res}, lo, hi, vec_ok, do_scale, nf, ctl, max_tiles);
     } else if (p.diag == 2) {
@@ -1056,6 +1152,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
       if (tid < N) s_loc[tid] = s_src[me];
       __syncthreads();
       done = fold_tiles<N, In>(p, s_loc, SinkOne{res}, lo, hi, vec_ok, do_scale, nf, ctl, max_tiles);
+#endif
     } else if (p.flags & kFlagSGD) {
       done = fold_tiles<N, In>(p, s_src,
                                SinkSGD{res, direct ? p.out[me] : nullptr, SgdRefs{p.sgd_p[me], p.sgd_m[me], p.sgd_po[me], p.sgd_mo[me]},
@@ -1216,7 +1313,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
                     khi - klo, vec_ok, p.sgd_lr, p.sgd_beta);
       else if (tma)
         tma_copy_span(out + klo, s_res[k], khi - klo, dsmem, p.tma_stages,
-                      (uint32_t)(N * kTmaTile * In::kBytes), gseq);
+                      (uint32_t)tma_stage_bytes(N, In::kBytes), gseq);
       else
         copy_f32<8>(out + klo, s_res[k], khi - klo, vec_ok);
     }
@@ -1312,10 +1409,17 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
   __shared__ int s_blame;
   __shared__ uint64_t s_t0;
   __shared__ uint64_t s_t1;
+  if (tid < 32) {
+    // zombie guard (remote reads, overlapping the previous kernel's tail):
+    // a member dropped from the ring must not push into the regrouped one
+    const uint32_t newer = p.emulated ? 0u : newer_peers(p, N, me, tag);
+    if (tid == 0) {
+      s_status = newer ? ST_PEER_RESET : ST_OK;
+      s_blame = newer ? __ffs(newer) - 1 : -1;
+    }
+  }
   if (tid == 0) {
-    s_status = ST_OK;
     s_nf = 0;
-    s_blame = -1;
     s_t0 = globaltimer_ns();
     s_t1 = 0;
     if (blockIdx.x == 0) {
@@ -1338,7 +1442,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
   const uint64_t fp = call_fingerprint(p, N);
   const bool contributes = (p.contrib >> me) & 1u;
   // 1. push my input to every peer (grid-stride 16-byte copies)
-  if (contributes && bytes) {
+  if (contributes && bytes && s_status == ST_OK) {
     const uint64_t stride = (uint64_t)gridDim.x * kThreads;
     const uint64_t first = (uint64_t)blockIdx.x * kThreads + tid;
     for (int jj = 1; jj < N; ++jj) {
@@ -1350,8 +1454,8 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
   if (tid == 0) {
     if (gridDim.x > 1) __threadfence();
     const uint32_t old = gridDim.x > 1 ? atomicAdd(&hdr->sm_arrive[parity], 1u) : 0u;
-    if (old == gridDim.x - 1) {
-      hdr->sm_arrive[parity] = 0;  // nobody touches this parity's counter until the call after next
+    if (old == gridDim.x - 1) hdr->sm_arrive[parity] = 0;  // untouched until the call after next
+    if (old == gridDim.x - 1 && s_status != ST_PEER_RESET) {  // (a zombie raises no flags either)
       for (int jj = 1; jj < N; ++jj)
         st_relaxed_sys(&reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->sm_meta[me], fp);
       fence_acq_rel_sys();  // all my CTAs' posted writes (and the fingerprints) before the flags
@@ -2185,7 +2289,11 @@ int tma_ctas(uint64_t slice_bytes) {
 }
 int small_ctas(uint64_t bytes) { return (int)std::max<uint64_t>(1, std::min<uint64_t>(16, (bytes + (32u << 10) - 1) >> 15)); }
 int rs_layout() { return env_int("FTAR_RS_LAYOUT", 0); }
+#ifdef FTAR_DIAGNOSTICS
 int diag_mode() { return env_int("FTAR_DIAG", 0); }
+#else
+int diag_mode() { return 0; }  // the product library has no result-changing diagnostics
+#endif
 
 // Host wait policy: pure spinning (pause) for the first 50 ms of a wait —
 // sleep_for() of a few us really sleeps ~50 us (timer slack), which would add
@@ -2508,7 +2616,11 @@ void reset_ctl(HostCtl* c) {
 extern "C" {
 
 const char* ftar_last_error(void) { return g_err.c_str(); }
-const char* ftar_version(void) { return "ftar_b200 1.0 sm_100a (two-shot NVLink pull, fp32 fold)"; }
+#ifdef FTAR_DIAGNOSTICS
+const char* ftar_version(void) { return "ftar_b200 2.0 sm_100a DIAGNOSTIC VARIANT (FTAR_DIAG honoured)"; }
+#else
+const char* ftar_version(void) { return "ftar_b200 2.0 sm_100a (two-shot NVLink, TMA bulk-copy reduce-scatter, fp32 fold)"; }
+#endif
 
 int ftar_set_tuning(int ctas, int local_ctas) {
   g_ctas = ctas;
@@ -2676,6 +2788,12 @@ int ftar_set_membership(ftar_ctx* c, const int* ring_slots, int n, int self_inde
     if (s < 0 || s >= kMaxSlots || !c->peer[s]) return fail(FTAR_ST_INVARIANT, "ring member not mapped");
     c->ring_slots[i] = s;
   }
+  // publish the installed generation in my arena (the zombie guard of
+  // senders that push into it); no kernel of mine is running here
+  {
+    DeviceGuard g(c->device);
+    CK(cudaMemcpy(c->arena + offsetof(ArenaHdr, gen_word), &generation, sizeof(uint64_t), cudaMemcpyHostToDevice));
+  }
   c->n = n;
   c->self = self_index;
   c->contrib = contrib_mask & ((n >= 32) ? 0xffffffffu : ((1u << n) - 1u));
@@ -2824,7 +2942,7 @@ static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, ui
     if (p.flags & kFlagDirect) p.flags |= kFlagSmallDirect;
     p.flags &= ~(kFlagPush | kFlagDirect);
     G = g_ctas > 0 ? g_ctas : small_ctas(in_bytes);
-  } else if (!sgd && c->n >= 2 && tma_on() && p.p_base / (uint64_t)c->n >= kTmaTile) {
+  } else if (!sgd && c->n >= 2 && tma_on() && p.p_base / (uint64_t)c->n >= tma_tile(c->n, (int)esz)) {
     // every segment spans >= one tile: the bulk-copy data path
     p.tma_stages = tma_stages_for(c->n, (int)esz);
     G = tma_ctas(p.slice * esz);
@@ -2947,6 +3065,7 @@ static int launch_local(ftar_ctx** ctxs, int n, const void* const* ins, int in_d
   p.fault_member = fault_member;
   p.fault_after_tiles = fault_after_tiles;
   p.rs_layout = rs_layout();
+  p.diag = diag_mode();
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (!(flags & FTAR_F_PROTOCOL) && fault_member < 0) {
@@ -3006,7 +3125,7 @@ static int launch_local(ftar_ctx** ctxs, int n, const void* const* ins, int in_d
     }
     return FTAR_OK;
   }
-  if (!sgd_p && n >= 2 && tma_on() && p.p_base / (uint64_t)n >= kTmaTile) {
+  if (!sgd_p && n >= 2 && tma_on() && p.p_base / (uint64_t)n >= tma_tile(n, in_dtype == FTAR_DT_BF16 ? 2 : 4)) {
     p.tma_stages = tma_stages_for(n, in_dtype == FTAR_DT_BF16 ? 2 : 4);
     if (g_local_ctas <= 0) G = std::min(G, tma_ctas(p.slice * (in_dtype == FTAR_DT_BF16 ? 2 : 4)));
   }
@@ -3327,6 +3446,16 @@ int ftar_probe_pattern(float* c, const float* a, const float* b, uint64_t n, int
     default: return fail(FTAR_ST_INVARIANT, "unroll must be 1, 2, 4 or 8");
   }
   CK(cudaGetLastError());
+  return FTAR_OK;
+}
+
+int ftar_debug_trace(ftar_ctx* c, uint64_t* out, int n) {
+  // the diagnostic build's per-tile pipeline stamps of CTA 0 (last call)
+  if (!c || !out) return fail(FTAR_ST_INVARIANT, "bad args");
+  DeviceGuard g(c->device);
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(out, c->arena + offsetof(ArenaHdr, dbg_trace), sizeof(uint64_t) * std::min(n, 512),
+                cudaMemcpyDeviceToHost));
   return FTAR_OK;
 }
 

@@ -102,6 +102,9 @@ struct alignas(128) ArenaHdr {
   alignas(128) uint64_t sm_in[kMaxMembers];  // small one-shot: member k's whole input is in my recv slot
   uint64_t sm_meta[kMaxMembers];             // its call fingerprint (validated like an entry record)
   alignas(128) uint32_t sm_arrive[2];        // small one-shot: push-arrival counter per call parity
+  alignas(128) uint64_t gen_word;            // the generation my host installed (ftar_set_membership):
+                                             // a sender whose call is older stops before pushing here
+  alignas(128) uint64_t dbg_trace[512];      // diagnostic build: CTA 0's per-tile pipeline stamps
 };
 static_assert(sizeof(ArenaHdr) <= kHdrBytes, "header too large");
 

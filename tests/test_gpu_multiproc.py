@@ -473,6 +473,73 @@ def _worker(rank, world, port, scenario, outdir):
             store.set(f"f_done{rank}", b"1")
             store.wait([f"f_done{r}" for r in range(world)])
             snap.close()
+        elif scenario == "zombie":
+            # a member dropped on timeout that resumes and
+            # pushes its old generation's small-bucket call late, with its old
+            # ring index, must never corrupt the regrouped ring's results
+            # (replica 1 leaves {0,1,2,..}: replica 2 takes ring index 1)
+            import time
+            victim = 1
+            cfg = ftar.PipelineConfig(per_chunk_timeout_s=1.0)
+            e = 65_537  # the small-bucket (push one-shot) path
+            group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, 1, deadline_s=30)
+            arrays = member_inputs(world, e, seed=91)
+            buf = torch.from_numpy(arrays[rank]).to(dev)
+            ftar.ftar_all_reduce(group, buf, 1, cfg)
+            (res["ok"] if np.array_equal(buf.cpu().numpy(), orc.oracle_reduce(arrays, 8 << 20, 4))
+             else res["errors"]).append("gen1")
+            store.set(f"z1_{rank}", b"1")
+            store.wait([f"z1_{r}" for r in range(world)])
+            survivors = [r for r in range(world) if r != victim]
+            if rank == victim:
+                store.wait(["z_regrouped"])
+                junk = torch.full((e,), 1.0e6, device=dev)
+                for k in range(20):  # the zombie: stale generation, stale mappings, late
+                    try:
+                        ftar.ftar_all_reduce(group, junk.clone(), 10 + k, cfg)
+                    except errors.FtdpError:
+                        pass
+                    group._links_up = True  # keep pushing as a confused replica would
+                store.set("z_zombie_done", b"1")
+                res["ok"].append("victim")
+            else:
+                try:
+                    ftar.ftar_all_reduce(group, torch.from_numpy(arrays[rank]).to(dev), 2, cfg)
+                    res["errors"].append("no error without the victim")
+                except errors.Recoverable:
+                    pass
+                gen, it, wrong, okc, retried = 2, 0, 0, 0, 0
+                sub = [arrays[r] for r in survivors]
+                want = orc.oracle_reduce(sub, 8 << 20, 4)
+                group.reconfig({r: ftar.PeerAddress(r) for r in survivors}, gen, deadline_s=30)
+                if rank == survivors[0]:
+                    store.set("z_regrouped", b"1")
+                t_end = None
+                while True:
+                    it += 1
+                    b = torch.from_numpy(arrays[rank]).to(dev)
+                    st = b"ok"
+                    try:
+                        ftar.ftar_all_reduce(group, b, it, cfg)
+                        if np.array_equal(b.cpu().numpy(), want):
+                            okc += 1
+                        else:
+                            wrong += 1
+                    except errors.Recoverable:
+                        st = b"retry"
+                    store.set(f"z_it{it}_{rank}", st)
+                    store.wait([f"z_it{it}_{r}" for r in survivors])
+                    if any(store.get(f"z_it{it}_{r}") != b"ok" for r in survivors):
+                        retried += 1
+                        gen += 1
+                        group.reconfig({r: ftar.PeerAddress(r) for r in survivors}, gen, deadline_s=30)
+                    if t_end is None and store.check(["z_zombie_done"]):
+                        t_end = it + 20
+                    if (t_end is not None and it >= t_end) or it > 2000:
+                        break
+                res["zombie"] = {"calls": it, "ok": okc, "wrong": wrong, "regroups": retried}
+                (res["ok"] if wrong == 0 else res["errors"]).append(f"never_wrong:{wrong}")
+                (res["ok"] if okc > 0 else res["errors"]).append("progress")
         elif scenario == "catchup":
             from paper_2602_00277_b200 import checkpoint as ck
             snap = ck.SnapshotStore(capacity_bytes=64 << 20, device=dev, fabric=fabric, rank=0, replica_id=rank)
@@ -610,6 +677,15 @@ def test_catchup_pull_over_nvlink():
     rec = res[world - 1]
     assert not rec["errors"], rec["errors"]
     assert {"connected", "pull", "striped", "unavailable"} <= set(rec["ok"])
+
+
+def test_zombie_member_never_corrupts_regrouped_ring():
+    world = world_size()
+    if world < 3:
+        pytest.skip("needs >= 3 GPUs (a survivor must take the zombie's ring index)")
+    res = run("zombie", world)
+    for r in res:
+        assert not r["errors"], (r["errors"], r.get("zombie"))
 
 
 def test_kill_rejoin_churn_keeps_memory_flat():
