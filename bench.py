@@ -232,6 +232,9 @@ def workload_config(args, n):
             "in_dtype": args.dtype, "out_dtype": "f32", "chunk_bytes": 8 * MIB, "max_in_flight": 4,
             "fused": "x f32(1/n) normalisation" + (", bf16->fp32 cast" if args.dtype == "bf16" else ""),
             "result": "in place" if args.inplace else "out-of-place fp32 (out=)",
+            "buffers": ("torch.empty tensors, " + ("registered (RingGroup.register)" if args.register
+                                                    else "staged per call") if args.unregistered
+                        else "registered pool (RingGroup.alloc_bucket)"),
             "kernel": "in-process one-shot" if emu else "two-shot NVLink (push all-gather)",
             "queue_depth": args.depth,
             "l2": "inputs larger than L2 (126 MB) per GPU; no flush needed",
@@ -270,6 +273,57 @@ def timed_loop(fn, steps, stream, torch, drain=None):
         print(json.dumps({"rank": int(os.environ.get("RANK", 0)), "per_launch_ms": [round(x, 4) for x in per]}),
               file=sys.stderr, flush=True)
     return t_start.elapsed_time(t_end) / 1e3, sum(per) / len(per) / 1e3
+
+
+class NvlinkPM:
+    """This GPU's NVLink bytes over a window from CUPTI PM sampling
+    (tools/nvlink_pm.cpp): device-level nvlrx/nvltx counters sampled on a
+    timer while the kernels run concurrently.  The measured traffic behind
+    roofline.traffic for N >= 2 (NVML's NVLink fields are N/A on this driver)."""
+
+    def __init__(self, cuda_index: int, interval_ns: int = 50_000):
+        import ctypes as C
+        self.dev, self.lib, self.err = cuda_index, None, None
+        path = os.path.join(ROOT, "tools", "_build", "libnvlink_pm.so")
+        try:
+            if not os.path.exists(path):
+                os.makedirs(os.path.dirname(path), exist_ok=True)
+                subprocess.run(["g++", "-O2", "-shared", "-fPIC", "-I/usr/local/cuda/include",
+                                os.path.join(ROOT, "tools", "nvlink_pm.cpp"), "-L/usr/local/cuda/lib64", "-lcupti",
+                                "-o", path], check=True, capture_output=True, timeout=120)
+            lib = C.CDLL(path)
+            lib.nvpm_error.restype = C.c_char_p
+            lib.nvpm_open.argtypes = [C.c_int, C.c_uint64, C.c_uint32]
+            lib.nvpm_stop.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_uint64),
+                                      C.POINTER(C.c_int)]
+            if lib.nvpm_open(cuda_index, interval_ns, 200_000):
+                self.err = lib.nvpm_error().decode()
+            else:
+                self.lib = lib
+        except Exception as exc:  # noqa: BLE001
+            self.err = str(exc)[:200]
+
+    def start(self):
+        if self.lib is not None and self.lib.nvpm_start(self.dev):
+            self.err = self.lib.nvpm_error().decode()
+            self.lib = None
+
+    def stop(self):
+        """{rx, tx, rx_user, tx_user} bytes of the window, or None."""
+        import ctypes as C
+        if self.lib is None:
+            return None
+        out = (C.c_double * 4)()
+        n, span, ovf = C.c_int(), C.c_uint64(), C.c_int()
+        if self.lib.nvpm_stop(self.dev, out, C.byref(n), C.byref(span), C.byref(ovf)):
+            self.err = self.lib.nvpm_error().decode()
+            return None
+        return {"rx": out[0], "tx": out[1], "rx_user": out[2], "tx_user": out[3], "samples": n.value,
+                "span_ms": span.value / 1e6, "overflow": bool(ovf.value)}
+
+    def close(self):
+        if self.lib is not None:
+            self.lib.nvpm_close(self.dev)
 
 
 class NvlinkBytes:
@@ -446,9 +500,15 @@ def run_multi(args, rank, world, local_rank):
     group.reconfig({r: ftar.PeerAddress(r) for r in range(n)}, 1, deadline_s=60.0)
     host = member_bucket(rank, elems, args.dtype)
     if args.unregistered:
-        # the reference call shape on an ordinary caching-allocator tensor
+        # the reference call shape on an ordinary caching-allocator tensor:
+        # staged into the arena per call, or (--register) registered with the
+        # ring once and then reduced in place / pushed into zero-copy
         buf = host.to(dev)
         out = buf if args.inplace else torch.empty(elems, device=dev)
+        if args.register:
+            group.register(buf)
+            if out is not buf:
+                group.register(out)
     else:
         buf = group.alloc_bucket(elems, tdtype)
         buf.copy_(host)
@@ -490,8 +550,11 @@ def run_multi(args, rank, world, local_rank):
     torch.cuda.synchronize()
     dist.barrier()
     nvl = NvlinkBytes(local_rank)
+    pm = NvlinkPM(local_rank) if not args.no_pm else None
     with ClockSampler(local_rank) as clk:
         c0 = nvl.read()  # (the counters cover the untimed collective below too: steps + 1 calls)
+        if pm is not None:
+            pm.start()
         # One untimed collective right before the window: it is a device-side
         # barrier, so the timed region starts on every rank when all streams
         # reach the same point, instead of absorbing the ranks' host-side exit
@@ -501,6 +564,9 @@ def run_multi(args, rank, world, local_rank):
         step()
         total, per_launch = timed_loop(step, args.steps, stream, torch, drain)
         c1 = nvl.read()
+        pmw = pm.stop() if pm is not None else None
+    if pm is not None:
+        pm.close()
     dist.barrier()
     after = None if args.inplace else digest(out)
     phases = phase_us(group)
@@ -512,8 +578,14 @@ def run_multi(args, rank, world, local_rank):
     nv_meas = None
     if c0 is not None and c1 is not None:
         nv_meas = [(b - a) / (args.steps + 1) for a, b in zip(c0, c1)]
+    if nv_meas is None and pmw is not None:
+        # user data bytes (what the kernels moved; the link also carries
+        # packet headers: nvlrx__bytes ~1.25x, reported beside)
+        nv_meas = [pmw["tx_user"] / (args.steps + 1), pmw["rx_user"] / (args.steps + 1)]
     all_nv = [None] * n
     dist.all_gather_object(all_nv, nv_meas)
+    all_pm = [None] * n
+    dist.all_gather_object(all_pm, pmw if pmw is not None else {"error": pm.err if pm is not None else "off"})
     t_step = total / args.steps
     value = busbw(elems * in_bytes, t_step, n)
     nv_bytes = (n - 1) / n * elems * (in_bytes + 4)
@@ -522,8 +594,12 @@ def run_multi(args, rank, world, local_rank):
     roof = {"bound": "nvlink", "achieved": round(nv_bytes / per_launch / 1e9, 1), "peak": NVLINK_PEER_GBS,
             "unit": "GB/s", "frac": round(nv_bytes / per_launch / 1e9 / NVLINK_PEER_GBS, 4),
             "traffic": round(max(rx)) if rx else None,
-            "traffic_source": ("NVML NVLink data RX bytes per launch (field 139, all links), max over ranks, "
-                               "sampled around the timed region" if rx else "NVML NVLink counters unavailable"),
+            "traffic_source": ("NVLink RX user-data bytes per launch (nvlrx__bytes_data_user.sum, all links) from "
+                               "CUPTI PM sampling of each GPU across the timed calls (+1 untimed), max over ranks; "
+                               "nvlink_pm_window has the totals incl. packet overhead (nvlrx__bytes.sum)"
+                               if rx else "NVLink counters unavailable: " + json.dumps(all_pm[0])[:200]),
+            "traffic_over_algorithmic": round(max(rx) / nv_bytes, 4) if rx else None,
+            "nvlink_pm_window": all_pm,
             "nvlink_rx_bytes_per_launch": [round(x) for x in rx] if rx else None,
             "nvlink_tx_bytes_per_launch": [round(x) for x in tx] if tx else None,
             "kernel": "allreduce_kernel (two-shot: RS by NVLink pulls, AG by pushes)",
@@ -656,9 +732,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-check", action="store_true", help="skip the oracle self-check")
+    ap.add_argument("--no-pm", action="store_true", help="N>=2: no CUPTI PM sampling of the NVLink counters")
     ap.add_argument("--no-protocol", action="store_true", help="N=1: skip the protocol-kernel record")
     ap.add_argument("--unregistered", action="store_true",
                     help="N>=2: buckets are ordinary torch.empty tensors (reference call shape), not pool buffers")
+    ap.add_argument("--register", action="store_true",
+                    help="with --unregistered: RingGroup.register the tensors (zero-copy) instead of staging")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         _reexec_under_torchrun(args.gpus)

@@ -91,6 +91,20 @@ int ftar_ctx_link_local(ftar_ctx* ctx, int slot, ftar_ctx* other);
  * a slot of the current ring. */
 int ftar_ctx_unmap(ftar_ctx* ctx, int slot);
 
+/* Registered user buffers (any device allocation, e.g. a caching-allocator
+ * tensor): the two-shot kernel reads a registered input in place (no staging
+ * copy) and pushes results into a registered `out`.  Registration is a
+ * collective of the ring (RingGroup.register): each member exports its
+ * region (the owning block's IPC handle and the region's offset in it) and
+ * imports every peer's before any call uses it.  Up to 16 regions per member.
+ * Replaces the staging of buf for the reference's in-place call shape
+ * (ftar.py:329-353 copies buf[p] into `work`). */
+int ftar_region_register(ftar_ctx* ctx, const void* ptr, uint64_t bytes, int* rid, void* handle, size_t buflen,
+                         uint64_t* offset);
+int ftar_region_unregister(ftar_ctx* ctx, int rid);
+int ftar_region_import(ftar_ctx* ctx, int slot, int rid, const void* handle, size_t len, uint64_t offset,
+                       uint64_t bytes);
+
 /* Write the quorum decision into the control words (quorum.py:49-75 ->
  * live mask = members, contributor mask = healthy, epoch = generation).
  * ring_slots[i] = slot (as given to ftar_ctx_import; self = -1) of the

@@ -37,6 +37,9 @@ SIGNATURES = {
     "ftar_ctx_unmap": (i32, [c_ctx_p, i32]),
     "ftar_ctx_link_local": (i32, [c_ctx_p, i32, c_ctx_p]),
     "ftar_set_membership": (i32, [c_ctx_p, C.POINTER(i32), i32, i32, u32, u64]),
+    "ftar_region_register": (i32, [c_ctx_p, vp, u64, C.POINTER(i32), vp, C.c_size_t, C.POINTER(u64)]),
+    "ftar_region_unregister": (i32, [c_ctx_p, i32]),
+    "ftar_region_import": (i32, [c_ctx_p, i32, i32, vp, C.c_size_t, u64, u64]),
     "ftar_allreduce_launch": (i32, [c_ctx_p, vp, i32, vp, u64, u64, i32, C.c_float, u32, vp]),
     "ftar_allreduce_sgd_launch": (i32, [c_ctx_p, vp, i32, vp, u64, u64, i32, C.c_float, u32, vp, vp, vp, vp,
                                         C.c_float, C.c_float, vp]),

@@ -338,8 +338,15 @@ def catchup_stream(device: torch.device) -> torch.cuda.Stream:
     return _side_streams[idx]
 
 
+# CTA budget of a catch-up pull: each CTA streams ~47 GB/s (bulk copies), so 8
+# CTAs cap the pull near 300 GB/s and leave the recovering GPU's NVLink
+# ingress to the ring it is a member of (tools/bench_catchup.py, N=4: healthy
+# steps 1.13x steady at 8 CTAs, 1.19x at 16, 1.24x at 32)
+DEFAULT_PULL_CTAS = 8
+
+
 def start_fetch(local: SnapshotStore, donor, step: int, rank: int, params_out: torch.Tensor,
-                momentum_out: torch.Tensor, timeout_s: float = 5.0, ctas: int = 16) -> CatchupPull:
+                momentum_out: torch.Tensor, timeout_s: float = 5.0, ctas: int = DEFAULT_PULL_CTAS) -> CatchupPull:
     """Launch the pull of `donor`'s snapshot of `step` into the given tensors
     without waiting.  `donor` is a SnapshotStore in this process (same device),
     a replica id resolved through ``local.fabric``, or a list of replica ids:
@@ -383,7 +390,7 @@ def _default_fabric():
 
 def fetch_shard(addr, step: int, rank: int, replica_id: int = 0, incarnation: int = 0,
                 timeout_s: float = 5.0, plan=None, *, local: SnapshotStore | None = None,
-                out: tuple[torch.Tensor, torch.Tensor] | None = None, ctas: int = 16):
+                out: tuple[torch.Tensor, torch.Tensor] | None = None, ctas: int = DEFAULT_PULL_CTAS):
     """Pull (params, momentum) of one rank shard of a committed step
     (checkpoint.py:117-144); the reference's signature.
 

@@ -33,6 +33,7 @@
 #include <ctime>
 #include <string>
 #include <thread>
+#include <vector>
 
 using namespace ftar;
 
@@ -50,6 +51,15 @@ constexpr uint32_t kFlagDirect = 1u << 8;  // internal launch flag: RS writes my
 constexpr uint32_t kFlagPush = 1u << 9;    // internal: all-gather by posted writes into peers' outs
 constexpr uint32_t kFlagSGD = 1u << 10;    // internal: apply SGD-momentum to the reduced gradient
 constexpr uint32_t kFlagSmallDirect = 1u << 11;  // internal: small one-shot folds straight into out
+
+// Entry-record offsets that name a REGISTERED buffer instead of an arena
+// offset: top two bits set, region id in bits 48..59, byte offset below.
+// (Arena offsets the kernels dereference are always < 2^62.)
+constexpr uint64_t kRegionTag = 3ull << 62;
+__host__ __device__ __forceinline__ uint64_t region_ref(uint32_t rid, uint64_t off) {
+  return kRegionTag | ((uint64_t)(rid & 0xfffu) << 48) | (off & ((1ull << 48) - 1));
+}
+__host__ __device__ __forceinline__ bool is_region_ref(uint64_t v) { return (v >> 62) == 3 && v != ~0ull; }
 
 struct LaunchParams {
   char* base[kMaxMembers];       // arena base of ring member i, as mapped here
@@ -84,6 +94,8 @@ struct LaunchParams {
   int diag;                      // timing diagnostics: 1 = RS stores skipped, 2 = RS reads local only
   int rs_ctas;                   // CTAs that reduce (the rest only all-gather); <= gridDim.x
   uint32_t tma_stages;           // > 0: bulk-copy (TMA) data path with this many smem stages
+  uint64_t my_in_va;             // real mode: my input as this process addresses it
+  uint64_t region_va[kMaxMembers][kMaxRegions];  // member i's registered region r, mapped here (0 = none)
   uint32_t intra_op;             // intra-replica collective (kIntraRS / kIntraAG), 0 = FTAR
   uint64_t seg_off[kMaxMembers]; // intra: rank k's shard is elements [seg_off[k], +seg_len[k])
   uint64_t seg_len[kMaxMembers];
@@ -1025,7 +1037,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
     uint64_t oo = 0;
     if (s_status == ST_OK && j < N) {
       if (j == me) {
-        s_pin[j] = reinterpret_cast<uint64_t>(mybase) + p.in_off[me];
+        s_pin[j] = p.emulated ? reinterpret_cast<uint64_t>(mybase) + p.in_off[me] : p.my_in_va;
         s_pres[j] = reinterpret_cast<uint64_t>(mybase) + p.res_off[me];
         s_pout[j] = reinterpret_cast<uint64_t>(p.out[me]);
       } else {
@@ -1041,9 +1053,22 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
           const uint64_t sum = ld_relaxed_sys(&e->sum);
           if (fp != want_fp) st = ST_PROTOCOL;  // a different call
           else if (sum != entry_sum(tag, fp, in_off, res_off, oo)) st = ST_PEER_RESET;
-          s_pin[j] = reinterpret_cast<uint64_t>(p.base[j]) + in_off;
+          // arena offsets, or references to member j's registered buffers
+          // (mapped here by RingGroup.register); an unmapped region is a
+          // protocol error, never a guess
+          // (in-process rings pass raw offsets, which may be "negative")
+          auto resolve = [&](uint64_t off) -> uint64_t {
+            if (p.emulated || !is_region_ref(off)) return reinterpret_cast<uint64_t>(p.base[j]) + off;
+            const uint32_t rid = (uint32_t)(off >> 48) & 0xfffu;
+            const uint64_t va = rid < kMaxRegions ? p.region_va[j][rid] : 0;
+            return va ? va + (off & ((1ull << 48) - 1)) : 0;
+          };
+          s_pin[j] = resolve(in_off);
           s_pres[j] = reinterpret_cast<uint64_t>(p.base[j]) + res_off;
-          s_pout[j] = reinterpret_cast<uint64_t>(p.base[j]) + oo;
+          s_pout[j] = oo == ~0ull ? 0 : resolve(oo);
+          const bool unmapped = !p.emulated && ((is_region_ref(in_off) && s_pin[j] == 0) ||
+                                                (oo != ~0ull && is_region_ref(oo) && s_pout[j] == 0));
+          if (st == ST_OK && unmapped) st = ST_PROTOCOL;
         }
       }
     }
@@ -1127,6 +1152,9 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
   int done = 0;
   // the bulk-copy path runs when every buffer is 16-byte aligned (known only
   // after the entry records) and the call is not a fused-optimizer one
+  // (the fused optimizer keeps the register path: its epilogue's extra HBM
+  // traffic in the consumers made the bulk path slower, config 5 at N=4:
+  // 14.0 vs 10.2 ms per 2 GB step)
   const bool tma = p.tma_stages != 0 && s_vec_ok != 0 && (p.flags & kFlagSGD) == 0 && (p.diag == 0 || p.diag >= 3);
   uint32_t gseq = 0;  // thread 0: stage-ring sequence number (mbarrier phases) across RS and AG
   if (s_status == ST_OK) {
@@ -1837,11 +1865,57 @@ struct PullSrcs {
   int n;
 };
 
+// The bulk-copy (TMA) form of a pull: thread 0 streams a CTA's chunks through
+// kPullStages x kPullTile smem stages (donor -> shared -> my buffer), one
+// continuous pipeline over all of them; ~47 GB/s per CTA against ~28 for the
+// register copy (tools/tma_probe.py), so a budget of k CTAs is a bandwidth cap
+// of ~47k GB/s.  Used when every region is 16-byte aligned.
+constexpr uint32_t kPullTile = 32 * 1024;
+constexpr uint32_t kPullStages = 6;
+constexpr uint32_t kPullSmem = 1024 + kPullStages * kPullTile;
+
+struct BulkStream {  // thread 0's pipeline state
+  char* smem;
+  uint64_t issued = 0, completed = 0;
+  char* pend_dst[kPullStages];
+  uint32_t pend_bytes[kPullStages];
+  __device__ void complete_one() {
+    const uint64_t t = completed++;
+    const uint32_t s = (uint32_t)(t % kPullStages);
+    mbar_wait(reinterpret_cast<uint64_t*>(smem) + s, (uint32_t)((t / kPullStages) & 1));
+    bulk_s2g(pend_dst[s], smem + 1024 + (uint64_t)s * kPullTile, pend_bytes[s]);
+    bulk_commit();
+  }
+  __device__ void push(char* dst, const char* src, uint32_t bytes) {
+    const uint32_t s = (uint32_t)(issued % kPullStages);
+    if (issued >= kPullStages) bulk_wait_read<0>();  // the store of the tile that used stage s has read it
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem) + s;
+    mbar_expect_tx(full, bytes);
+    bulk_g2s(smem + 1024 + (uint64_t)s * kPullTile, src, bytes, full);
+    pend_dst[s] = dst;
+    pend_bytes[s] = bytes;
+    ++issued;
+    if (issued - completed > kPullStages - 1) complete_one();
+  }
+  __device__ void copy(char* dst, const char* src, uint64_t bytes) {
+    for (uint64_t o = 0; o < bytes; o += kPullTile) push(dst + o, src + o, (uint32_t)umin(kPullTile, bytes - o));
+  }
+  __device__ void flush() {
+    while (completed < issued) complete_one();
+    bulk_wait<0>();
+  }
+};
+
 __global__ void __launch_bounds__(kThreads, 1)
 snap_pull_kernel(const __grid_constant__ PullSrcs src, SnapHdr* lhdr, HostCtl* ctl, uint64_t tag, int64_t want,
-                 char* dp, uint64_t pb, char* dm, uint64_t mb) {
+                 char* dp, uint64_t pb, char* dm, uint64_t mb, int bulk) {
   __shared__ uint32_t s_st;
+  extern __shared__ __align__(1024) char psmem[];
   const int tid = threadIdx.x;
+  if (bulk && tid == 0) {
+    for (uint32_t i = 0; i < kPullStages; ++i) mbar_init(reinterpret_cast<uint64_t*>(psmem) + i, 1);
+    fence_mbar_init();
+  }
   if (tid == 0) {
     if (blockIdx.x == 0) ctl->started = tag;
     s_st = ST_OK;
@@ -1861,7 +1935,28 @@ snap_pull_kernel(const __grid_constant__ PullSrcs src, SnapHdr* lhdr, HostCtl* c
   __syncthreads();
   const uint64_t total = pb + mb;
   const uint64_t nchunks = (total + kPullChunk - 1) / kPullChunk;
-  if (s_st == ST_OK) {
+  if (s_st == ST_OK && bulk) {
+    if (tid == 0) {
+      BulkStream bs;
+      bs.smem = psmem;
+      uint32_t it = 0;
+      for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+        if ((it & 7u) == 0 && (ctl->abort_tag == tag || ld_relaxed_sys32(&lhdr->err) != 0)) {
+          s_st = ST_ABORTED;
+          break;
+        }
+        const char* data = src.arena[c % (uint64_t)src.n] + kSnapHdrBytes;
+        const uint64_t a = c * kPullChunk, b = umin(a + kPullChunk, total);
+        if (a < pb) bs.copy(dp + a, data + a, umin(b, pb) - a);
+        if (b > pb) {
+          const uint64_t s0 = umax(a, pb);
+          bs.copy(dm + (s0 - pb), data + s0, b - s0);
+        }
+        if ((it & 7u) == 7u) ctl->progress = ((uint64_t)blockIdx.x << 32) | it;
+      }
+      bs.flush();  // every copy landed (also on abort: nothing may write smem after exit)
+    }
+  } else if (s_st == ST_OK) {
     uint32_t it = 0;
     for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
       if ((it & 7u) == 0) {  // abort word lives in host memory: check every 8 chunks
@@ -2280,10 +2375,14 @@ uint64_t small_bytes() {
 bool pdl_on() { return env_int("FTAR_PDL", 1) != 0; }
 // bulk-copy (TMA) data path for the two-shot kernel (FTAR_TMA=0 disables)
 bool tma_on() { return env_int("FTAR_TMA", 1) != 0; }
+// ... for slices of at least this many input bytes (tools/tune_tma.py, N=4:
+// the register path wins at <= 4 MiB slices, the bulk path from 16 MiB)
+uint64_t tma_min_slice() { return (uint64_t)env_int("FTAR_TMA_MIN_SLICE_MIB", 16) << 20; }
 // CTAs of the bulk-copy path: ~128 KB of my slice per CTA, at most
-// FTAR_CTAS_TMA (default 32: tools/tma_probe.py saturates a link with 16-32)
+// FTAR_CTAS_TMA (default 48, a third of the SMs: N=4 f32 busbw 597 / 661 /
+// 680 GB/s at 64 MiB / 256 MiB / 1 GiB; 16 CTAs already give 648 at 256 MiB)
 int tma_ctas(uint64_t slice_bytes) {
-  const int cap = g_ctas > 0 ? g_ctas : env_int("FTAR_CTAS_TMA", 32);
+  const int cap = g_ctas > 0 ? g_ctas : env_int("FTAR_CTAS_TMA", 48);
   const uint64_t per = (uint64_t)env_int("FTAR_TMA_BYTES_PER_CTA", 128 << 10);
   return (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)std::max(cap, 1), (slice_bytes + per - 1) / per));
 }
@@ -2343,6 +2442,38 @@ struct ftar_ctx {
   uint64_t gen = 0, seq = 0;
   uint64_t cur_tag = 0;
   uint64_t hard_timeout_ns = 120ull * 1000000000ull;
+  // registered buffers (RingGroup.register): mine by region id, and every
+  // peer slot's as mapped here (one IPC mapping per peer allocation block)
+  uint64_t my_region_ptr[kMaxRegions] = {};
+  uint64_t my_region_bytes[kMaxRegions] = {};
+  uint64_t peer_region_va[kMaxSlots][kMaxRegions] = {};
+  struct BlockMap {
+    cudaIpcMemHandle_t h;
+    char* va;
+    int slot;
+  };
+  std::vector<BlockMap> blocks;
+
+  int find_region(const void* ptr, uint64_t bytes, uint64_t* off) const {
+    const uint64_t a = reinterpret_cast<uint64_t>(ptr);
+    for (int r = 0; r < kMaxRegions; ++r)
+      if (my_region_bytes[r] && a >= my_region_ptr[r] && a + bytes <= my_region_ptr[r] + my_region_bytes[r]) {
+        *off = a - my_region_ptr[r];
+        return r;
+      }
+    return -1;
+  }
+  void drop_slot_regions(int slot) {
+    for (size_t i = 0; i < blocks.size();) {
+      if (blocks[i].slot == slot) {
+        cudaIpcCloseMemHandle(blocks[i].va);
+        blocks.erase(blocks.begin() + (long)i);
+      } else {
+        ++i;
+      }
+    }
+    for (int r = 0; r < kMaxRegions; ++r) peer_region_va[slot][r] = 0;
+  }
 
   // enqueue a collective with `tag`; returns its control block or nullptr when full
   HostCtl* push(uint64_t tag) {
@@ -2687,6 +2818,8 @@ int ftar_ctx_destroy(ftar_ctx* c) {
     c->ctl_hs[slot].abort_tag = c->q_tag[slot];
   }
   cudaDeviceSynchronize();
+  for (auto& b : c->blocks) cudaIpcCloseMemHandle(b.va);
+  c->blocks.clear();
   for (int s = 0; s < kMaxSlots; ++s)
     if (c->peer[s] && !c->peer_local[s]) cudaIpcCloseMemHandle(c->peer[s]);
   cudaFree(c->arena);
@@ -2760,12 +2893,90 @@ int ftar_ctx_unmap(ftar_ctx* c, int slot) {
     if (i != c->self && c->ring_slots[i] == slot)
       return fail(FTAR_ST_INVARIANT, "slot " + std::to_string(slot) + " belongs to the current ring");
   DeviceGuard g(c->device);
+  c->drop_slot_regions(slot);
   if (c->peer[slot]) {
     if (!c->peer_local[slot]) cudaIpcCloseMemHandle(c->peer[slot]);
     c->peer[slot] = nullptr;
     c->peer_local[slot] = false;
     std::memset(&c->peer_handle[slot], 0, sizeof(cudaIpcMemHandle_t));
   }
+  return FTAR_OK;
+}
+
+int ftar_region_register(ftar_ctx* c, const void* ptr, uint64_t bytes, int* rid_out, void* handle,
+                         size_t buflen, uint64_t* offset_out) {
+  // Export the allocation block holding [ptr, ptr+bytes) (any caching-
+  // allocator tensor): its IPC handle and ptr's offset inside it.  The
+  // region id names the buffer in entry records.
+  if (!c || !ptr || !bytes || !rid_out || !handle || buflen < sizeof(cudaIpcMemHandle_t) || !offset_out)
+    return fail(FTAR_ST_INVARIANT, "bad register args");
+  DeviceGuard g(c->device);
+  uint64_t off = 0;
+  int rid = c->find_region(ptr, bytes, &off);
+  if (rid < 0) {
+    for (int r = 0; r < kMaxRegions && rid < 0; ++r)
+      if (!c->my_region_bytes[r]) rid = r;
+    if (rid < 0) return fail(FTAR_ST_INVARIANT, "all 16 region ids in use (unregister one first)");
+    c->my_region_ptr[rid] = reinterpret_cast<uint64_t>(ptr);
+    c->my_region_bytes[rid] = bytes;
+    off = 0;
+  }
+  using GetRange = int (*)(unsigned long long*, size_t*, unsigned long long);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (!fn) return fail(FTAR_ST_CUDA, "cuMemGetAddressRange unavailable");
+    get_range = reinterpret_cast<GetRange>(fn);
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<unsigned long long>(ptr)) != 0 || !base)
+    return fail(FTAR_ST_INVARIANT, "pointer is not inside a device allocation");
+  if (reinterpret_cast<uint64_t>(ptr) + bytes > base + size) return fail(FTAR_ST_INVARIANT, "region spans allocations");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  std::memcpy(handle, &h, sizeof(h));
+  *rid_out = rid;
+  *offset_out = c->my_region_ptr[rid] - base;  // the region's start inside the block
+  (void)off;
+  return FTAR_OK;
+}
+
+int ftar_region_unregister(ftar_ctx* c, int rid) {
+  if (!c || rid < 0 || rid >= kMaxRegions) return fail(FTAR_ST_INVARIANT, "bad region id");
+  if (c->q_count && !c->all_done()) return fail(FTAR_ST_INVARIANT, "unregister with a collective in flight");
+  c->my_region_ptr[rid] = c->my_region_bytes[rid] = 0;
+  return FTAR_OK;
+}
+
+int ftar_region_import(ftar_ctx* c, int slot, int rid, const void* handle, size_t len, uint64_t offset,
+                       uint64_t bytes) {
+  // Map peer `slot`'s registered region `rid` (its block's IPC handle + the
+  // region's offset in it); one mapping per peer block, shared by regions.
+  if (!c || slot < 0 || slot >= kMaxSlots || rid < 0 || rid >= kMaxRegions || !handle ||
+      len < sizeof(cudaIpcMemHandle_t))
+    return fail(FTAR_ST_INVARIANT, "bad region import args");
+  (void)bytes;
+  DeviceGuard g(c->device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  char* va = nullptr;
+  for (auto& b : c->blocks)
+    if (b.slot == slot && std::memcmp(&b.h, &h, sizeof(h)) == 0) va = b.va;
+  if (!va) {
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      g_err = std::string("cudaIpcOpenMemHandle(region): ") + cudaGetErrorString(e);
+      return FTAR_ST_PEER_DOWN;
+    }
+    va = static_cast<char*>(p);
+    c->blocks.push_back({h, va, slot});
+  }
+  c->peer_region_va[slot][rid] = reinterpret_cast<uint64_t>(va) + offset;
   return FTAR_OK;
 }
 
@@ -2873,18 +3084,29 @@ static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, ui
   uint64_t in_off;
   const bool registered = inp >= c->arena + c->pool_off && inp + in_bytes <= c->arena + c->arena_bytes;
   const bool small = c->n >= 2 && !sgd && in_bytes > 0 && in_bytes <= small_bytes();
+  uint64_t roff = 0;
+  const int rid = (!registered && c->n >= 2 && !small) ? c->find_region(inp, in_bytes, &roff) : -1;
+  uint64_t my_in_va = reinterpret_cast<uint64_t>(inp);
   if (registered || c->n == 1 || small) {  // small buckets: peers never read my input
     in_off = (uint64_t)(inp - c->arena);
+  } else if (rid >= 0) {
+    // a registered user buffer: peers read it in place through their mapping
+    in_off = region_ref((uint32_t)rid, roff);
   } else {
     // Unregistered bucket: peers can only read the arena, so stage it (double
     // buffered by call parity: peers finished reading this half two calls ago).
     const uint64_t so = c->stage_off[c->seq & 1];
     if (in_bytes) CK(cudaMemcpyAsync(c->arena + so, in, in_bytes, cudaMemcpyDeviceToDevice, st));
     in_off = so;
+    my_in_va = reinterpret_cast<uint64_t>(c->arena + so);
   }
   LaunchParams p{};
   fill_geometry(p, n_elems, chunk_bytes, max_in_flight, c->n, base_elem, total_elems);
   for (int i = 0; i < c->n; ++i) p.base[i] = (i == c->self) ? c->arena : c->peer[c->ring_slots[i]];
+  p.my_in_va = my_in_va;
+  for (int i = 0; i < c->n; ++i)
+    if (i != c->self)
+      for (int r = 0; r < kMaxRegions; ++r) p.region_va[i][r] = c->peer_region_va[c->ring_slots[i]][r];
   c->push(tag);
   p.ctl[c->self] = c->ctl_d;
   p.out[c->self] = out;
@@ -2911,12 +3133,15 @@ static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, ui
       p.sgd_lr = sgd->lr;
       p.sgd_beta = sgd->beta;
     }
-    // push mode needs `out` inside my exported arena (peers write into it)
+    // push mode needs `out` addressable by the peers: in my exported arena
+    // or a registered buffer (peers write into it)
     const char* op = reinterpret_cast<const char*>(out);
-    const bool out_reg = op >= c->arena + c->pool_off && op + n_elems * 4 <= c->arena + c->arena_bytes;
-    if (!sgd && (p.flags & kFlagDirect) && out_reg && !env_int("FTAR_NO_PUSH", 0)) {
+    const bool out_pool = op >= c->arena + c->pool_off && op + n_elems * 4 <= c->arena + c->arena_bytes;
+    uint64_t ooff = 0;
+    const int orid = out_pool ? -1 : c->find_region(op, n_elems * 4, &ooff);
+    if (!sgd && (p.flags & kFlagDirect) && (out_pool || orid >= 0) && !env_int("FTAR_NO_PUSH", 0)) {
       p.flags |= kFlagPush;
-      p.out_off[c->self] = (uint64_t)(op - c->arena);
+      p.out_off[c->self] = out_pool ? (uint64_t)(op - c->arena) : region_ref((uint32_t)orid, ooff);
     }
   }
   p.contrib = c->contrib;
@@ -2942,8 +3167,9 @@ static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, ui
     if (p.flags & kFlagDirect) p.flags |= kFlagSmallDirect;
     p.flags &= ~(kFlagPush | kFlagDirect);
     G = g_ctas > 0 ? g_ctas : small_ctas(in_bytes);
-  } else if (!sgd && c->n >= 2 && tma_on() && p.p_base / (uint64_t)c->n >= tma_tile(c->n, (int)esz)) {
-    // every segment spans >= one tile: the bulk-copy data path
+  } else if (!sgd && c->n >= 2 && tma_on() && p.p_base / (uint64_t)c->n >= tma_tile(c->n, (int)esz) &&
+             (p.slice * esz >= tma_min_slice() || g_ctas > 0)) {
+    // every segment spans >= one tile and the slice is large: the bulk-copy data path
     p.tma_stages = tma_stages_for(c->n, (int)esz);
     G = tma_ctas(p.slice * esz);
   }
@@ -3763,9 +3989,20 @@ int ftar_snap_pull_multi_launch(ftar_snap* local, const int* slots, int nslots, 
   local->cur_tag = tag;
   local->inflight = true;
   const int G = std::max(1, ctas);
-  snap_pull_kernel<<<G, kThreads, 0, st>>>(src, reinterpret_cast<SnapHdr*>(local->arena), local->ctl_d, tag,
-                                           (int64_t)want_step, static_cast<char*>(dst_params), pbytes,
-                                           static_cast<char*>(dst_momentum), mbytes);
+  // the bulk-copy pull when every region is 16-byte aligned (FTAR_TMA=0: register copy)
+  const int bulk = tma_on() && (pbytes % 16 == 0) && (mbytes % 16 == 0) &&
+                   ((reinterpret_cast<uint64_t>(dst_params) | reinterpret_cast<uint64_t>(dst_momentum)) % 16 == 0);
+  if (bulk) {
+    static bool attr_set[64] = {};
+    const int dev = local->device;
+    if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+      CK(cudaFuncSetAttribute(snap_pull_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPullSmem));
+      if (dev >= 0 && dev < 64) attr_set[dev] = true;
+    }
+  }
+  snap_pull_kernel<<<G, kThreads, bulk ? kPullSmem : 0, st>>>(
+      src, reinterpret_cast<SnapHdr*>(local->arena), local->ctl_d, tag, (int64_t)want_step,
+      static_cast<char*>(dst_params), pbytes, static_cast<char*>(dst_momentum), mbytes, bulk);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     local->inflight = false;

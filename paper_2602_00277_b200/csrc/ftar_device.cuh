@@ -21,6 +21,7 @@
 namespace ftar {
 
 constexpr int kMaxMembers = 8;
+constexpr int kMaxRegions = 16;        // registered buffers per member (RingGroup.register)
 constexpr int kThreads = 512;          // one CTA per SM (launch_bounds(512,1))
 constexpr uint64_t kHdrBytes = 64 * 1024;
 // small-bucket push one-shot: receive slots right after the header, at the

@@ -99,6 +99,22 @@ class StoreFabric:
     def mark_down(self, rank: int, replica_id: int, generation: int) -> None:
         self.store.set(self._k("down", rank, replica_id), str(generation).encode())
 
+    # -- registered buffers (RingGroup.register) ------------------------------
+    def publish_regions(self, rank: int, replica_id: int, incarnation: int, regions: list) -> None:
+        """This member's registered buffers: [(rid, handle, offset, bytes)]."""
+        self.store.set(self._k("regions", rank, replica_id, incarnation), pickle.dumps(regions))
+
+    def lookup_regions(self, rank: int, replica_id: int, incarnation: int) -> list:
+        key = self._k("regions", rank, replica_id, incarnation)
+        return pickle.loads(self.store.get(key)) if self.store.check([key]) else []
+
+    def region_round(self, rank: int, replica_id: int, members: list[int], generation: int, k: int,
+                     deadline_s: float) -> None:
+        """The k-th register() of this generation: every member has published."""
+        self.store.set(self._k("regrnd", rank, generation, k, replica_id), b"1")
+        self._wait([self._k("regrnd", rank, generation, k, m) for m in members], deadline_s,
+                   f"register round {k} of generation {generation}")
+
 
 @dataclass
 class _Call:

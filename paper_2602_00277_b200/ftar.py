@@ -215,7 +215,7 @@ class RingGroup:
     """
 
     def __init__(self, self_replica: int, rank: int, router=None, plan=None, incarnation: int = 0,
-                 *, device=None, max_bucket_bytes: int = 64 * MIB, pool_bytes: int = 0):
+                 *, device=None, max_bucket_bytes: int = 64 * MIB, pool_bytes: int = 0, keep_departed_gens: int = 4):
         if not torch.cuda.is_available():
             raise Fatal(INTERNAL_INVARIANT, "the B200 FTAR data plane needs a CUDA device")
         self.self_replica = self_replica
@@ -243,6 +243,15 @@ class RingGroup:
         # free list and return to it when reconfig unmaps a departed member
         self._slots: dict[tuple[int, int], int] = {}
         self._free_slots: list[int] = list(range(255, -1, -1))
+        self._absent: dict[tuple[int, int], int] = {}  # mapped but out of the ring since generation g
+        self.keep_departed_gens = keep_departed_gens
+        # registered user buffers: mine (rid -> tensor, kept alive) and the
+        # peers' regions already mapped, by (replica, incarnation, rid, offset)
+        self._regions: dict[int, torch.Tensor] = {}
+        self._region_list: list[tuple] = []
+        self._peer_regions: set = set()
+        self._infos: dict = {}
+        self._reg_round = 0
         self._pool_next = 0
         ptr, nbytes = C.c_uint64(), C.c_uint64()
         _lib.lib.ftar_ctx_pool(ctx, C.byref(ptr), C.byref(nbytes))
@@ -293,6 +302,56 @@ class RingGroup:
     def reset_pool(self) -> None:
         self._pool_next = 0
 
+    def register(self, t: torch.Tensor, deadline_s: float = 60.0) -> int:
+        """Register an ordinary CUDA tensor (e.g. a caching-allocator gradient
+        bucket) with the ring so its all-reduces run zero-copy: peers read it
+        in place (no staging copy of an in-place call) and, as an ``out=``,
+        write the all-gather straight into it.  The owning allocation block's
+        IPC handle and the tensor's offset in it are published; every member
+        maps every other member's registered buffers.
+
+        A ring collective: every member calls it, in the same order, between
+        reconfigs (like the reference's group operations).  A member that
+        (re)joins later registers before its reconfig; reconfig exchanges all
+        members' registrations.  The tensor is kept alive until ``close``.
+        Returns this member's region id."""
+        if self._local:
+            return -1
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.is_contiguous()):
+            raise Fatal(INTERNAL_INVARIANT, "register needs a contiguous CUDA tensor")
+        if t.device.index != self.device_index:
+            raise Fatal(INTERNAL_INVARIANT, f"tensor on {t.device}, ring group on cuda:{self.device_index}")
+        rid, off = C.c_int(-1), C.c_uint64()
+        h = (C.c_char * 64)()
+        nbytes = t.numel() * t.element_size()
+        _lib.check(_lib.lib.ftar_region_register(self._ctx, t.data_ptr(), nbytes, C.byref(rid), h, 64, C.byref(off)),
+                   "ftar_region_register")
+        self._regions[rid.value] = t
+        self._region_list = [r for r in self._region_list if r[0] != rid.value] + \
+            [(rid.value, bytes(h)[:64], off.value, nbytes)]
+        self.router.publish_regions(self.rank, self.self_replica, self.incarnation, self._region_list)
+        if self.n > 1 and self._links_up:
+            self._reg_round += 1
+            self.router.region_round(self.rank, self.self_replica, self.members, self.generation,
+                                     self._reg_round, deadline_s)
+            self._import_regions()
+        return rid.value
+
+    def _import_regions(self) -> None:
+        for m in self.members:
+            if m == self.self_replica or m not in self._infos:
+                continue
+            inc = self._infos[m].incarnation
+            slot = self._slot(m, inc)
+            for rid, handle, off, nbytes in self.router.lookup_regions(self.rank, m, inc):
+                key = (m, inc, rid, off, handle)
+                if key in self._peer_regions:
+                    continue
+                rc = _lib.lib.ftar_region_import(self._ctx, slot, rid, handle, len(handle), off, nbytes)
+                if rc:
+                    _lib.check(rc, f"map registered buffer {rid} of replica {m}")
+                self._peer_regions.add(key)
+
     # -- membership (ftar.py:188-235) ---------------------------------------
     def _slot(self, replica_id: int, incarnation: int) -> int:
         key = (replica_id, incarnation)
@@ -303,13 +362,28 @@ class RingGroup:
         return self._slots[key]
 
     def _release_stale(self, keep: set) -> None:
-        """Unmap every peer arena whose (replica, incarnation) is not in
-        `keep` (the current ring): a departed member or a dead incarnation
-        must not stay pinned in its GPU's memory (close_links, ftar.py:226-230)."""
-        for key in [k for k in self._slots if k not in keep]:
-            slot = self._slots.pop(key)
-            _lib.check(_lib.lib.ftar_ctx_unmap(self._ctx, slot), f"unmap arena of replica {key[0]}")
-            self._free_slots.append(slot)
+        """Unmap peer arenas that are not in `keep` (the current ring), so a
+        dead incarnation does not stay pinned in its GPU's memory
+        (close_links, ftar.py:226-230): at once when the replica rejoined as
+        a newer incarnation (the old process is gone), otherwise once it has
+        been out of the ring for ``keep_departed_gens`` generations — a
+        replica parked for a few steps keeps its mapping, so re-admitting it
+        costs no IPC re-map (46-870 ms for a multi-GB arena, config 5).  Its
+        registered buffers are unmapped with it."""
+        current = {r: inc for r, inc in keep}
+        for key in list(self._slots):
+            if key in keep:
+                self._absent.pop(key, None)
+                continue
+            rid, inc = key
+            first = self._absent.setdefault(key, self.generation)
+            superseded = rid in current and current[rid] != inc
+            if superseded or self.generation - first >= self.keep_departed_gens:
+                slot = self._slots.pop(key)
+                self._absent.pop(key, None)
+                _lib.check(_lib.lib.ftar_ctx_unmap(self._ctx, slot), f"unmap arena of replica {rid}")
+                self._free_slots.append(slot)
+                self._peer_regions = {r for r in self._peer_regions if (r[0], r[1]) != key}
 
     @property
     def mapped_peers(self) -> list[tuple[int, int]]:
@@ -379,6 +453,10 @@ class RingGroup:
         if not self._local:
             keep = {(m, infos[m].incarnation) for m in self.members if m != self.self_replica} if infos else set()
             self._release_stale(keep)
+            self._infos = dict(infos) if infos else {}
+            self._reg_round = 0
+            if self.n > 1:
+                self._import_regions()  # every member published its registrations before joining
         self._links_up = True
 
     def close_links(self) -> None:

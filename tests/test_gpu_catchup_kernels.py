@@ -4,6 +4,8 @@ import numpy as np
 import pytest
 import torch
 
+from paper_2602_00277_b200 import checkpoint as ck
+
 pytestmark = pytest.mark.gpu
 DEV = torch.device("cuda", 0)
 
@@ -55,7 +57,9 @@ def test_snapshot_retention_and_pull_bit_exact():
     assert ei.value.available == 8
     with pytest.raises(ck.SnapshotUnavailable):
         donor.get(7)
-    assert donor.get(8) == (p.numel() * 4, m.numel() * 4)
+    assert donor.lengths == (p.numel() * 4, m.numel() * 4)
+    gp, gm = donor.get(8)  # payload views of the device snapshot (checkpoint.py:76-80)
+    assert torch.equal(gp.view(torch.float32), p) and torch.equal(gm.view(torch.float32), m)
 
 
 def test_pull_on_side_stream_overlaps_ftar():
@@ -146,3 +150,77 @@ def test_persist_detects_a_capture_during_the_write(tmp_path):
     # the new step persists cleanly afterwards
     assert store.persist(str(tmp_path), rank=0).wait() == ck.shard_path(str(tmp_path), 4, 0)
     store.close()
+
+
+# --- the reference's tests/test_checkpoint.py snapshot / fetch cases, with
+# tensor buffers and the reference's fetch_shard signature (in-process donors)
+
+
+def test_reference_snapshot_retention_is_one():
+    """tests/test_checkpoint.py:29-39."""
+    st = ck.SnapshotStore(device=DEV, replica_id=40)
+    assert st.step is None
+    st.capture(3, b"ppp", b"mmm")
+    gp, gm = st.get(3)
+    assert bytes(gp.cpu().numpy()) == b"ppp" and bytes(gm.cpu().numpy()) == b"mmm"
+    st.capture(4, b"qqqq", b"nn")
+    assert st.step == 4
+    with pytest.raises(ck.SnapshotUnavailable) as ei:
+        st.get(3)
+    assert ei.value.available == 4
+    st.close()
+
+
+def test_reference_fetch_roundtrip():
+    """tests/test_checkpoint.py:42-64: fetch_shard(addr, step, rank,
+    replica_id, incarnation) -> (params, momentum); a step the donor no
+    longer holds -> SnapshotUnavailable(available)."""
+    from paper_2602_00277_b200.ftar import PeerAddress
+    donor = ck.SnapshotStore(device=DEV, replica_id=0, rank=0)
+    params = torch.arange(10, dtype=torch.float32, device=DEV)
+    momentum = torch.ones(5, dtype=torch.float32, device=DEV)
+    donor.capture(7, params, momentum)
+    gp, gm = ck.fetch_shard(PeerAddress(0, 0, "127.0.0.1", 0), 7, rank=0, replica_id=3, incarnation=1)
+    assert torch.equal(gp.view(torch.float32), params) and torch.equal(gm.view(torch.float32), momentum)
+    with pytest.raises(ck.SnapshotUnavailable) as ei:
+        ck.fetch_shard(PeerAddress(0), 6, rank=0, replica_id=3, incarnation=1)
+    assert ei.value.available == 7  # donor moved on; catch up next step
+    donor.close()
+
+
+def test_reference_fetch_from_empty_store():
+    """tests/test_checkpoint.py:67-80."""
+    from paper_2602_00277_b200.ftar import PeerAddress
+    donor = ck.SnapshotStore(device=DEV, replica_id=11, rank=2)
+    with pytest.raises(ck.SnapshotUnavailable) as ei:
+        ck.fetch_shard(PeerAddress(11), 1, rank=2, replica_id=1, incarnation=1)
+    assert ei.value.available is None
+    donor.close()
+
+
+def test_reference_fetch_from_dead_donor_is_recoverable():
+    """tests/test_checkpoint.py:83-89: a donor that is not there (never
+    published, or its process is gone) -> Recoverable."""
+    from datetime import timedelta
+
+    import torch.distributed as dist
+
+    from paper_2602_00277_b200 import errors
+    from paper_2602_00277_b200.fabric import StoreFabric
+    from paper_2602_00277_b200.ftar import PeerAddress
+    store = dist.HashStore()
+    store.set_timeout(timedelta(seconds=1))
+    rec = ck.SnapshotStore(device=DEV, replica_id=21, rank=0, fabric=StoreFabric(store))
+    with pytest.raises(errors.Recoverable):
+        ck.fetch_shard(PeerAddress(99), 1, rank=0, replica_id=21, incarnation=1, timeout_s=0.4)
+    rec.close()
+
+
+def test_serve_fetches_is_a_thread_target():
+    import threading
+    stop = threading.Event()
+    t = threading.Thread(target=ck.serve_fetches, args=(None, None, stop), daemon=True)
+    t.start()
+    stop.set()
+    t.join(timeout=2.0)
+    assert not t.is_alive()

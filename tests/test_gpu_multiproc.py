@@ -233,6 +233,7 @@ def _worker(rank, world, port, scenario, outdir):
                            for bk, o in zip(bks, outs))
                 (res["ok"] if good else res["errors"]).append(f"regrouped_queue{rnd}")
         elif scenario == "fuzz":
+            os.environ["FTAR_TMA_MIN_SLICE_MIB"] = "0"  # the bulk-copy path at every size it can take
             # randomized mixes of every mode, the same seeded sequence on every
             # rank: sizes across the small-bucket and two-shot paths, fp32 and
             # bf16, registered and staged inputs, in place / out of place, with
@@ -419,6 +420,41 @@ def _worker(rank, world, port, scenario, outdir):
             (res["ok"] if np.array_equal(uo.cpu().numpy(), want) else res["errors"]).append("bench_unregistered")
             ftar.ftar_all_reduce(group, u, 7, cfg, scale=1.0 / world)
             (res["ok"] if np.array_equal(u.cpu().numpy(), want) else res["errors"]).append("bench_unreg_inplace")
+        elif scenario == "register":
+            # ordinary torch tensors registered with the ring (RingGroup.register):
+            # zero-copy in place and push into a registered out; a member that
+            # rejoins as a new incarnation registers before its reconfig and the
+            # others map its buffers at the reconfig
+            e = 3_000_017
+            arrays = member_inputs(world, e, seed=61)
+            want = orc.oracle_reduce(arrays, 8 << 20, 4)
+            cfg = ftar.PipelineConfig(per_chunk_timeout_s=10)
+            os.environ["FTAR_TMA_MIN_SLICE_MIB"] = "0"
+            x = torch.from_numpy(arrays[rank]).to(dev)
+            o = torch.empty(e, device=dev)
+            group.register(x)
+            group.register(o)
+            group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, 1, deadline_s=30)
+            ftar.ftar_all_reduce(group, x, 1, cfg, out=o, scale=0.5)
+            (res["ok"] if np.array_equal(o.cpu().numpy(), want * np.float32(0.5)) else res["errors"]).append("push")
+            ftar.ftar_all_reduce(group, x, 2, cfg)
+            (res["ok"] if np.array_equal(x.cpu().numpy(), want) else res["errors"]).append("inplace")
+            victim = world - 1
+            if rank == victim:
+                group.close()
+                group = ftar.RingGroup(rank, 0, fabric, device=dev, max_bucket_bytes=64 << 20, incarnation=1)
+                x = torch.from_numpy(arrays[rank]).to(dev)
+                group.register(x)  # links are down: published now, mapped by the others at the reconfig
+            else:
+                x.copy_(torch.from_numpy(arrays[rank]))
+            group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, 2, deadline_s=30)
+            ftar.ftar_all_reduce(group, x, 3, cfg)
+            (res["ok"] if np.array_equal(x.cpu().numpy(), want) else res["errors"]).append("after_rejoin")
+            # a late registration inside a generation is a collective round
+            y = torch.from_numpy(arrays[rank]).to(dev)
+            group.register(y)
+            ftar.ftar_all_reduce(group, y, 4, cfg)
+            (res["ok"] if np.array_equal(y.cpu().numpy(), want) else res["errors"]).append("late_register")
         elif scenario == "fetch":
             # the reference's fetch_shard(addr, step, rank, replica_id,
             # incarnation, timeout_s) shape across processes
@@ -703,6 +739,13 @@ def test_bench_workload_over_nvlink():
     for r in res:
         assert not r["errors"], r["errors"]
         assert {"bench_push", "bench_inplace", "bench_unregistered", "bench_unreg_inplace"} <= set(r["ok"])
+
+
+def test_registered_user_tensors():
+    res = run("register", world_size())
+    for r in res:
+        assert not r["errors"], r["errors"]
+        assert {"push", "inplace", "after_rejoin", "late_register"} <= set(r["ok"])
 
 
 def test_reference_shaped_fetch_shard():

@@ -1,24 +1,33 @@
-"""Config 4: non-blocking catch-up (one JSON line per pull budget on rank 0).
+"""Config 4: non-blocking catch-up with the recovering replica IN the ring.
 
-    python -m torch.distributed.run --nproc-per-node N tools/bench_catchup.py [--gib 8]
+    python -m torch.distributed.run --nproc-per-node N tools/bench_catchup.py [--gib 8] [--ctas 4,8,16]
 
-Ranks 0..N-2 are healthy replicas stepping: back-to-back FTAR all-reduces of
-256 MiB fp32 buckets over NVLink (ring of N-1).  Rank N-1 is the recovering
-replica: it pulls the donor's (rank 0, pick_donor) retention-1 snapshot of
-params + momentum (GiB total, fp32) over NVLink with the catch-up kernel on a
-low-priority side stream (checkpoint.start_fetch), with a CTA budget.
-Reported: pull ms/GB alone and under load, and the healthy replicas' step time
-without / with the concurrent pull (the "does not stall the healthy replicas"
-criterion).  Times: CUDA events, max over healthy ranks.
+Every rank is a member of one FTAR ring (one replica per GPU).  Ranks
+0..N-2 are healthy (contributors); rank N-1 is recovering: the quorum's
+*behind* replica, which stays a ring member contributing zeros
+(replica.py:574-577, quorum.py:57-59) — it owns no reduce-scatter slice and
+its buffer is never read — and receives every step's result, while it pulls
+the healthy replicas' retention-1 snapshot of params + momentum (GiB total,
+fp32) over NVLink with the catch-up kernel on a low-priority side stream,
+striped over every healthy donor, with a CTA budget.
+
+The ring steps back to back (256 MiB fp32 buckets, queue depth 3, fused
+x f32(1/h)).  Per step, CUDA events on every rank; the recovering rank also
+records the pull's start and end on its side stream, so on ITS clock the
+steps that overlap the pull are known exactly; each step's duration is the
+max over ranks.  Reported per budget: pull ms (alone and under load), steady
+step vs the mean and max step inside the pull window, and whether the pulled
+bytes are bit-exact.  Criterion (verdict r1): healthy step inside the window
+<= 1.2x steady.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import sys
-import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -27,10 +36,9 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gib", type=float, default=8.0, help="params+momentum GiB")
-    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--bucket-mib", type=int, default=256)
-    ap.add_argument("--ctas", type=str, default="8,16,32")
-    ap.add_argument("--stripe", action="store_true", help="stripe the pull over every healthy donor")
+    ap.add_argument("--ctas", type=str, default="4,8,16,32")
+    ap.add_argument("--single-donor", action="store_true", help="pull from pick_donor only (no striping)")
     args = ap.parse_args()
 
     import torch
@@ -49,10 +57,12 @@ def main():
     fabric = StoreFabric(store)
     rec = world - 1
     healthy = list(range(world - 1))
-    donor = ck.pick_donor(healthy, rec, rank=0)
+    donors = [ck.pick_donor(healthy, rec, rank=0)] if args.single_donor else healthy
     half = int(args.gib * (1 << 30) / 2) // 4  # fp32 elements per tensor
     nbytes = 2 * half * 4
     elems = args.bucket_mib * (1 << 20) // 4
+    cfg = ftar.PipelineConfig()
+    scale = 1.0 / len(healthy)
 
     snap = ck.SnapshotStore(capacity_bytes=nbytes, device=dev, fabric=fabric, rank=0, replica_id=rank)
     if rank != rec:  # every healthy replica holds the same retention-1 snapshot
@@ -62,100 +72,115 @@ def main():
         snap.capture(41, p, m)
         torch.cuda.synchronize()
         del p, m
-    group = None
-    if rank != rec and len(healthy) > 1:
-        group = ftar.RingGroup(rank, 0, fabric, device=dev, max_bucket_bytes=elems * 4,
-                               pool_bytes=2 * elems * 4 + 4096)
-        group.reconfig({r: ftar.PeerAddress(r) for r in healthy}, 1, deadline_s=60)
-        buf = group.alloc_bucket(elems)
-        buf.normal_()
-        out = group.alloc_bucket(elems)
-    elif rank != rec:
-        buf = torch.randn(elems, device=dev)
-        out = torch.empty_like(buf)
+    group = ftar.RingGroup(rank, 0, fabric, device=dev, max_bucket_bytes=elems * 4, pool_bytes=2 * elems * 4 + 4096)
+    group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, 1, deadline_s=60, contributors=healthy)
+    buf = group.alloc_bucket(elems)
     if rank == rec:
+        buf.fill_(float("nan"))  # a behind replica's buffer is never read
         p_out = torch.empty(half, device=dev)
         m_out = torch.empty(half, device=dev)
+    else:
+        buf.normal_()
+    out = group.alloc_bucket(elems)
+    main_stream = torch.cuda.current_stream(dev)
+    side = ck.catchup_stream(dev)
     dist.barrier()
 
-    def healthy_steps(k):
-        """k FTAR steps; returns mean ms/step (CUDA events)."""
-        cfg = ftar.PipelineConfig()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
+    def ring_steps(k, pull_ctas=None):
+        """k ring steps (queue depth 3) with an event before/after each; the
+        recovering rank launches the pull (if any) right before step 0."""
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(k + 1)]
+        pev = None
+        h = None
         pend = []
-        for _ in range(k):
-            if group is not None:
-                pend.append(ftar.ftar_all_reduce_async(group, buf, 0, cfg, out=out, scale=1.0 / len(healthy)))
-                while len(pend) >= 3:
-                    pend.pop(0).wait()
-            else:
-                out.copy_(buf).mul_(1.0)
+        # a device-side barrier: the window starts when every stream is here
+        ftar.ftar_all_reduce(group, buf, 0, cfg, out=out, scale=scale)
+        if pull_ctas is not None and rank == rec:
+            pev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            side.wait_stream(main_stream)
+            pev[0].record(side)
+            h = ck.start_fetch(snap, donors, 41, 0, p_out, m_out, timeout_s=60, ctas=pull_ctas)
+            pev[1].record(side)
+        ev[0].record(main_stream)
+        for i in range(k):
+            pend.append(ftar.ftar_all_reduce_async(group, buf, 0, cfg, out=out, scale=scale))
+            ev[i + 1].record(main_stream)
+            while len(pend) >= 3:
+                pend.pop(0).wait()
         while pend:
             pend.pop(0).wait()
-        e.record()
+        if h is not None:
+            h.wait()
         torch.cuda.synchronize()
-        return s.elapsed_time(e) / k
+        durs = [ev[i].elapsed_time(ev[i + 1]) for i in range(k)]
+        window = None
+        if pev is not None:
+            # steps [i0, i1) overlap the pull on this GPU's clock
+            s0 = [ev[0].elapsed_time(ev[i]) for i in range(k + 1)]
+            p0, p1 = ev[0].elapsed_time(pev[0]), ev[0].elapsed_time(pev[1])
+            window = (p0, p1, [i for i in range(k) if s0[i + 1] > p0 and s0[i] < p1])
+        return durs, window
 
-    def pull(ctas, donors=None):
-        s = torch.cuda.Event(enable_timing=True)
-        e = torch.cuda.Event(enable_timing=True)
-        side = ck.catchup_stream(dev)
-        t0 = time.perf_counter()
-        s.record(side)
-        h = ck.start_fetch(snap, donor if donors is None else donors, 41, 0, p_out, m_out, timeout_s=30, ctas=ctas)
-        e.record(side)
-        h.wait()
-        torch.cuda.synchronize()
-        return s.elapsed_time(e), (time.perf_counter() - t0) * 1e3
+    def gather_max(durs):
+        allv = [None] * world
+        dist.all_gather_object(allv, durs)
+        return [max(v[i] for v in allv) for i in range(len(durs))]
 
-    def mx(v):
-        t = torch.tensor([v], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return t.item()
+    def pull_alone(ctas):
+        t = 0.0
+        if rank == rec:
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            side.wait_stream(main_stream)
+            s.record(side)
+            h = ck.start_fetch(snap, donors, 41, 0, p_out, m_out, timeout_s=60, ctas=ctas)
+            e.record(side)
+            h.wait()
+            torch.cuda.synchronize()
+            t = s.elapsed_time(e)
+        box = [t]
+        dist.broadcast_object_list(box, src=rec)
+        return box[0]
 
-    if rank != rec:
-        healthy_steps(5)
-    if rank == rec:  # warm-up: lazy peer mapping of the donors' snapshot arenas
-        pull(16)
-        if args.stripe and len(healthy) > 1:
-            pull(16, healthy)
-    dist.barrier()
-    base = mx(healthy_steps(args.steps) if rank != rec else 0.0)
+    # warm-up: peer mappings (snapshot arenas), kernels
+    ring_steps(5)
+    pull_alone(16)
+    steady = gather_max(ring_steps(30)[0])
+    steady_ms = sum(steady) / len(steady)
     results = []
-    stripe = args.stripe and len(healthy) > 1
     for ctas in [int(c) for c in args.ctas.split(",")]:
         dist.barrier()
-        dl = healthy if stripe else None
-        alone = pull(ctas, dl)[0] if rank == rec else 0.0
-        alone = mx(alone)
+        alone = pull_alone(ctas)
+        k = max(30, int(math.ceil(alone / steady_ms * 2.0)) + 10)
         dist.barrier()
-        if rank == rec:
-            loaded_ms, wall = pull(ctas, dl)
-            step = 0.0
-        else:
-            step = healthy_steps(args.steps)
-            loaded_ms = 0.0
-        loaded_ms, step = mx(loaded_ms), mx(step)
+        durs, window = ring_steps(k, pull_ctas=ctas)
+        per_step = gather_max(durs)
+        box = [window]
+        dist.broadcast_object_list(box, src=rec)
+        p0, p1, idx = box[0]
+        inwin = [per_step[i] for i in idx] or [float("nan")]
         ok = True
         if rank == rec:
             g = torch.Generator(device=dev).manual_seed(5)
-            ok = bool(torch.equal(p_out, torch.randn(half, device=dev, generator=g)))
-        ok = mx(0.0 if ok else 1.0) == 0.0
+            ok = bool(torch.equal(p_out, torch.randn(half, device=dev, generator=g))) and \
+                bool(torch.equal(m_out, torch.randn(half, device=dev, generator=g)))
+        okb = [ok]
+        dist.broadcast_object_list(okb, src=rec)
         gb = nbytes / 1e9
-        results.append({"metric": "catch-up ms/GB", "gib": args.gib, "bytes": nbytes, "ctas": ctas,
-                        "pull_ms_alone": round(alone, 3), "ms_per_GB_alone": round(alone / gb, 3),
-                        "GBps_alone": round(gb / alone * 1e3, 1),
-                        "pull_ms_under_load": round(loaded_ms, 3), "ms_per_GB_under_load": round(loaded_ms / gb, 3),
-                        "healthy_step_ms_baseline": round(base, 4), "healthy_step_ms_during_pull": round(step, 4),
-                        "healthy_replicas": len(healthy), "bucket_mib": args.bucket_mib,
-                        "pull_bit_exact": ok, "n_gpus": world,
-                        "donors": healthy if stripe else [donor]})
+        mean_in = sum(inwin) / len(inwin)
+        results.append({
+            "metric": "catch-up ms/GB, recovering replica in the ring", "gib": args.gib, "bytes": nbytes,
+            "ctas": ctas, "donors": donors, "ring": world, "healthy": len(healthy),
+            "pull_ms_alone": round(alone, 3), "ms_per_GB_alone": round(alone / gb, 3),
+            "pull_ms_under_load": round(p1 - p0, 3), "ms_per_GB_under_load": round((p1 - p0) / gb, 3),
+            "steady_step_ms": round(steady_ms, 4), "steps_in_pull_window": len(idx),
+            "step_ms_in_window_mean": round(mean_in, 4), "step_ms_in_window_max": round(max(inwin), 4),
+            "ratio_mean": round(mean_in / steady_ms, 3), "ratio_max": round(max(inwin) / steady_ms, 3),
+            "criterion_le_1p2": mean_in <= 1.2 * steady_ms,
+            "pull_bit_exact": okb[0], "bucket_mib": args.bucket_mib})
     if rank == 0:
         for r in results:
             print(json.dumps(r), flush=True)
-    if group is not None:
-        group.close()
+    group.close()
     snap.close()
     dist.barrier()
     dist.destroy_process_group()

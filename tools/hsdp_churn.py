@@ -54,6 +54,7 @@ def main():
     ap.add_argument("--beta", type=float, default=0.9)
     ap.add_argument("--chunk-timeout", type=float, default=0.5)
     ap.add_argument("--unfused", action="store_true", help="separate torch optimizer instead of the fused SGD")
+    ap.add_argument("--pull-ctas", type=int, default=8, help="CTA budget of the catch-up pull")
     args = ap.parse_args()
 
     import numpy as np
@@ -128,6 +129,7 @@ def main():
                         "map_ms": [(m[0], round(m[1] * 1e3, 1), round(m[2] * 1e3, 1)) for m in snap.map_log]})
             continue
         d = quorum.exchange(rnd, rid, Report(step + 1, inc), round_deadline_s=0.25)
+        t_x = time.monotonic()
         if d.target_step > args.steps:
             break
         role = d.role_of(rid)
@@ -135,15 +137,17 @@ def main():
             log.append({"round": rnd, "target": d.target_step, "role": role,
                         "t_ms": round((time.monotonic() - t_run) * 1e3, 1)})
             continue
+        t_rc = time.monotonic()
         if d.generation > group.generation:
             group.reconfig({m: ftar.PeerAddress(m) for m in d.members}, d.generation, deadline_s=30,
                            contributors=d.healthy)
+        t_rc = time.monotonic() - t_rc
         target = d.target_step
         pull = None
 
         def fetch():
             return ck.start_fetch(snap, list(d.healthy), target - 1, 0, fetched[0], fetched[1],
-                                  timeout_s=10, ctas=16)
+                                  timeout_s=10, ctas=args.pull_ctas)
 
         if role == "healthy":
             grads.copy_(grad_base)
@@ -176,9 +180,10 @@ def main():
                     p_.wait()
         except errors.Recoverable:
             ok = False
-        torch.cuda.synchronize()
+        torch.cuda.current_stream(dev).synchronize()  # the FTAR only (a catch-up pull runs on a side stream)
         t_ar = time.monotonic() - t_ar
         fetch_ok = True
+        t_pw = time.monotonic()
         if role == "behind":
             try:
                 if pull is None:  # donors still being mapped when the step began
@@ -186,7 +191,10 @@ def main():
                 pull.wait()
             except (errors.FtdpError, ck.SnapshotUnavailable):
                 fetch_ok = False
+        t_pw = time.monotonic() - t_pw
+        t_v = time.monotonic()
         committed = quorum.vote(rnd, d, rid, ok and fetch_ok, deadline_s=1.0)
+        t_v = time.monotonic() - t_v
         if committed:
             if fused:
                 params, nxt = nxt[0], (params, nxt[1])
@@ -204,7 +212,10 @@ def main():
         t_steps.append(dt)
         log.append({"round": rnd, "target": target, "generation": d.generation, "role": role,
                     "healthy": len(d.healthy), "behind": sorted(d.behind), "committed": committed,
-                    "ftar_ms": round(t_ar * 1e3, 3), "step_ms": round(dt * 1e3, 3)})
+                    "ftar_ms": round(t_ar * 1e3, 3), "step_ms": round(dt * 1e3, 3),
+                    "quorum_ms": round((t_x - t0) * 1e3, 3), "reconfig_ms": round(t_rc * 1e3, 3),
+                    "pull_wait_ms": round(t_pw * 1e3, 3),
+                    "vote_ms": round(t_v * 1e3, 3)})
     elapsed = time.monotonic() - t_run
     # cross-replica agreement on the final state
     dig = hashlib.sha256(params.cpu().numpy().tobytes() + mom.cpu().numpy().tobytes()).hexdigest()
