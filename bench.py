@@ -281,9 +281,14 @@ class NvlinkPM:
     timer while the kernels run concurrently.  The measured traffic behind
     roofline.traffic for N >= 2 (NVML's NVLink fields are N/A on this driver)."""
 
-    def __init__(self, cuda_index: int, interval_ns: int = 50_000):
+    NVLINK = ("nvlrx__bytes.sum", "nvltx__bytes.sum", "nvlrx__bytes_data_user.sum", "nvltx__bytes_data_user.sum")
+    KEYS = ("rx", "tx", "rx_user", "tx_user")
+
+    def __init__(self, cuda_index: int, interval_ns: int = 50_000, metrics=None, keys=None):
         import ctypes as C
         self.dev, self.lib, self.err = cuda_index, None, None
+        self.metrics = tuple(metrics or self.NVLINK)
+        self.keys = tuple(keys or self.KEYS)
         path = os.path.join(ROOT, "tools", "_build", "libnvlink_pm.so")
         try:
             if not os.path.exists(path):
@@ -293,10 +298,10 @@ class NvlinkPM:
                                 "-o", path], check=True, capture_output=True, timeout=120)
             lib = C.CDLL(path)
             lib.nvpm_error.restype = C.c_char_p
-            lib.nvpm_open.argtypes = [C.c_int, C.c_uint64, C.c_uint32]
+            lib.nvpm_open.argtypes = [C.c_int, C.c_uint64, C.c_uint32, C.c_char_p]
             lib.nvpm_stop.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_uint64),
                                       C.POINTER(C.c_int)]
-            if lib.nvpm_open(cuda_index, interval_ns, 200_000):
+            if lib.nvpm_open(cuda_index, interval_ns, 200_000, ",".join(self.metrics).encode()):
                 self.err = lib.nvpm_error().decode()
             else:
                 self.lib = lib
@@ -313,13 +318,14 @@ class NvlinkPM:
         import ctypes as C
         if self.lib is None:
             return None
-        out = (C.c_double * 4)()
+        out = (C.c_double * 8)()
         n, span, ovf = C.c_int(), C.c_uint64(), C.c_int()
         if self.lib.nvpm_stop(self.dev, out, C.byref(n), C.byref(span), C.byref(ovf)):
             self.err = self.lib.nvpm_error().decode()
             return None
-        return {"rx": out[0], "tx": out[1], "rx_user": out[2], "tx_user": out[3], "samples": n.value,
-                "span_ms": span.value / 1e6, "overflow": bool(ovf.value)}
+        r = {k: out[i] for i, k in enumerate(self.keys)}
+        r.update({"samples": n.value, "span_ms": span.value / 1e6, "overflow": bool(ovf.value)})
+        return r
 
     def close(self):
         if self.lib is not None:
@@ -409,8 +415,17 @@ def run_single(args):
         for b, h in zip(bufs, hosts):
             b.copy_(h)
     torch.cuda.synchronize()
+    # live DRAM traffic of the timed calls (CUPTI PM sampling; the window
+    # holds only this kernel: inputs are resident, nothing else runs)
+    pm = None if args.no_pm else NvlinkPM(0, metrics=("dram__bytes_read.sum", "dram__bytes_write.sum"),
+                                          keys=("read", "write"))
     with ClockSampler(0) as clk:
+        if pm is not None:
+            pm.start()
         total, per_launch = timed_loop(step, args.steps, stream, torch, drain=drain)
+        pmw = pm.stop() if pm is not None else None
+    if pm is not None:
+        pm.close()
     t_step = total / args.steps
     after = None if args.inplace else [digest(o) for o in outs]
     parity = {"checked": "every replica's output of one call (before the timed region) vs the oracle digest"
@@ -423,7 +438,12 @@ def run_single(args):
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     roof = {"bound": "hbm", "achieved": round(alg_bytes / per_launch / 1e9, 1), "peak": hbm_peak,
             "unit": "GB/s", "frac": round(alg_bytes / per_launch / 1e9 / hbm_peak, 4),
-            "traffic": args.traffic if args.traffic is not None else _ncu_traffic(args),
+            "traffic": (round((pmw["read"] + pmw["write"]) / args.steps) if pmw is not None
+                        else args.traffic if args.traffic is not None else _ncu_traffic(args)),
+            "traffic_source": ("dram__bytes_read.sum + dram__bytes_write.sum per launch over the timed calls, "
+                               "CUPTI PM sampling (live)" if pmw is not None
+                               else "committed ncu capture (profiles/r01/ncu): " + str(pm.err if pm else "pm off")),
+            "pm_window": pmw,
             "kernel": "local_oneshot_kernel",
             "algorithmic_bytes_per_launch": alg_bytes,
             "definition": "n*E*(in_bytes+4): every replica's bucket read once, every replica's fp32 result "

@@ -276,6 +276,10 @@ int ftar_snap_pull_multi_launch(ftar_snap* local, const int* slots, int nslots,
                                 const ftar_snap* src_local, uint64_t want_step, void* dst_params,
                                 uint64_t pbytes, void* dst_momentum, uint64_t mbytes, int ctas,
                                 void* stream);
+/* Widen the pull in flight: a second grid of `ctas` CTAs on `stream` claims
+ * chunks from the same counter (a catch-up runs narrow while the step's
+ * collectives need NVLink, then wide).  No-op when the pull has finished. */
+int ftar_snap_pull_boost(ftar_snap* local, int ctas, void* stream);
 int ftar_snap_poll(ftar_snap* s, int* status, uint64_t* progress, int64_t* available);
 int ftar_snap_abort(ftar_snap* s);
 int ftar_snap_wait(ftar_snap* s, double progress_timeout_s, int64_t* available);

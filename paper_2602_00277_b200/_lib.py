@@ -77,6 +77,7 @@ SIGNATURES = {
     "ftar_snap_pull_launch": (i32, [c_snap_p, i32, c_snap_p, u64, vp, u64, vp, u64, i32, vp]),
     "ftar_snap_pull_multi_launch": (i32, [c_snap_p, C.POINTER(i32), i32, c_snap_p, u64, vp, u64, vp, u64, i32, vp]),
     "ftar_snap_poll": (i32, [c_snap_p, C.POINTER(i32), C.POINTER(u64), C.POINTER(i64)]),
+    "ftar_snap_pull_boost": (i32, [c_snap_p, i32, vp]),
     "ftar_snap_abort": (i32, [c_snap_p]),
     "ftar_snap_wait": (i32, [c_snap_p, dbl, C.POINTER(i64)]),
     "ftar_probe_copy": (i32, [vp, vp, u64, i32, vp]),

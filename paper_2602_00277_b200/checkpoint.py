@@ -305,6 +305,14 @@ class CatchupPull:
         self.timeout_s = timeout_s
         self.event = None
 
+    def boost(self, ctas: int = 32) -> None:
+        """Widen the pull now (e.g. once this step's collectives are done): a
+        second grid on another low-priority stream takes over part of the
+        remaining chunks."""
+        stream = catchup_stream(self.local.device, 1)
+        _lib.check(_lib.lib.ftar_snap_pull_boost(self.local.handle, ctas, stream.cuda_stream), "ftar_snap_pull_boost")
+        self.streams = getattr(self, "streams", [self.stream]) + [stream]
+
     def poll(self):
         st, prog, avail = C.c_int(), C.c_uint64(), C.c_int64()
         _lib.lib.ftar_snap_poll(self.local.handle, C.byref(st), C.byref(prog), C.byref(avail))
@@ -318,7 +326,8 @@ class CatchupPull:
         if st:
             raise from_status(st, _lib.last_error() if st == 10 else "catch-up pull failed")
         # make the consumer stream see the pulled bytes
-        torch.cuda.current_stream(self.local.device).wait_stream(self.stream)
+        for s in getattr(self, "streams", [self.stream]):
+            torch.cuda.current_stream(self.local.device).wait_stream(s)
         return self.params, self.momentum
 
 
@@ -326,16 +335,16 @@ def _lib_status(name: str) -> int:
     return {"UNAVAILABLE": 9}[name]
 
 
-_side_streams: dict[int, torch.cuda.Stream] = {}
+_side_streams: dict[tuple[int, int], torch.cuda.Stream] = {}
 
 
-def catchup_stream(device: torch.device) -> torch.cuda.Stream:
-    """A low-priority side stream per device for catch-up pulls."""
+def catchup_stream(device: torch.device, which: int = 0) -> torch.cuda.Stream:
+    """Low-priority side streams per device for catch-up pulls (1: boost grids)."""
     idx = device.index if device.index is not None else torch.cuda.current_device()
-    if idx not in _side_streams:
+    if (idx, which) not in _side_streams:
         lo, hi = torch.cuda.Stream.priority_range()
-        _side_streams[idx] = torch.cuda.Stream(device=idx, priority=lo if lo > hi else 0)
-    return _side_streams[idx]
+        _side_streams[(idx, which)] = torch.cuda.Stream(device=idx, priority=lo if lo > hi else 0)
+    return _side_streams[(idx, which)]
 
 
 # CTA budget of a catch-up pull: each CTA streams ~47 GB/s (bulk copies), so 8
@@ -369,6 +378,7 @@ def start_fetch(local: SnapshotStore, donor, step: int, rank: int, params_out: t
         slots, src = [local._map_donor(int(d), rank, timeout_s) for d in donors], None
     stream = catchup_stream(local.device)
     stream.wait_stream(torch.cuda.current_stream(local.device))
+    stream.wait_stream(catchup_stream(local.device, 1))  # a previous pull's boost grid has exited
     arr = (C.c_int * max(1, len(slots)))(*slots)
     rc = _lib.lib.ftar_snap_pull_multi_launch(local.handle, arr, len(slots), src, step, p.data_ptr(), pb,
                                               m.data_ptr(), mb, ctas, stream.cuda_stream)

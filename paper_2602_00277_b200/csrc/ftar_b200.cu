@@ -1906,16 +1906,37 @@ struct BulkStream {  // thread 0's pipeline state
   }
 };
 
+// Pull kernel.  Chunks are CLAIMED from lhdr->next_chunk (atomicAdd), not
+// assigned by block index, so ftar_snap_pull_boost can launch a second grid
+// of the same pull that takes over part of what is left: a catch-up runs at a
+// small CTA budget while the step's collectives need the links, then at full
+// width.  Each CTA adds the chunks it claimed to chunks_done once they have
+// landed; the CTA that completes the count validates every donor's seqlock
+// and publishes `done`.  (ftar_snap_pull_multi_launch resets the counters on
+// the pull stream before the first grid.)
+__global__ void snap_pull_reset_kernel(SnapHdr* h) {
+  h->next_chunk = 0;
+  h->chunks_done = 0;
+  h->err = 0;
+  for (int d = 0; d < kMaxMembers; ++d) {
+    h->seq_min[d] = ~0ull;
+    h->seq_max[d] = 0;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
 snap_pull_kernel(const __grid_constant__ PullSrcs src, SnapHdr* lhdr, HostCtl* ctl, uint64_t tag, int64_t want,
                  char* dp, uint64_t pb, char* dm, uint64_t mb, int bulk) {
   __shared__ uint32_t s_st;
+  __shared__ uint64_t s_c;
   extern __shared__ __align__(1024) char psmem[];
   const int tid = threadIdx.x;
   if (bulk && tid == 0) {
     for (uint32_t i = 0; i < kPullStages; ++i) mbar_init(reinterpret_cast<uint64_t*>(psmem) + i, 1);
     fence_mbar_init();
   }
+  const uint64_t total = pb + mb;
+  const uint64_t nchunks = (total + kPullChunk - 1) / kPullChunk;
   if (tid == 0) {
     if (blockIdx.x == 0) ctl->started = tag;
     s_st = ST_OK;
@@ -1926,25 +1947,33 @@ snap_pull_kernel(const __grid_constant__ PullSrcs src, SnapHdr* lhdr, HostCtl* c
       const uint64_t spb = ld_relaxed_sys(&sh->pbytes), smb = ld_relaxed_sys(&sh->mbytes);
       if ((seq & 1u) || step != want || spb != pb || smb != mb) {
         s_st = ST_UNAVAILABLE;
-        if (blockIdx.x == 0) ctl->available = (seq & 1u) ? -1 : step;
+        ctl->available = (seq & 1u) ? -1 : step;
       }
       atomicMin(reinterpret_cast<unsigned long long*>(&lhdr->seq_min[d]), (unsigned long long)seq);
       atomicMax(reinterpret_cast<unsigned long long*>(&lhdr->seq_max[d]), (unsigned long long)seq);
     }
   }
   __syncthreads();
-  const uint64_t total = pb + mb;
-  const uint64_t nchunks = (total + kPullChunk - 1) / kPullChunk;
-  if (s_st == ST_OK && bulk) {
+  uint64_t mine = 0;  // chunks this CTA claimed (thread 0)
+  auto claim = [&]() -> uint64_t {  // thread 0
+    if (s_st != ST_OK || ctl->abort_tag == tag || ld_relaxed_sys32(&lhdr->err) != 0) {
+      if (s_st == ST_OK) s_st = ST_ABORTED;
+      // take everything left so the count still completes
+      const uint64_t k = atomicExch(reinterpret_cast<unsigned long long*>(&lhdr->next_chunk),
+                                    (unsigned long long)nchunks);
+      if (k < nchunks) mine += nchunks - k;
+      return nchunks;
+    }
+    const uint64_t c = atomicAdd(reinterpret_cast<unsigned long long*>(&lhdr->next_chunk), 1ull);
+    if (c < nchunks) ++mine;
+    return c;
+  };
+  if (bulk) {
     if (tid == 0) {
       BulkStream bs;
       bs.smem = psmem;
       uint32_t it = 0;
-      for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
-        if ((it & 7u) == 0 && (ctl->abort_tag == tag || ld_relaxed_sys32(&lhdr->err) != 0)) {
-          s_st = ST_ABORTED;
-          break;
-        }
+      for (uint64_t c = claim(); c < nchunks; c = claim(), ++it) {
         const char* data = src.arena[c % (uint64_t)src.n] + kSnapHdrBytes;
         const uint64_t a = c * kPullChunk, b = umin(a + kPullChunk, total);
         if (a < pb) bs.copy(dp + a, data + a, umin(b, pb) - a);
@@ -1956,24 +1985,21 @@ snap_pull_kernel(const __grid_constant__ PullSrcs src, SnapHdr* lhdr, HostCtl* c
       }
       bs.flush();  // every copy landed (also on abort: nothing may write smem after exit)
     }
-  } else if (s_st == ST_OK) {
+  } else {
     uint32_t it = 0;
-    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
-      if ((it & 7u) == 0) {  // abort word lives in host memory: check every 8 chunks
-        if (tid == 0 && (ctl->abort_tag == tag || ld_relaxed_sys32(&lhdr->err) != 0)) s_st = ST_ABORTED;
-        __syncthreads();
-        if (s_st != ST_OK) break;
-      }
+    for (;; ++it) {
+      if (tid == 0) s_c = claim();
+      __syncthreads();
+      const uint64_t c = s_c;
+      __syncthreads();
+      if (c >= nchunks) break;
       const char* data = src.arena[c % (uint64_t)src.n] + kSnapHdrBytes;
       const uint64_t a = c * kPullChunk, b = umin(a + kPullChunk, total);
       // a chunk may straddle params|momentum
-      if (a < pb) {
-        const uint64_t e = umin(b, pb);
-        copy_bytes_grid(dp + a, data + a, e - a, tid, kThreads);
-      }
+      if (a < pb) copy_bytes_grid(dp + a, data + a, umin(b, pb) - a, tid, kThreads);
       if (b > pb) {
-        const uint64_t s = umax(a, pb);
-        copy_bytes_grid(dm + (s - pb), data + s, b - s, tid, kThreads);
+        const uint64_t s0 = umax(a, pb);
+        copy_bytes_grid(dm + (s0 - pb), data + s0, b - s0, tid, kThreads);
       }
       if (tid == 0 && (it & 7u) == 7u) ctl->progress = ((uint64_t)blockIdx.x << 32) | it;
     }
@@ -1986,9 +2012,12 @@ snap_pull_kernel(const __grid_constant__ PullSrcs src, SnapHdr* lhdr, HostCtl* c
       atomicMax(reinterpret_cast<unsigned long long*>(&lhdr->seq_max[d]), (unsigned long long)seq2);
     }
     if (s_st != ST_OK) atomicMax(&lhdr->err, s_st);
-    __threadfence();
-    const uint32_t old = atomicAdd(&lhdr->done_arrive, 1u);
-    if (old == gridDim.x - 1) {
+    __threadfence();  // my chunks (and my err / seq words) before the count
+    const uint64_t old = mine ? atomicAdd(reinterpret_cast<unsigned long long*>(&lhdr->chunks_done),
+                                          (unsigned long long)mine)
+                              : nchunks + 1;
+    const bool finisher = (old < nchunks && old + mine >= nchunks) || (nchunks == 0 && blockIdx.x == 0);
+    if (finisher) {
       __threadfence_system();
       uint32_t err = ld_relaxed_sys32(&lhdr->err);
       for (int d = 0; d < src.n; ++d) {
@@ -1998,13 +2027,8 @@ snap_pull_kernel(const __grid_constant__ PullSrcs src, SnapHdr* lhdr, HostCtl* c
           const SnapHdr* sh = reinterpret_cast<const SnapHdr*>(src.arena[d]);
           ctl->available = (int64_t)ld_relaxed_sys(reinterpret_cast<const uint64_t*>(&sh->step));
         }
-        lhdr->seq_min[d] = ~0ull;
-        lhdr->seq_max[d] = 0;
       }
       ctl->progress = total;
-      lhdr->err = 0;
-      lhdr->done_arrive = 0;
-      lhdr->bytes_done = 0;
       __threadfence_system();
       ctl->done = mk_flag(tag, err);
     }
@@ -2506,12 +2530,24 @@ struct ftar_ctx {
   }
 };
 
+struct PullArgs {
+  PullSrcs src;
+  int64_t want;
+  char* dp;
+  uint64_t pb;
+  char* dm;
+  uint64_t mb;
+  int bulk;
+};
+
 struct ftar_snap {
   int device = 0;
   char* arena = nullptr;
   uint64_t cap = 0;
   HostCtl* ctl_h = nullptr;
   HostCtl* ctl_d = nullptr;
+  PullArgs last{};  // the pull in flight (ftar_snap_pull_boost relaunches it)
+  cudaEvent_t reset_done = nullptr;  // the pull's counters are reset (a boost grid waits for it)
   char* peer[kMaxSlots] = {};
   cudaIpcMemHandle_t peer_handle[kMaxSlots] = {};
   uint64_t seq = 0;
@@ -3844,6 +3880,7 @@ int ftar_snap_destroy(ftar_snap* s) {
   cudaDeviceSynchronize();
   for (int i = 0; i < kMaxSlots; ++i)
     if (s->peer[i]) cudaIpcCloseMemHandle(s->peer[i]);
+  if (s->reset_done) cudaEventDestroy(s->reset_done);
   cudaFree(s->arena);
   cudaFreeHost((void*)s->ctl_h);
   delete s;
@@ -3989,6 +4026,9 @@ int ftar_snap_pull_multi_launch(ftar_snap* local, const int* slots, int nslots, 
   local->cur_tag = tag;
   local->inflight = true;
   const int G = std::max(1, ctas);
+  snap_pull_reset_kernel<<<1, 1, 0, st>>>(reinterpret_cast<SnapHdr*>(local->arena));
+  if (!local->reset_done) CK(cudaEventCreateWithFlags(&local->reset_done, cudaEventDisableTiming));
+  CK(cudaEventRecord(local->reset_done, st));
   // the bulk-copy pull when every region is 16-byte aligned (FTAR_TMA=0: register copy)
   const int bulk = tma_on() && (pbytes % 16 == 0) && (mbytes % 16 == 0) &&
                    ((reinterpret_cast<uint64_t>(dst_params) | reinterpret_cast<uint64_t>(dst_momentum)) % 16 == 0);
@@ -4003,11 +4043,29 @@ int ftar_snap_pull_multi_launch(ftar_snap* local, const int* slots, int nslots, 
   snap_pull_kernel<<<G, kThreads, bulk ? kPullSmem : 0, st>>>(
       src, reinterpret_cast<SnapHdr*>(local->arena), local->ctl_d, tag, (int64_t)want_step,
       static_cast<char*>(dst_params), pbytes, static_cast<char*>(dst_momentum), mbytes, bulk);
+  local->last = {src, (int64_t)want_step, static_cast<char*>(dst_params), pbytes, static_cast<char*>(dst_momentum),
+                 mbytes, bulk};
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     local->inflight = false;
     return cuda_fail(e, "snapshot pull launch");
   }
+  return FTAR_OK;
+}
+
+int ftar_snap_pull_boost(ftar_snap* local, int ctas, void* stream) {
+  // A second grid for the pull in flight, on another stream: its CTAs claim
+  // chunks from the same counter, so the remaining transfer widens at once.
+  // A no-op when the pull already finished.
+  if (!local) return fail(FTAR_ST_INVARIANT, "null snapshot");
+  if (!local->inflight || flag_tag(local->ctl_h->done) == local->cur_tag) return FTAR_OK;
+  DeviceGuard g(local->device);
+  const PullArgs& a = local->last;
+  CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), local->reset_done, 0));  // not on the first grid
+  snap_pull_kernel<<<std::max(1, ctas), kThreads, a.bulk ? kPullSmem : 0, static_cast<cudaStream_t>(stream)>>>(
+      a.src, reinterpret_cast<SnapHdr*>(local->arena), local->ctl_d, local->cur_tag, a.want, a.dp, a.pb, a.dm, a.mb,
+      a.bulk);
+  CK(cudaGetLastError());
   return FTAR_OK;
 }
 

@@ -134,6 +134,8 @@ struct alignas(128) SnapHdr {
   alignas(128) uint64_t seq_min[kMaxMembers], seq_max[kMaxMembers];  // pull-side, per donor (local)
   uint32_t done_arrive, err;
   uint64_t bytes_done;
+  alignas(128) uint64_t next_chunk;   // pull-side: chunks are claimed from this counter, so a
+  uint64_t chunks_done;               // second (boost) launch shares the remaining work
 };
 constexpr uint64_t kSnapHdrBytes = 4096;
 

@@ -224,3 +224,26 @@ def test_serve_fetches_is_a_thread_target():
     stop.set()
     t.join(timeout=2.0)
     assert not t.is_alive()
+
+
+def test_pull_boost_bit_exact():
+    """A pull started narrow and widened by a second grid (chunks claimed from
+    one counter) lands every byte exactly once; a boost after the pull ended
+    is a no-op; the next pull after a boosted one is exact too."""
+    donor = ck.SnapshotStore(device=DEV, replica_id=50)
+    rec = ck.SnapshotStore(device=DEV, replica_id=51)
+    g = torch.Generator(device=DEV).manual_seed(3)
+    p = torch.randn(40 << 20, device=DEV, generator=g)   # 160 MiB
+    m = torch.randn(24 << 20, device=DEV, generator=g)
+    donor.capture(9, p, m)
+    for boost in (True, False, True):
+        po, mo = torch.full_like(p, float("nan")), torch.full_like(m, float("nan"))
+        h = ck.start_fetch(rec, donor, 9, 0, po, mo, ctas=1)
+        if boost:
+            h.boost(16)
+        h.wait()
+        h.boost(8)  # finished: no-op
+        torch.cuda.synchronize()
+        assert torch.equal(po, p) and torch.equal(mo, m)
+    donor.close()
+    rec.close()

@@ -55,6 +55,8 @@ def main():
     ap.add_argument("--chunk-timeout", type=float, default=0.5)
     ap.add_argument("--unfused", action="store_true", help="separate torch optimizer instead of the fused SGD")
     ap.add_argument("--pull-ctas", type=int, default=8, help="CTA budget of the catch-up pull")
+    ap.add_argument("--boost-ctas", type=int, default=0,
+                    help="widen the pull to this many more CTAs once the step's FTAR is done (0: never)")
     args = ap.parse_args()
 
     import numpy as np
@@ -188,6 +190,8 @@ def main():
             try:
                 if pull is None:  # donors still being mapped when the step began
                     pull = fetch()
+                if args.boost_ctas:
+                    pull.boost(args.boost_ctas)  # the collectives are done: full width
                 pull.wait()
             except (errors.FtdpError, ck.SnapshotUnavailable):
                 fetch_ok = False

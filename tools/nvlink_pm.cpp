@@ -1,4 +1,4 @@
-// nvlink_pm.cpp — NVLink bytes of one GPU over a time window, from CUPTI PM
+// nvlink_pm.cpp — NVLink (and DRAM) bytes of one GPU over a time window, from CUPTI PM
 // sampling (device-level hardware counters sampled on a timer; kernels run
 // undisturbed and concurrently, unlike ncu, which serialises kernels and so
 // cannot profile collectives whose kernels wait on each other).  NVML's
@@ -24,9 +24,9 @@ namespace {
 
 thread_local std::string g_err;
 
-const char* kMetrics[] = {"nvlrx__bytes.sum", "nvltx__bytes.sum", "nvlrx__bytes_data_user.sum",
-                          "nvltx__bytes_data_user.sum"};
-constexpr int kNumMetrics = 4;
+// default metric set; nvpm_open takes any comma-separated list of up to 8
+const char* kDefault = "nvlrx__bytes.sum,nvltx__bytes.sum,nvlrx__bytes_data_user.sum,nvltx__bytes_data_user.sum";
+constexpr int kMaxMetrics = 8;
 
 struct Sampler {
   bool open = false;
@@ -34,6 +34,8 @@ struct Sampler {
   CUpti_Profiler_Host_Object* host = nullptr;
   CUpti_PmSampling_Object* pm = nullptr;
   std::vector<uint8_t> config, counter_data;
+  std::vector<std::string> names;
+  std::vector<const char*> metrics;
 };
 Sampler g_s[16];
 
@@ -61,10 +63,23 @@ const char* nvpm_error(void) { return g_err.c_str(); }
 
 // Prepare PM sampling of `device` every `interval_ns` (at most `max_samples`
 // samples per window).  Returns 0 on success.
-int nvpm_open(int device, uint64_t interval_ns, uint32_t max_samples) {
+int nvpm_open(int device, uint64_t interval_ns, uint32_t max_samples, const char* metrics_csv) {
   if (device < 0 || device >= 16) return (g_err = "bad device", 1);
   Sampler& S = g_s[device];
   if (S.open) return 0;
+  {
+    std::string all = (metrics_csv && *metrics_csv) ? metrics_csv : kDefault;
+    size_t pos = 0;
+    while (pos <= all.size() && (int)S.names.size() < kMaxMetrics) {
+      const size_t q = all.find(',', pos);
+      S.names.push_back(all.substr(pos, q == std::string::npos ? std::string::npos : q - pos));
+      if (q == std::string::npos) break;
+      pos = q + 1;
+    }
+    for (auto& n : S.names) S.metrics.push_back(n.c_str());
+  }
+  const char** kMetrics = S.metrics.data();
+  const size_t kNumMetrics = S.metrics.size();
   CUpti_Profiler_Initialize_Params pi{CUpti_Profiler_Initialize_Params_STRUCT_SIZE};
   if (!ok(cuptiProfilerInitialize(&pi), "cuptiProfilerInitialize")) return 1;
   CUpti_Device_GetChipName_Params cn{CUpti_Device_GetChipName_Params_STRUCT_SIZE};
@@ -133,11 +148,14 @@ int nvpm_start(int device) {
   return ok(cuptiPmSamplingStart(&st), "cuptiPmSamplingStart") ? 0 : 1;
 }
 
-// Stop and sum the window's samples: out[0..3] = rx, tx, rx user, tx user
-// bytes; *samples = completed samples; *span_ns = first start to last end.
+// Stop and sum the window's samples: out[k] = metric k over the window (in
+// the order given to nvpm_open); *samples = completed samples; *span_ns =
+// first sample start to last sample end.
 int nvpm_stop(int device, double* out, int* samples, uint64_t* span_ns, int* overflow) {
   Sampler& S = g_s[device];
   if (!S.open) return (g_err = "not open", 1);
+  const char** kMetrics = S.metrics.data();
+  const size_t kNumMetrics = S.metrics.size();
   CUpti_PmSampling_Stop_Params sp{CUpti_PmSampling_Stop_Params_STRUCT_SIZE};
   sp.pPmSamplingObject = S.pm;
   if (!ok(cuptiPmSamplingStop(&sp), "cuptiPmSamplingStop")) return 1;
@@ -155,7 +173,7 @@ int nvpm_stop(int device, double* out, int* samples, uint64_t* span_ns, int* ove
   gi.pCounterDataImage = S.counter_data.data();
   gi.counterDataImageSize = S.counter_data.size();
   if (!ok(cuptiPmSamplingGetCounterDataInfo(&gi), "cuptiPmSamplingGetCounterDataInfo")) return 1;
-  double sum[kNumMetrics] = {0, 0, 0, 0};
+  double sum[kMaxMetrics] = {0, 0, 0, 0, 0, 0, 0, 0};
   uint64_t t_first = 0, t_last = 0;
   for (size_t i = 0; i < gi.numCompletedSamples; ++i) {
     CUpti_PmSampling_CounterData_GetSampleInfo_Params si{CUpti_PmSampling_CounterData_GetSampleInfo_Params_STRUCT_SIZE};
@@ -166,7 +184,7 @@ int nvpm_stop(int device, double* out, int* samples, uint64_t* span_ns, int* ove
     if (!ok(cuptiPmSamplingCounterDataGetSampleInfo(&si), "cuptiPmSamplingCounterDataGetSampleInfo")) return 1;
     if (i == 0) t_first = si.startTimestamp;
     t_last = si.endTimestamp;
-    double v[kNumMetrics];
+    double v[kMaxMetrics];
     CUpti_Profiler_Host_EvaluateToGpuValues_Params ev{CUpti_Profiler_Host_EvaluateToGpuValues_Params_STRUCT_SIZE};
     ev.pHostObject = S.host;
     ev.pCounterDataImage = S.counter_data.data();
@@ -176,9 +194,9 @@ int nvpm_stop(int device, double* out, int* samples, uint64_t* span_ns, int* ove
     ev.rangeIndex = i;
     ev.pMetricValues = v;
     if (!ok(cuptiProfilerHostEvaluateToGpuValues(&ev), "cuptiProfilerHostEvaluateToGpuValues")) return 1;
-    for (int k = 0; k < kNumMetrics; ++k) sum[k] += v[k];
+    for (size_t k = 0; k < kNumMetrics; ++k) sum[k] += v[k];
   }
-  for (int k = 0; k < kNumMetrics; ++k) out[k] = sum[k];
+  for (size_t k = 0; k < kNumMetrics; ++k) out[k] = sum[k];
   if (samples) *samples = (int)gi.numCompletedSamples;
   if (span_ns) *span_ns = t_last - t_first;
   if (overflow) *overflow = ovf;
