@@ -96,6 +96,11 @@ class SnapshotStore:
         self._free_slots: list[int] = list(range(255, -1, -1))
         self.map_log: list[tuple] = []
         _STORES[(replica_id, rank)] = self
+        # the pull's side streams exist before any pull: creating them inside
+        # a recovering replica's first catch-up step cost 17.6 ms of host time
+        # right between two of its collective launches (config 5, N=4)
+        catchup_stream(self.device, 0)
+        catchup_stream(self.device, 1)
         if capacity_bytes:
             self._alloc(capacity_bytes)
 
@@ -243,7 +248,17 @@ class SnapshotStore:
                 err, self._connect_err = self._connect_err, None
                 raise err
 
-    def _map_donor(self, donor_replica: int, rank: int, timeout_s: float) -> int:
+    def _map_donor(self, donor_replica: int, rank: int, timeout_s: float, refresh: bool = True) -> int:
+        """Slot of the donor's snapshot mapping.  ``refresh=False`` reuses the
+        newest mapping of that donor without asking the fabric (a Store round
+        trip per donor: ~4 ms each, on the recovering replica's critical path
+        right before its first collective); a stale mapping (the donor
+        restarted) shows up as SnapshotUnavailable, and callers then retry
+        with a refresh."""
+        if not refresh:
+            known = sorted(k for k in self._peers if k[0] == donor_replica)
+            if known:
+                return self._peers[known[-1]]
         if self.fabric is None:
             raise Recoverable(PEER_DOWN, f"replica {donor_replica} is not in this process and no fabric is set")
         t0 = time.monotonic()
@@ -355,13 +370,15 @@ DEFAULT_PULL_CTAS = 8
 
 
 def start_fetch(local: SnapshotStore, donor, step: int, rank: int, params_out: torch.Tensor,
-                momentum_out: torch.Tensor, timeout_s: float = 5.0, ctas: int = DEFAULT_PULL_CTAS) -> CatchupPull:
+                momentum_out: torch.Tensor, timeout_s: float = 5.0, ctas: int = DEFAULT_PULL_CTAS,
+                refresh: bool = True) -> CatchupPull:
     """Launch the pull of `donor`'s snapshot of `step` into the given tensors
     without waiting.  `donor` is a SnapshotStore in this process (same device),
     a replica id resolved through ``local.fabric``, or a list of replica ids:
     the pull is then striped across all of them (every healthy replica holds
     the same retention-1 snapshot), so no single donor's NVLink egress carries
-    the whole catch-up."""
+    the whole catch-up.  ``refresh=False`` reuses existing donor mappings
+    without a fabric lookup (see SnapshotStore._map_donor)."""
     p, m = _as_bytes_tensor(params_out), _as_bytes_tensor(momentum_out)
     pb, mb = p.numel() * p.element_size(), m.numel() * m.element_size()
     local.join_connect()
@@ -375,14 +392,17 @@ def start_fetch(local: SnapshotStore, donor, step: int, rank: int, params_out: t
             _lib.check(_lib.lib.ftar_peer_enable(local.device_index, donor.device_index), "ftar_peer_enable")
     else:
         donors = list(donor) if isinstance(donor, (list, tuple)) else [donor]
-        slots, src = [local._map_donor(int(d), rank, timeout_s) for d in donors], None
+        slots, src = [local._map_donor(int(d), rank, timeout_s, refresh) for d in donors], None
+    t0 = time.monotonic()
     stream = catchup_stream(local.device)
     stream.wait_stream(torch.cuda.current_stream(local.device))
     stream.wait_stream(catchup_stream(local.device, 1))  # a previous pull's boost grid has exited
+    t1 = time.monotonic()
     arr = (C.c_int * max(1, len(slots)))(*slots)
     rc = _lib.lib.ftar_snap_pull_multi_launch(local.handle, arr, len(slots), src, step, p.data_ptr(), pb,
                                               m.data_ptr(), mb, ctas, stream.cuda_stream)
     _lib.check(rc, "ftar_snap_pull_launch")
+    local.launch_log = (round((t1 - t0) * 1e3, 3), round((time.monotonic() - t1) * 1e3, 3))
     return CatchupPull(local, p, m, stream, timeout_s)
 
 

@@ -2466,6 +2466,7 @@ struct ftar_ctx {
   uint64_t gen = 0, seq = 0;
   uint64_t cur_tag = 0;
   uint64_t hard_timeout_ns = 120ull * 1000000000ull;
+  bool warmed = false;  // this ring size's kernels loaded (warm_ring_kernels)
   // registered buffers (RingGroup.register): mine by region id, and every
   // peer slot's as mapped here (one IPC mapping per peer allocation block)
   uint64_t my_region_ptr[kMaxRegions] = {};
@@ -2683,6 +2684,30 @@ cudaError_t launch_dispatch(int n, const LaunchParams& p, dim3 grid, cudaStream_
     case 8: return launch_n<8, In>(p, grid, st, coop, pdl);
   }
   return cudaErrorInvalidValue;
+}
+
+// CUDA loads kernels lazily, at their first launch (or attribute query).
+// Loading a module while other kernels run can stall the launching thread
+// for milliseconds to hundreds of ms, and a collective's first launch of a
+// kernel instance (a replica joining a new ring size, a recovering replica's
+// first catch-up pull) is exactly when that hurts: the other members wait at
+// the entry barrier.  So the instances a ring of size n will use are loaded
+// when its membership is installed, and the catch-up kernels when a
+// snapshot store is created.
+template <class In>
+void warm_ring_kernels(int n) {
+  cudaFuncAttributes a;
+  switch (n) {
+#define CASE(K)                                                     \
+  case K:                                                           \
+    cudaFuncGetAttributes(&a, allreduce_kernel<K, In>);             \
+    cudaFuncGetAttributes(&a, intra_kernel<K, In>);                 \
+    if (K > 1) cudaFuncGetAttributes(&a, small_allreduce_kernel<(K > 1 ? K : 2), In>); \
+    break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+  }
+  cudaGetLastError();
 }
 
 template <class In>
@@ -3040,6 +3065,12 @@ int ftar_set_membership(ftar_ctx* c, const int* ring_slots, int n, int self_inde
   {
     DeviceGuard g(c->device);
     CK(cudaMemcpy(c->arena + offsetof(ArenaHdr, gen_word), &generation, sizeof(uint64_t), cudaMemcpyHostToDevice));
+  }
+  if (n != c->n || !c->warmed) {  // load this ring size's kernel instances now, not mid-collective
+    DeviceGuard g(c->device);
+    warm_ring_kernels<F32In>(n);
+    warm_ring_kernels<BF16In>(n);
+    c->warmed = true;
   }
   c->n = n;
   c->self = self_index;
@@ -3864,6 +3895,16 @@ int ftar_snap_create(int device, uint64_t capacity_bytes, int exportable, ftar_s
     return cuda_fail(e, "cudaMalloc(snapshot)");
   }
   snap_init_kernel<<<1, 1>>>(reinterpret_cast<SnapHdr*>(s->arena));
+  {  // load the catch-up kernels now (see warm_ring_kernels): a recovering
+     // replica's first pull must not load modules while the ring runs
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, snap_pull_kernel);
+    cudaFuncGetAttributes(&a, snap_pull_reset_kernel);
+    cudaFuncGetAttributes(&a, snap_copy_kernel);
+    cudaFuncGetAttributes(&a, snap_mark_kernel);
+    cudaFuncSetAttribute(snap_pull_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPullSmem);
+    cudaGetLastError();
+  }
   e = cudaHostAlloc(&s->ctl_h, sizeof(HostCtl), cudaHostAllocMapped | cudaHostAllocPortable);
   if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc(snap ctl)");
   std::memset((void*)s->ctl_h, 0, sizeof(HostCtl));

@@ -147,15 +147,14 @@ def main():
         target = d.target_step
         pull = None
 
-        def fetch():
+        def fetch(refresh=False):
+            # donors were mapped at restart (connect): no Store lookups here
             return ck.start_fetch(snap, list(d.healthy), target - 1, 0, fetched[0], fetched[1],
-                                  timeout_s=10, ctas=args.pull_ctas)
+                                  timeout_s=10, ctas=args.pull_ctas, refresh=refresh)
 
         if role == "healthy":
             grads.copy_(grad_base)
             grads.mul_(1.0 / (1.0 + 0.1 * target))  # the step's synthetic gradient
-        elif not snap.connecting():
-            pull = fetch()  # overlaps this step's FTAR on a low-priority side stream
         if rid == victim and target == args.kill_at and inc == 0:
             # killed mid-collective: never joins this step's FTAR
             killed = True
@@ -163,8 +162,10 @@ def main():
             continue
         ok = True
         fused = role == "healthy" and not args.unfused
+        bucket_ms = []
         t_ar = time.monotonic()
         try:
+            bucket_ms = []
             if fused:
                 # §8f: all-reduce + x f32(1/h) + SGD-momentum in one kernel per
                 # bucket, out of place (applied by the swap at commit)
@@ -172,14 +173,27 @@ def main():
                     ftar.ftar_all_reduce_sgd(group, grads[o:o + n], target, cfg, params=params[o:o + n],
                                              momentum=mom[o:o + n], lr=args.lr, beta=args.beta, scale=d.scale(),
                                              params_out=nxt[0][o:o + n], momentum_out=nxt[1][o:o + n])
+                    bucket_ms.append(round((time.monotonic() - t_ar) * 1e3, 2))
             else:
                 pend = [ftar.ftar_all_reduce_async(group, grads[o:o + n], target, cfg, out=red[o:o + n],
                                                    scale=d.scale()) for o, n in buckets[:3]]
+                if role == "behind" and not snap.connecting():
+                    # the ring's first buckets are queued: now start the pull on its
+                    # low-priority side stream (its host-side donor lookups must not
+                    # delay this replica's entry into the collective)
+                    t_f = time.monotonic()
+                    pull = fetch()
+                    bucket_ms.append(("fetch_call_ms", round((time.monotonic() - t_f) * 1e3, 3),
+                                      "streams_ms/launch_ms", getattr(snap, "launch_log", None)))
                 for o, n in buckets[3:]:
+                    t_l = time.monotonic()
                     pend.append(ftar.ftar_all_reduce_async(group, grads[o:o + n], target, cfg, out=red[o:o + n],
                                                            scale=d.scale()))
+                    if role == "behind":
+                        bucket_ms.append(("launch_ms", round((time.monotonic() - t_l) * 1e3, 3)))
                 for p_ in pend:
                     p_.wait()
+                    bucket_ms.append(round((time.monotonic() - t_ar) * 1e3, 2))
         except errors.Recoverable:
             ok = False
         torch.cuda.current_stream(dev).synchronize()  # the FTAR only (a catch-up pull runs on a side stream)
@@ -192,7 +206,11 @@ def main():
                     pull = fetch()
                 if args.boost_ctas:
                     pull.boost(args.boost_ctas)  # the collectives are done: full width
-                pull.wait()
+                try:
+                    pull.wait()
+                except ck.SnapshotUnavailable:
+                    pull = fetch(refresh=True)  # a donor restarted since it was mapped
+                    pull.wait()
             except (errors.FtdpError, ck.SnapshotUnavailable):
                 fetch_ok = False
         t_pw = time.monotonic() - t_pw
@@ -218,6 +236,7 @@ def main():
                     "healthy": len(d.healthy), "behind": sorted(d.behind), "committed": committed,
                     "ftar_ms": round(t_ar * 1e3, 3), "step_ms": round(dt * 1e3, 3),
                     "quorum_ms": round((t_x - t0) * 1e3, 3), "reconfig_ms": round(t_rc * 1e3, 3),
+                    "bucket_done_ms": bucket_ms,
                     "pull_wait_ms": round(t_pw * 1e3, 3),
                     "vote_ms": round(t_v * 1e3, 3)})
     elapsed = time.monotonic() - t_run
