@@ -94,6 +94,7 @@ struct LaunchParams {
   int diag;                      // timing diagnostics: 1 = RS stores skipped, 2 = RS reads local only
   int rs_ctas;                   // CTAs that reduce (the rest only all-gather); <= gridDim.x
   uint32_t tma_stages;           // > 0: bulk-copy (TMA) data path with this many smem stages
+  uint32_t tma_piece;            // elements per bulk copy (a tile's per-peer part is split; 0 = whole)
   uint64_t my_in_va;             // real mode: my input as this process addresses it
   uint64_t region_va[kMaxMembers][kMaxRegions];  // member i's registered region r, mapped here (0 = none)
   uint32_t intra_op;             // intra-replica collective (kIntraRS / kIntraAG), 0 = FTAR
@@ -389,7 +390,10 @@ struct Unroll {
 // (out-of-range vectors re-read a valid one and are masked; a
 // non-contributor's loads are predicated off and read as +0.0) before the
 // first add, so no branch separates the loads; scalars at the ragged edges.
-template <int N, class In, int U, class Sink>
+// kAll: every member contributes (the common case), so the loads need no
+// predicate: the predicated form's extra moves measured 4% on the HBM-bound
+// in-process kernel.
+template <int N, class In, int U, class Sink, bool kAll = false>
 __device__ __forceinline__ void fold_range(const typename In::T* const* src, const Sink& sink,
                                            uint64_t a, uint64_t b, int s, uint32_t contrib,
                                            bool vec_ok, bool do_scale, float scale,
@@ -429,7 +433,7 @@ __device__ __forceinline__ void fold_range(const typename In::T* const* src, con
         const uint64_t v = v0 + (uint64_t)u * kThreads;
         const uint64_t vv = v < ve ? v : vb;  // clamp: keep the load unconditional
 #pragma unroll
-        for (int k = 0; k < N; ++k) raw[u][k] = In::load4_if(rs[k], vv * 4, cb[k]);
+        for (int k = 0; k < N; ++k) raw[u][k] = kAll ? In::load4(rs[k], vv * 4) : In::load4_if(rs[k], vv * 4, cb[k]);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -489,7 +493,10 @@ __device__ __forceinline__ int fold_tiles(const LaunchParams& p, const typename 
         sbeg = cur;
       }
       const uint64_t end = umin(send, b);
-      fold_range<N, In, U>(src, sink, cur, end, s, p.contrib, vec_ok, do_scale, p.scale, nf);
+      if (((p.contrib >> 0) & ((1u << N) - 1u)) == ((1u << N) - 1u))
+        fold_range<N, In, U, Sink, true>(src, sink, cur, end, s, p.contrib, vec_ok, do_scale, p.scale, nf);
+      else
+        fold_range<N, In, U, Sink, false>(src, sink, cur, end, s, p.contrib, vec_ok, do_scale, p.scale, nf);
       cur = end;
     }
     ++done;
@@ -710,9 +717,17 @@ __device__ __forceinline__ void tma_issue(const LaunchParams& p, const typename 
     return;
   }
   mbar_expect_tx(&full[s], bytes * (uint32_t)__popc(peers));
+  // several smaller copies per peer where the ring is small: an SM's copy
+  // engine needs many copies in flight, not just many bytes
+  const uint32_t pe = p.tma_piece && p.tma_piece < cnt ? p.tma_piece : cnt;
+  for (uint32_t o = 0; o < cnt; o += pe) {
+    const uint32_t c = (uint32_t)umin(pe, cnt - o);
 #pragma unroll
-  for (int k = 0; k < N; ++k)
-    if ((peers >> k) & 1u) bulk_g2s(stage + (uint64_t)tma_slot(k, me) * TE * In::kBytes, src[k] + a, bytes, &full[s]);
+    for (int k = 0; k < N; ++k)
+      if ((peers >> k) & 1u)
+        bulk_g2s(stage + ((uint64_t)tma_slot(k, me) * TE + o) * In::kBytes, src[k] + a + o, c * (uint32_t)In::kBytes,
+                 &full[s]);
+  }
 }
 
 // Fold one 4-element vector (elements off..off+3 of the tile) whose fold
@@ -1734,7 +1749,8 @@ __global__ void __launch_bounds__(kThreads, 1) intra_kernel(const __grid_constan
       const uint64_t TL = (uint64_t)kThreads * 4 * U;
       uint32_t nf = 0;
       for (uint64_t a = a0; a < a1; a += TL)
-        fold_range<N, In, U>(s_src, SinkOne{out - off}, a, umin(a + TL, a1), 0, 0xffffffffu, vec_ok, false, 1.0f, nf);
+        fold_range<N, In, U, SinkOne, true>(s_src, SinkOne{out - off}, a, umin(a + TL, a1), 0, 0xffffffffu, vec_ok,
+                                            false, 1.0f, nf);
     } else {
       // every CTA starts on a different rank so all links stay busy
       for (int i = 0; i < N; ++i) {
@@ -2087,6 +2103,7 @@ __global__ void __launch_bounds__(kThreads, 1) local_oneshot_kernel(const __grid
   const uint64_t ntiles = (E + TL - 1) / TL;
   uint32_t nf = 0;
   const bool direct = p.stage == nullptr;
+  const bool all = (p.contrib & ((1u << N) - 1u)) == ((1u << N) - 1u);
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const uint64_t a = t * TL, b = umin(a + TL, E);
     uint64_t cur = a;
@@ -2096,9 +2113,15 @@ __global__ void __launch_bounds__(kThreads, 1) local_oneshot_kernel(const __grid
       owner_of(cur, g, N, s, send);
       const uint64_t end = umin(send, b);
       if (direct)
-        fold_range<N, In, U>(s_src, SinkAll<N>{p.out}, cur, end, s, p.contrib, vec_ok, do_scale, p.scale, nf);
+        all ? fold_range<N, In, U, SinkAll<N>, true>(s_src, SinkAll<N>{p.out}, cur, end, s, p.contrib, vec_ok, do_scale,
+                                                       p.scale, nf)
+            : fold_range<N, In, U, SinkAll<N>, false>(s_src, SinkAll<N>{p.out}, cur, end, s, p.contrib, vec_ok,
+                                                        do_scale, p.scale, nf);
       else
-        fold_range<N, In, U>(s_src, SinkOne{p.stage}, cur, end, s, p.contrib, vec_ok, do_scale, p.scale, nf);
+        all ? fold_range<N, In, U, SinkOne, true>(s_src, SinkOne{p.stage}, cur, end, s, p.contrib, vec_ok, do_scale,
+                                                  p.scale, nf)
+            : fold_range<N, In, U, SinkOne, false>(s_src, SinkOne{p.stage}, cur, end, s, p.contrib, vec_ok, do_scale,
+                                                   p.scale, nf);
       cur = end;
     }
   }
@@ -2410,7 +2433,43 @@ int tma_ctas(uint64_t slice_bytes) {
   const uint64_t per = (uint64_t)env_int("FTAR_TMA_BYTES_PER_CTA", 128 << 10);
   return (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)std::max(cap, 1), (slice_bytes + per - 1) / per));
 }
+// elements per bulk copy of the bulk-copy path (FTAR_TMA_PIECE_BYTES; 0 =
+// one copy per peer per tile), a multiple of 8 elements (16-byte granules)
+uint32_t tma_piece(uint64_t esz) {
+  const int b = env_int("FTAR_TMA_PIECE_BYTES", 0);
+  return b <= 0 ? 0u : (uint32_t)std::max<uint64_t>(8, ((uint64_t)b / esz) & ~7ull);
+}
 int small_ctas(uint64_t bytes) { return (int)std::max<uint64_t>(1, std::min<uint64_t>(16, (bytes + (32u << 10) - 1) >> 15)); }
+
+// The data path and grid of one call (launch_real and ftar_inflight_bound
+// share it, so the in-flight meter reports the path the call really takes).
+enum PathKind { kPathNone = 0, kPathSmall = 1, kPathBulk = 2, kPathRegister = 3 };
+struct PathChoice {
+  int kind;
+  int ctas;
+  uint32_t stages;  // bulk-copy pipeline stages (0: not the bulk path)
+  uint32_t piece;   // elements per bulk copy (0: one per peer per tile)
+};
+PathChoice choose_path(int n, const LaunchParams& p, uint64_t esz, bool small, bool sgd, bool push) {
+  PathChoice pc{kPathRegister, real_ctas(push), 0, 0};
+  // fewer CTAs for small slices (CTA arrival + fences dominate): ~64 KB of
+  // my slice per CTA, at least 1, at most the tuned shape
+  const uint64_t per = (uint64_t)env_int("FTAR_BYTES_PER_CTA", 64 << 10);
+  const uint64_t want = (p.slice * esz + per - 1) / per;
+  if (g_ctas <= 0 && want < (uint64_t)pc.ctas) pc.ctas = (int)std::max<uint64_t>(1, want);
+  if (small) {
+    pc.kind = kPathSmall;
+    pc.ctas = g_ctas > 0 ? g_ctas : small_ctas(p.nelems * esz);
+  } else if (!sgd && n >= 2 && tma_on() && p.p_base / (uint64_t)n >= tma_tile(n, (int)esz) &&
+             (p.slice * esz >= tma_min_slice() || g_ctas > 0)) {
+    // every segment spans >= one tile and the slice is large: the bulk-copy data path
+    pc.kind = kPathBulk;
+    pc.stages = tma_stages_for(n, (int)esz);
+    pc.ctas = tma_ctas(p.slice * esz);
+    pc.piece = tma_piece(esz);
+  }
+  return pc;
+}
 int rs_layout() { return env_int("FTAR_RS_LAYOUT", 0); }
 #ifdef FTAR_DIAGNOSTICS
 int diag_mode() { return env_int("FTAR_DIAG", 0); }
@@ -3095,6 +3154,45 @@ int ftar_geometry(uint64_t n_elems, int n, uint64_t* slice_elems, int* ctas, int
   return FTAR_OK;
 }
 
+int ftar_inflight_bound(ftar_ctx* c, uint64_t n_elems, int in_dtype, uint64_t chunk_bytes, int max_in_flight,
+                        int push, uint64_t* bytes_per_link, int* ctas, int* path) {
+  // The InflightMeter's figure (ftar.py:141-159): the most bytes one peer
+  // link can have outstanding for this call, on the path launch_real picks.
+  //   small push one-shot: the whole input, posted to each peer;
+  //   bulk-copy reduce-scatter: G CTAs x (S-1) stages x one tile per peer;
+  //   register path: G CTAs x 512 threads x U vectors of 4 elements per peer.
+  if (!c) return fail(FTAR_ST_INVARIANT, "null ctx");
+  int v = validate_common(in_dtype, c->n, chunk_bytes, max_in_flight);
+  if (v) return v;
+  const uint64_t esz = in_dtype == FTAR_DT_BF16 ? 2 : 4;
+  const uint64_t in_bytes = n_elems * esz;
+  LaunchParams p{};
+  fill_geometry(p, n_elems, chunk_bytes, max_in_flight, c->n);
+  p.nelems = n_elems;
+  const bool small = c->n >= 2 && in_bytes > 0 && in_bytes <= small_bytes();
+  PathChoice pc{kPathNone, 0, 0, 0};
+  uint64_t bound = 0;
+  if (c->n >= 2 && in_bytes > 0) {
+    pc = choose_path(c->n, p, esz, small, false, push != 0);
+    if (pc.kind == kPathSmall) {
+      bound = in_bytes;
+    } else if (pc.kind == kPathBulk) {
+      bound = (uint64_t)pc.ctas * (pc.stages - 1) * tma_tile(c->n, (int)esz) * esz;
+    } else {
+      const int N = c->n;
+      const int budget = (N >= 6 && esz == 2) ? 8 : (N >= 5 ? 12 : 16);  // Unroll<N, In>
+      const int u0 = (budget * 16 / (int)(esz * 4)) / N;
+      const int umax = N <= 2 ? 16 : (N == 3 ? 6 : 8);
+      const int U = u0 < 1 ? 1 : (u0 > umax ? umax : u0);
+      bound = (uint64_t)pc.ctas * kThreads * (uint64_t)U * 4 * esz;
+    }
+  }
+  if (bytes_per_link) *bytes_per_link = bound;
+  if (ctas) *ctas = pc.ctas;
+  if (path) *path = pc.kind;
+  return FTAR_OK;
+}
+
 struct SgdArgs {
   const float* p = nullptr;
   const float* m = nullptr;
@@ -3221,26 +3319,14 @@ static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, ui
   p.rs_layout = rs_layout();
   p.diag = diag_mode();
   p.rs_ctas = rs_ctas_knob();
-  // small buckets: fewer CTAs (CTA arrival + fences dominate); ~256 KB of
-  // my slice per CTA, at least 1, at most the tuned shape
-  int G = real_ctas((p.flags & kFlagPush) != 0);
-  {
-    const uint64_t slice_bytes = p.slice * (uint64_t)esz;
-    const uint64_t per = (uint64_t)env_int("FTAR_BYTES_PER_CTA", 64 << 10);
-    const uint64_t want = (slice_bytes + per - 1) / per;
-    if (g_ctas <= 0 && want < (uint64_t)G) G = (int)std::max<uint64_t>(1, want);
-  }
+  const PathChoice pc = choose_path(c->n, p, esz, small, sgd != nullptr, (p.flags & kFlagPush) != 0);
   if (small) {
     if (p.flags & kFlagDirect) p.flags |= kFlagSmallDirect;
     p.flags &= ~(kFlagPush | kFlagDirect);
-    G = g_ctas > 0 ? g_ctas : small_ctas(in_bytes);
-  } else if (!sgd && c->n >= 2 && tma_on() && p.p_base / (uint64_t)c->n >= tma_tile(c->n, (int)esz) &&
-             (p.slice * esz >= tma_min_slice() || g_ctas > 0)) {
-    // every segment spans >= one tile and the slice is large: the bulk-copy data path
-    p.tma_stages = tma_stages_for(c->n, (int)esz);
-    G = tma_ctas(p.slice * esz);
   }
-  const dim3 grid(G, 1);
+  p.tma_stages = pc.stages;
+  p.tma_piece = pc.piece;
+  const dim3 grid(pc.ctas, 1);
   cudaError_t e = small ? (in_dtype == FTAR_DT_BF16 ? launch_small<BF16In>(c->n, p, grid, st, false, pdl_on())
                                                     : launch_small<F32In>(c->n, p, grid, st, false, pdl_on()))
                         : (in_dtype == FTAR_DT_BF16 ? launch_dispatch<BF16In>(c->n, p, grid, st, false, pdl_on())
@@ -3420,6 +3506,7 @@ static int launch_local(ftar_ctx** ctxs, int n, const void* const* ins, int in_d
   }
   if (!sgd_p && n >= 2 && tma_on() && p.p_base / (uint64_t)n >= tma_tile(n, in_dtype == FTAR_DT_BF16 ? 2 : 4)) {
     p.tma_stages = tma_stages_for(n, in_dtype == FTAR_DT_BF16 ? 2 : 4);
+    p.tma_piece = tma_piece(in_dtype == FTAR_DT_BF16 ? 2 : 4);
     if (g_local_ctas <= 0) G = std::min(G, tma_ctas(p.slice * (in_dtype == FTAR_DT_BF16 ? 2 : 4)));
   }
   const dim3 grid(G, n);

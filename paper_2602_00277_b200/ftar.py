@@ -134,9 +134,12 @@ def classify_error(err: BaseException) -> str:
 
 
 class InflightMeter:
-    """ftar.py:141-159.  On NVLink there is no ack window; the meter records
-    the data plane's per-link in-flight bound for each call (CTAs x threads x
-    outstanding 16-byte loads per peer), which the kernel can never exceed."""
+    """ftar.py:141-159.  On NVLink there is no ack window; the meter records,
+    per call, the most bytes one peer link can have outstanding on the path
+    the library takes (ftar_inflight_bound): the whole input for the small
+    push one-shot, CTAs x (stages-1) x one tile for the bulk-copy
+    reduce-scatter, CTAs x 512 threads x U 4-element vectors for the register
+    path.  The kernel cannot exceed it; max_unacked_bytes is the largest."""
 
     def __init__(self):
         self.unacked_bytes = 0
@@ -258,6 +261,7 @@ class RingGroup:
         self._pool_ptr, self._pool_bytes = ptr.value, nbytes.value
         self._lock = threading.Lock()
         self._pending: deque = deque()  # queued collectives, oldest first (PendingAllReduce)
+        self._bound_cache: dict = {}
         if self._local:
             self.router.register(self)
         else:
@@ -483,18 +487,23 @@ class RingGroup:
         except Exception:  # noqa: BLE001 - interpreter teardown
             pass
 
-    def inflight_bound(self, in_dtype_bytes: int) -> tuple[int, int]:
-        """(bytes, CTAs) a single peer link can have outstanding per call:
-        CTAs x threads x one 4-element vector per unrolled load."""
-        key = (self.n, in_dtype_bytes)
-        cache = self.__dict__.setdefault("_bound_cache", {})
+    def inflight_bound(self, nelems: int, dtype_code: int, cfg: "PipelineConfig", push: bool = False) -> tuple[int, int]:
+        """(bytes, CTAs) one peer link can have outstanding for this call, on
+        the path the library takes for it (ftar_inflight_bound: small push
+        one-shot / bulk-copy reduce-scatter / register path)."""
+        if self._local or self.n < 2:
+            return 0, 0
+        key = (self.n, nelems, dtype_code, cfg.chunk_bytes, cfg.max_in_flight, push)
+        cache = self._bound_cache
         if key not in cache:
-            slice_e, ctas, threads = C.c_uint64(), C.c_int(), C.c_int()
-            _lib.lib.ftar_geometry(1, max(1, self.n), C.byref(slice_e), C.byref(ctas), C.byref(threads))
-            n = max(1, self.n)
-            vec_bytes = 4 * in_dtype_bytes
-            unroll = max(1, min(16, (16 * 16 // vec_bytes) // n))
-            cache[key] = (ctas.value * threads.value * unroll * vec_bytes, ctas.value)
+            b, g, path = C.c_uint64(), C.c_int(), C.c_int()
+            _lib.check(_lib.lib.ftar_inflight_bound(self._ctx, nelems, dtype_code, cfg.chunk_bytes,
+                                                    cfg.max_in_flight, int(push), C.byref(b), C.byref(g),
+                                                    C.byref(path)),
+                       "ftar_inflight_bound")
+            if len(cache) > 64:
+                cache.clear()
+            cache[key] = (b.value, g.value)
         return cache[key]
 
 
@@ -538,7 +547,7 @@ def ftar_all_reduce(group: RingGroup, buf: torch.Tensor, step: int, cfg: Pipelin
         raise Recoverable(PEER_RESET, "ring links not established")
     flags = _lib.F_SCALE if scale is not None else 0
     f_scale = _f32(scale) if scale is not None else 1.0
-    bound, ctas = group.inflight_bound(buf.element_size())
+    bound, ctas = group.inflight_bound(buf.numel(), code, cfg, dst.data_ptr() != buf.data_ptr())
     try:
         if group._local:
             _local_all_reduce(group, buf, dst, code, cfg, f_scale, flags)
@@ -623,7 +632,7 @@ def ftar_all_reduce_async(group: RingGroup, buf: torch.Tensor, step: int, cfg: P
     _lib.check(rc, "ftar_allreduce_launch")
     p = PendingAllReduce(group, dst, cfg)
     q.append(p)
-    bound, ctas = group.inflight_bound(buf.element_size())
+    bound, ctas = group.inflight_bound(buf.numel(), code, cfg, dst.data_ptr() != buf.data_ptr())
     group.meter.sent(bound, ctas)
     group.meter.acked(bound, ctas)
     return p

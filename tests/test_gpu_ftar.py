@@ -422,6 +422,49 @@ def test_registered_pool_zero_copy(ftar):
             g.close()
 
 
+def test_inflight_bound_follows_the_path(ftar, monkeypatch):
+    """InflightMeter (ftar.py:141-159): each call records the per-link bound of
+    the path it takes -- small push one-shot (the whole input), register path
+    (CTAs x 512 x U x 16 B), bulk-copy (CTAs x (stages-1) x tile)."""
+    from paper_2602_00277_b200 import _lib
+    from paper_2602_00277_b200.fabric import LocalFabric
+    monkeypatch.delenv("FTAR_TMA", raising=False)
+    fab = LocalFabric()
+    gs = [ftar.RingGroup(r, 0, fab, device=DEV, max_bucket_bytes=1 << 20, pool_bytes=4 << 20) for r in range(2)]
+    try:
+        addrs = {r: ftar.PeerAddress(r) for r in range(2)}
+        ts = [threading.Thread(target=g.reconfig, args=(addrs, 1)) for g in gs]
+        [t.start() for t in ts]
+        [t.join() for t in ts]
+        cfg = ftar.PipelineConfig()
+        paths = {}
+        for elems in (256, 1 << 21, 1 << 24):
+            b, g, path = _lib.C.c_uint64(), _lib.C.c_int(), _lib.C.c_int()
+            _lib.check(_lib.lib.ftar_inflight_bound(gs[0].ctx, elems, _lib.DT_F32, cfg.chunk_bytes,
+                                                    cfg.max_in_flight, 1, _lib.C.byref(b), _lib.C.byref(g),
+                                                    _lib.C.byref(path)), "bound")
+            paths[elems] = path.value
+            assert (b.value, g.value) == gs[0].inflight_bound(elems, _lib.DT_F32, cfg, True)
+            assert g.value >= 1
+            if path.value == 1:
+                assert b.value == elems * 4
+            elif path.value == 3:  # n=2: U = 16 vectors of 4 fp32 per thread
+                assert b.value == g.value * 512 * 16 * 16
+            else:
+                assert path.value == 2 and b.value % g.value == 0 and b.value < elems * 4
+        assert paths == {256: 1, 1 << 21: 3, 1 << 24: 2}
+        # a call records its bound in the meter
+        buf = gs[0].alloc_bucket(256)
+        buf2 = gs[1].alloc_bucket(256)
+        th = [threading.Thread(target=ftar.ftar_all_reduce, args=(g, t, 1)) for g, t in zip(gs, (buf, buf2))]
+        [t.start() for t in th]
+        [t.join() for t in th]
+        assert gs[0].meter.max_unacked_bytes == 1024 and gs[0].meter.unacked_bytes == 0
+    finally:
+        for g in gs:
+            g.close()
+
+
 # ---------------------------------------------------------------------------
 # Host buffers (the reference's numpy call shape) and range launches.
 

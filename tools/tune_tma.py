@@ -25,6 +25,10 @@ def main():
     ap.add_argument("--tma-ctas", default="8,12,16,24,32,48")
     ap.add_argument("--ldg-ctas", default="32,64,128")
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--ag", default="push", help="comma list of all-gather modes: push (into registered outs), "
+                                                  "pull (FTAR_NO_PUSH=1: members pull the reduced slices)")
+    ap.add_argument("--pieces", default="0", help="comma list of FTAR_TMA_PIECE_BYTES for the tma cells "
+                                                   "(bytes per bulk copy; 0 = one copy per peer per tile)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -81,17 +85,23 @@ def main():
             buf.copy_(torch.randn(elems, device=dev).to(tdt))
             out = group.alloc_bucket(elems, torch.float32)
             steps = max(5, min(args.steps * 8, int(args.steps * 256 / max(mib, 1))))
-            cells = [("tma", c) for c in args.tma_ctas.split(",")] + [("ldg", c) for c in args.ldg_ctas.split(",")]
-            for path, c in cells:
-                os.environ["FTAR_TMA"] = "1" if path == "tma" else "0"
-                _lib.lib.ftar_set_tuning(int(c), 0)
-                t = timed(buf, out, steps)
-                if rank == 0:
-                    busbw = elems * ib / t * 2 * (n - 1) / n / 1e9
-                    ingress = (n - 1) / n * elems * (ib + 4) / t / 1e9
-                    print(json.dumps({"n": n, "dtype": dt, "MiB": mib, "path": path, "ctas": int(c),
-                                      "us": round(t * 1e6, 2), "busbw": round(busbw, 1),
-                                      "nvlink_ingress_GBps": round(ingress, 1)}), flush=True)
+            cells = [("tma", c, pc) for pc in args.pieces.split(",") for c in args.tma_ctas.split(",") if c] + \
+                    [("ldg", c, "0") for c in args.ldg_ctas.split(",") if c]
+            for ag in args.ag.split(","):
+                os.environ["FTAR_NO_PUSH"] = "1" if ag == "pull" else "0"
+                for path, c, piece in cells:
+                    os.environ["FTAR_TMA"] = "1" if path == "tma" else "0"
+                    os.environ["FTAR_TMA_PIECE_BYTES"] = piece
+                    _lib.lib.ftar_set_tuning(int(c), 0)
+                    t = timed(buf, out, steps)
+                    if rank == 0:
+                        busbw = elems * ib / t * 2 * (n - 1) / n / 1e9
+                        ingress = (n - 1) / n * elems * (ib + 4) / t / 1e9
+                        print(json.dumps({"n": n, "dtype": dt, "MiB": mib, "path": path, "ag": ag, "ctas": int(c),
+                                          "piece": int(piece),
+                                          "us": round(t * 1e6, 2), "busbw": round(busbw, 1),
+                                          "nvlink_ingress_GBps": round(ingress, 1)}), flush=True)
+            os.environ["FTAR_NO_PUSH"] = "0"
     _lib.lib.ftar_set_tuning(0, 0)
     group.close()
     dist.barrier()
