@@ -225,11 +225,13 @@ int ftar_set_tuning(int ctas, int local_ctas);
  * grid used — for tests and the in-flight meter. */
 int ftar_geometry(uint64_t n_elems, int n, uint64_t* slice_elems, int* ctas, int* threads);
 
-/* The InflightMeter's figure (ftar.py:141-159) for a call of n_elems on this
- * group: the most bytes one peer link can have outstanding (*path: 0 none,
- * 1 small push one-shot, 2 bulk-copy reduce-scatter, 3 register path). */
-int ftar_inflight_bound(ftar_ctx* ctx, uint64_t n_elems, int in_dtype, uint64_t chunk_bytes, int max_in_flight,
-                        int push, uint64_t* bytes_per_link, int* ctas, int* path);
+/* The InflightMeter's figure (ftar.py:141-159) for a call of n_elems on an
+ * n-member ring (one process per GPU; push = out-of-place into a peer-
+ * addressable buffer): the most bytes one peer link can have outstanding
+ * (*path: 0 none, 1 small push one-shot, 2 bulk-copy reduce-scatter,
+ * 3 register path) and the CTAs of the launch. */
+int ftar_inflight_bound(int n, uint64_t n_elems, int in_dtype, uint64_t chunk_bytes, int max_in_flight, int push,
+                        uint64_t* bytes_per_link, int* ctas, int* path);
 
 /* -------------------------------------------------------- operator plugin
  * kernels.accumulate / kernels.copy_into (kernels.py:16-48 ->

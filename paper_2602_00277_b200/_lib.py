@@ -61,7 +61,7 @@ SIGNATURES = {
     "ftar_wait": (i32, [c_ctx_p, dbl, C.POINTER(i32)]),
     "ftar_wait_local": (i32, [C.POINTER(c_ctx_p), i32, dbl, C.POINTER(i32), C.POINTER(i32)]),
     "ftar_geometry": (i32, [u64, i32, C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]),
-    "ftar_inflight_bound": (i32, [c_ctx_p, u64, i32, u64, i32, i32, C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]),
+    "ftar_inflight_bound": (i32, [i32, u64, i32, u64, i32, i32, C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]),
     "ftar_probe_clock": (i32, [i32, i32, C.POINTER(C.c_int64)]),
     "ftar_snap_region": (i32, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(u64), C.POINTER(u64), C.POINTER(u64),
                                C.POINTER(C.c_int64)]),

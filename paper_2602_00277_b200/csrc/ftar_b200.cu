@@ -95,6 +95,7 @@ struct LaunchParams {
   int rs_ctas;                   // CTAs that reduce (the rest only all-gather); <= gridDim.x
   uint32_t tma_stages;           // > 0: bulk-copy (TMA) data path with this many smem stages
   uint32_t tma_piece;            // elements per bulk copy (a tile's per-peer part is split; 0 = whole)
+  uint32_t tma_l2pf;             // 1: the producer also prefetches my own tile into L2
   uint64_t my_in_va;             // real mode: my input as this process addresses it
   uint64_t region_va[kMaxMembers][kMaxRegions];  // member i's registered region r, mapped here (0 = none)
   uint32_t intra_op;             // intra-replica collective (kIntraRS / kIntraAG), 0 = FTAR
@@ -710,6 +711,9 @@ __device__ __forceinline__ void tma_issue(const LaunchParams& p, const typename 
   }
   meta[s] = m;
   const uint32_t bytes = cnt * (uint32_t)In::kBytes;
+  // my own copy is read by the consumers with plain loads S-1 tiles later:
+  // start it towards L2 now so those loads do not pay the HBM latency
+  if (p.tma_l2pf && ((p.contrib >> me) & 1u)) bulk_prefetch_l2(src[me] + a, bytes);
   const uint32_t peers = p.contrib & ((1u << N) - 1u) & ~(1u << me);
   char* stage = smem + tma_stage_off() + (uint64_t)s * tma_stage_bytes(N, In::kBytes);
   if (peers == 0) {
@@ -832,17 +836,24 @@ __device__ int fold_tiles_tma(const LaunchParams& p, const typename In::T* const
     }
   } else {
     // ---- consumer warps
-    for (uint64_t j = 0; j < run; ++j) {
-      const uint32_t s = (uint32_t)(j % S);
-      // this member's own copy: local HBM, loaded before the tile lands
-      const uint64_t a = lo + (t0 + j) * TE;
+    // this member's own copy comes from local HBM by plain loads, issued one
+    // tile ahead so their latency hides behind the previous tile's fold
+    Raw mine[V], ahead[V];
+    auto load_mine = [&](uint64_t jj, Raw (&dst)[V]) {
+      const uint64_t a = lo + (t0 + jj) * TE;
       const uint32_t tcnt = (uint32_t)umin(TE, end - a);
-      Raw mine[V];
 #pragma unroll
       for (uint32_t v = 0; v < V; ++v) {
         const uint32_t off = (v * kTmaConsumers + (uint32_t)tid) * 4;
-        mine[v] = In::load4_if(mine_g, a + (off < tcnt ? off : 0), i_contribute);
+        dst[v] = In::load4_if(mine_g, a + (off < tcnt ? off : 0), i_contribute);
       }
+    };
+    if (run > 0) load_mine(0, ahead);
+    for (uint64_t j = 0; j < run; ++j) {
+      const uint32_t s = (uint32_t)(j % S);
+#pragma unroll
+      for (uint32_t v = 0; v < V; ++v) mine[v] = ahead[v];
+      if (j + 1 < run) load_mine(j + 1, ahead);
       mbar_wait(&full[s], (uint32_t)((j / S) & 1));
 #ifdef FTAR_DIAGNOSTICS
       if (trace && tid == 0 && j < 128) trace[256 + j] = globaltimer_ns();
@@ -2435,6 +2446,8 @@ int tma_ctas(uint64_t slice_bytes) {
 }
 // elements per bulk copy of the bulk-copy path (FTAR_TMA_PIECE_BYTES; 0 =
 // one copy per peer per tile), a multiple of 8 elements (16-byte granules)
+// L2 prefetch of the local tile by the bulk-copy producer (FTAR_TMA_L2PF=0 disables)
+uint32_t tma_l2pf() { return env_int("FTAR_TMA_L2PF", 1) != 0 ? 1u : 0u; }
 uint32_t tma_piece(uint64_t esz) {
   const int b = env_int("FTAR_TMA_PIECE_BYTES", 0);
   return b <= 0 ? 0u : (uint32_t)std::max<uint64_t>(8, ((uint64_t)b / esz) & ~7ull);
@@ -3154,32 +3167,32 @@ int ftar_geometry(uint64_t n_elems, int n, uint64_t* slice_elems, int* ctas, int
   return FTAR_OK;
 }
 
-int ftar_inflight_bound(ftar_ctx* c, uint64_t n_elems, int in_dtype, uint64_t chunk_bytes, int max_in_flight,
-                        int push, uint64_t* bytes_per_link, int* ctas, int* path) {
+int ftar_inflight_bound(int n, uint64_t n_elems, int in_dtype, uint64_t chunk_bytes, int max_in_flight, int push,
+                        uint64_t* bytes_per_link, int* ctas, int* path) {
   // The InflightMeter's figure (ftar.py:141-159): the most bytes one peer
   // link can have outstanding for this call, on the path launch_real picks.
   //   small push one-shot: the whole input, posted to each peer;
   //   bulk-copy reduce-scatter: G CTAs x (S-1) stages x one tile per peer;
   //   register path: G CTAs x 512 threads x U vectors of 4 elements per peer.
-  if (!c) return fail(FTAR_ST_INVARIANT, "null ctx");
-  int v = validate_common(in_dtype, c->n, chunk_bytes, max_in_flight);
+  if (n < 1 || n > kMaxMembers) return fail(FTAR_ST_INVARIANT, "ring size out of range");
+  int v = validate_common(in_dtype, n, chunk_bytes, max_in_flight);
   if (v) return v;
   const uint64_t esz = in_dtype == FTAR_DT_BF16 ? 2 : 4;
   const uint64_t in_bytes = n_elems * esz;
   LaunchParams p{};
-  fill_geometry(p, n_elems, chunk_bytes, max_in_flight, c->n);
+  fill_geometry(p, n_elems, chunk_bytes, max_in_flight, n);
   p.nelems = n_elems;
-  const bool small = c->n >= 2 && in_bytes > 0 && in_bytes <= small_bytes();
+  const bool small = n >= 2 && in_bytes > 0 && in_bytes <= small_bytes();
   PathChoice pc{kPathNone, 0, 0, 0};
   uint64_t bound = 0;
-  if (c->n >= 2 && in_bytes > 0) {
-    pc = choose_path(c->n, p, esz, small, false, push != 0);
+  if (n >= 2 && in_bytes > 0) {
+    pc = choose_path(n, p, esz, small, false, push != 0);
     if (pc.kind == kPathSmall) {
       bound = in_bytes;
     } else if (pc.kind == kPathBulk) {
-      bound = (uint64_t)pc.ctas * (pc.stages - 1) * tma_tile(c->n, (int)esz) * esz;
+      bound = (uint64_t)pc.ctas * (pc.stages - 1) * tma_tile(n, (int)esz) * esz;
     } else {
-      const int N = c->n;
+      const int N = n;
       const int budget = (N >= 6 && esz == 2) ? 8 : (N >= 5 ? 12 : 16);  // Unroll<N, In>
       const int u0 = (budget * 16 / (int)(esz * 4)) / N;
       const int umax = N <= 2 ? 16 : (N == 3 ? 6 : 8);
@@ -3326,6 +3339,7 @@ static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, ui
   }
   p.tma_stages = pc.stages;
   p.tma_piece = pc.piece;
+  p.tma_l2pf = tma_l2pf();
   const dim3 grid(pc.ctas, 1);
   cudaError_t e = small ? (in_dtype == FTAR_DT_BF16 ? launch_small<BF16In>(c->n, p, grid, st, false, pdl_on())
                                                     : launch_small<F32In>(c->n, p, grid, st, false, pdl_on()))
@@ -3507,6 +3521,7 @@ static int launch_local(ftar_ctx** ctxs, int n, const void* const* ins, int in_d
   if (!sgd_p && n >= 2 && tma_on() && p.p_base / (uint64_t)n >= tma_tile(n, in_dtype == FTAR_DT_BF16 ? 2 : 4)) {
     p.tma_stages = tma_stages_for(n, in_dtype == FTAR_DT_BF16 ? 2 : 4);
     p.tma_piece = tma_piece(in_dtype == FTAR_DT_BF16 ? 2 : 4);
+    p.tma_l2pf = tma_l2pf();
     if (g_local_ctas <= 0) G = std::min(G, tma_ctas(p.slice * (in_dtype == FTAR_DT_BF16 ? 2 : 4)));
   }
   const dim3 grid(G, n);

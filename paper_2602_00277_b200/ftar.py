@@ -491,13 +491,13 @@ class RingGroup:
         """(bytes, CTAs) one peer link can have outstanding for this call, on
         the path the library takes for it (ftar_inflight_bound: small push
         one-shot / bulk-copy reduce-scatter / register path)."""
-        if self._local or self.n < 2:
+        if self.n < 2:
             return 0, 0
         key = (self.n, nelems, dtype_code, cfg.chunk_bytes, cfg.max_in_flight, push)
         cache = self._bound_cache
         if key not in cache:
             b, g, path = C.c_uint64(), C.c_int(), C.c_int()
-            _lib.check(_lib.lib.ftar_inflight_bound(self._ctx, nelems, dtype_code, cfg.chunk_bytes,
+            _lib.check(_lib.lib.ftar_inflight_bound(self.n, nelems, dtype_code, cfg.chunk_bytes,
                                                     cfg.max_in_flight, int(push), C.byref(b), C.byref(g),
                                                     C.byref(path)),
                        "ftar_inflight_bound")

@@ -440,7 +440,7 @@ def test_inflight_bound_follows_the_path(ftar, monkeypatch):
         paths = {}
         for elems in (256, 1 << 21, 1 << 24):
             b, g, path = _lib.C.c_uint64(), _lib.C.c_int(), _lib.C.c_int()
-            _lib.check(_lib.lib.ftar_inflight_bound(gs[0].ctx, elems, _lib.DT_F32, cfg.chunk_bytes,
+            _lib.check(_lib.lib.ftar_inflight_bound(2, elems, _lib.DT_F32, cfg.chunk_bytes,
                                                     cfg.max_in_flight, 1, _lib.C.byref(b), _lib.C.byref(g),
                                                     _lib.C.byref(path)), "bound")
             paths[elems] = path.value
@@ -448,8 +448,8 @@ def test_inflight_bound_follows_the_path(ftar, monkeypatch):
             assert g.value >= 1
             if path.value == 1:
                 assert b.value == elems * 4
-            elif path.value == 3:  # n=2: U = 16 vectors of 4 fp32 per thread
-                assert b.value == g.value * 512 * 16 * 16
+            elif path.value == 3:  # n=2 f32: U = 8 vectors of 4 fp32 per thread
+                assert b.value == g.value * 512 * 8 * 16
             else:
                 assert path.value == 2 and b.value % g.value == 0 and b.value < elems * 4
         assert paths == {256: 1, 1 << 21: 3, 1 << 24: 2}

@@ -90,6 +90,35 @@ def test_classify_error():
     assert ftar.classify_error(ValueError("x")) == "fatal"
 
 
+def _bound(n, elems, dt=_lib.DT_F32, push=1, env=None):
+    b, g, path = C.c_uint64(), C.c_int(), C.c_int()
+    cfg = ftar.PipelineConfig()
+    rc = _lib.lib.ftar_inflight_bound(n, elems, dt, cfg.chunk_bytes, cfg.max_in_flight, push,
+                                      C.byref(b), C.byref(g), C.byref(path))
+    assert rc == 0
+    return b.value, g.value, path.value
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_inflight_bound_per_path(n, monkeypatch):
+    """The per-link in-flight bound follows the data path each bucket size takes
+    (host policy only: no device work)."""
+    for k in ("FTAR_TMA", "FTAR_SMALL_BYTES", "FTAR_TMA_MIN_SLICE_MIB", "FTAR_CTAS_TMA", "FTAR_CTAS_PUSH"):
+        monkeypatch.delenv(k, raising=False)
+    assert _bound(n, 0) == (0, 0, 0)
+    b, g, path = _bound(n, 256)  # 1 KB: the push one-shot posts the whole input
+    assert (b, path) == (1024, 1) and g >= 1
+    b, g, path = _bound(n, (2 << 20) // 4 * n)  # 2 MiB slices: register path
+    assert path == 3 and 1 <= g <= 128 and b % (g * 512 * 16) == 0
+    b, g, path = _bound(n, (64 << 20) // 4 * n)  # 64 MiB slices: bulk-copy reduce-scatter
+    assert path == 2 and 1 <= g <= 48 and b < 227 * 1024 * g
+    monkeypatch.setenv("FTAR_TMA", "0")
+    assert _bound(n, (64 << 20) // 4 * n)[2] == 3
+    monkeypatch.setenv("FTAR_CTAS_PUSH", "7")
+    assert _bound(n, (64 << 20) // 4 * n)[1] == 7
+    assert _lib.lib.ftar_inflight_bound(9, 1, 0, 8 << 20, 4, 0, None, None, None) == errors.ST_INVARIANT
+
+
 def test_inflight_meter():
     m = ftar.InflightMeter()
     m.sent(100, 2)

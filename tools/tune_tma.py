@@ -29,6 +29,8 @@ def main():
                                                   "pull (FTAR_NO_PUSH=1: members pull the reduced slices)")
     ap.add_argument("--pieces", default="0", help="comma list of FTAR_TMA_PIECE_BYTES for the tma cells "
                                                    "(bytes per bulk copy; 0 = one copy per peer per tile)")
+    ap.add_argument("--l2pf", default="1", help="comma list of FTAR_TMA_L2PF for the tma cells "
+                                                 "(1: the producer prefetches my own tile into L2)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -85,20 +87,22 @@ def main():
             buf.copy_(torch.randn(elems, device=dev).to(tdt))
             out = group.alloc_bucket(elems, torch.float32)
             steps = max(5, min(args.steps * 8, int(args.steps * 256 / max(mib, 1))))
-            cells = [("tma", c, pc) for pc in args.pieces.split(",") for c in args.tma_ctas.split(",") if c] + \
-                    [("ldg", c, "0") for c in args.ldg_ctas.split(",") if c]
+            cells = [("tma", c, pc, pf) for pf in args.l2pf.split(",") for pc in args.pieces.split(",")
+                     for c in args.tma_ctas.split(",") if c] + \
+                    [("ldg", c, "0", "0") for c in args.ldg_ctas.split(",") if c]
             for ag in args.ag.split(","):
                 os.environ["FTAR_NO_PUSH"] = "1" if ag == "pull" else "0"
-                for path, c, piece in cells:
+                for path, c, piece, pf in cells:
                     os.environ["FTAR_TMA"] = "1" if path == "tma" else "0"
                     os.environ["FTAR_TMA_PIECE_BYTES"] = piece
+                    os.environ["FTAR_TMA_L2PF"] = pf
                     _lib.lib.ftar_set_tuning(int(c), 0)
                     t = timed(buf, out, steps)
                     if rank == 0:
                         busbw = elems * ib / t * 2 * (n - 1) / n / 1e9
                         ingress = (n - 1) / n * elems * (ib + 4) / t / 1e9
                         print(json.dumps({"n": n, "dtype": dt, "MiB": mib, "path": path, "ag": ag, "ctas": int(c),
-                                          "piece": int(piece),
+                                          "piece": int(piece), "l2pf": int(pf),
                                           "us": round(t * 1e6, 2), "busbw": round(busbw, 1),
                                           "nvlink_ingress_GBps": round(ingress, 1)}), flush=True)
             os.environ["FTAR_NO_PUSH"] = "0"
