@@ -81,8 +81,9 @@ class ClockSampler:
                ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
                ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown")]
 
-    def __init__(self, cuda_index: int):
+    def __init__(self, cuda_index: int, interval_s: float | None = None):
         self.cuda_index = cuda_index
+        self.interval_s = float(os.environ.get("FTAR_CLOCK_INTERVAL_S", 0.002)) if interval_s is None else interval_s
         self.samples = []
         self.stop = threading.Event()
         self.err = None
@@ -117,7 +118,7 @@ class ClockSampler:
             except Exception as exc:  # noqa: BLE001
                 self.err = str(exc)[:120]
                 return
-            time.sleep(0.002)
+            time.sleep(self.interval_s)
 
     def __exit__(self, *exc):
         self.stop.set()
@@ -256,23 +257,40 @@ def _ncu_traffic(args):
 
 
 def timed_loop(fn, steps, stream, torch, drain=None):
-    """Run fn() `steps` times; CUDA events per launch and around the loop."""
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    """The timed region: fn() `steps` times between two CUDA events on the
+    launching stream (nothing else on the stream: an event recorded between
+    two launches costs ~5 us, 1.5% of a 0.37 ms step).  Returns (total s,
+    total / steps)."""
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
+    for _ in range(steps):
+        fn()
+    if drain is not None:
+        drain()
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    total = t_start.elapsed_time(t_end) / 1e3
+    return total, total / steps
+
+
+def launch_times(fn, steps, stream, torch, drain=None):
+    """Average launch duration (s) of the dominant kernel: a second pass of
+    `steps` calls right after the timed region with a CUDA event pair around
+    every launch (the roofline's denominator).  The events themselves add a
+    few us per launch, so this is an upper bound on the kernel time."""
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for i in range(steps):
         ev[i][0].record(stream)
         fn()
         ev[i][1].record(stream)
     if drain is not None:
         drain()
-    t_end.record(stream)
     torch.cuda.synchronize()
     per = [a.elapsed_time(b) for a, b in ev]
     if os.environ.get("FTAR_BENCH_VERBOSE"):
         print(json.dumps({"rank": int(os.environ.get("RANK", 0)), "per_launch_ms": [round(x, 4) for x in per]}),
               file=sys.stderr, flush=True)
-    return t_start.elapsed_time(t_end) / 1e3, sum(per) / len(per) / 1e3
+    return sum(per) / len(per) / 1e3
 
 
 class NvlinkPM:
@@ -415,14 +433,17 @@ def run_single(args):
         for b, h in zip(bufs, hosts):
             b.copy_(h)
     torch.cuda.synchronize()
-    # live DRAM traffic of the timed calls (CUPTI PM sampling; the window
+    # live DRAM traffic of the launch pass (CUPTI PM sampling; the window
     # holds only this kernel: inputs are resident, nothing else runs)
     pm = None if args.no_pm else NvlinkPM(0, metrics=("dram__bytes_read.sum", "dram__bytes_write.sum"),
                                           keys=("read", "write"))
     with ClockSampler(0) as clk:
+        total, _ = timed_loop(step, args.steps, stream, torch, drain=drain)
+        # the launch pass: per-launch events and the PM counters (sampling at
+        # 50 us perturbs the kernel by ~1.5%, so neither is in the timed region)
         if pm is not None:
             pm.start()
-        total, per_launch = timed_loop(step, args.steps, stream, torch, drain=drain)
+        per_launch = launch_times(step, args.steps, stream, torch, drain=drain)
         pmw = pm.stop() if pm is not None else None
     if pm is not None:
         pm.close()
@@ -440,15 +461,18 @@ def run_single(args):
             "unit": "GB/s", "frac": round(alg_bytes / per_launch / 1e9 / hbm_peak, 4),
             "traffic": (round((pmw["read"] + pmw["write"]) / args.steps) if pmw is not None
                         else args.traffic if args.traffic is not None else _ncu_traffic(args)),
-            "traffic_source": ("dram__bytes_read.sum + dram__bytes_write.sum per launch over the timed calls, "
+            "traffic_source": ("dram__bytes_read.sum + dram__bytes_write.sum per launch over the K-launch pass after the timed region, "
                                "CUPTI PM sampling (live)" if pmw is not None
                                else "committed ncu capture (profiles/r01/ncu): " + str(pm.err if pm else "pm off")),
             "pm_window": pmw,
-            "kernel": "local_oneshot_kernel",
+            "kernel": ("local_oneshot_kernel" if os.environ.get("FTAR_LOCAL_BULK", "1") == "0" or args.inplace
+                       or os.environ.get("FTAR_TMA", "1") == "0" else "local_bulk_kernel"),
             "algorithmic_bytes_per_launch": alg_bytes,
             "definition": "n*E*(in_bytes+4): every replica's bucket read once, every replica's fp32 result "
                           "written once; peak = MEASURED_PEAKS.json hbm_gbs (measured copy)",
-            "avg_launch_ms": round(per_launch * 1e3, 4)}
+            "avg_launch_ms": round(per_launch * 1e3, 4),
+            "launch_timing": "CUDA events around each of K launches, in a pass right after the timed region "
+                             "(events between launches cost ~5 us each, so they stay out of the timed region)"}
     # the same replicas through the multi-GPU protocol kernel (allreduce_kernel,
     # members as CTA groups of one cooperative launch): the product kernel's
     # code path, timed here for the record (not the headline)
@@ -573,8 +597,6 @@ def run_multi(args, rank, world, local_rank):
     pm = NvlinkPM(local_rank) if not args.no_pm else None
     with ClockSampler(local_rank) as clk:
         c0 = nvl.read()  # (the counters cover the untimed collective below too: steps + 1 calls)
-        if pm is not None:
-            pm.start()
         # One untimed collective right before the window: it is a device-side
         # barrier, so the timed region starts on every rank when all streams
         # reach the same point, instead of absorbing the ranks' host-side exit
@@ -582,8 +604,14 @@ def run_multi(args, rank, world, local_rank):
         # timed launch (measured: 0.7-1.5 ms vs 0.64 ms steady at 256 MiB, N=4;
         # host work between this call and the window would reopen the skew).
         step()
-        total, per_launch = timed_loop(step, args.steps, stream, torch, drain)
+        total, _ = timed_loop(step, args.steps, stream, torch, drain)
         c1 = nvl.read()
+        # the launch pass: per-launch events and the PM counters (neither in
+        # the timed region); the untimed call first is the device-side barrier
+        step()
+        if pm is not None:
+            pm.start()
+        per_launch = launch_times(step, args.steps, stream, torch, drain)
         pmw = pm.stop() if pm is not None else None
     if pm is not None:
         pm.close()
@@ -601,7 +629,7 @@ def run_multi(args, rank, world, local_rank):
     if nv_meas is None and pmw is not None:
         # user data bytes (what the kernels moved; the link also carries
         # packet headers: nvlrx__bytes ~1.25x, reported beside)
-        nv_meas = [pmw["tx_user"] / (args.steps + 1), pmw["rx_user"] / (args.steps + 1)]
+        nv_meas = [pmw["tx_user"] / args.steps, pmw["rx_user"] / args.steps]
     all_nv = [None] * n
     dist.all_gather_object(all_nv, nv_meas)
     all_pm = [None] * n
@@ -615,7 +643,7 @@ def run_multi(args, rank, world, local_rank):
             "unit": "GB/s", "frac": round(nv_bytes / per_launch / 1e9 / NVLINK_PEER_GBS, 4),
             "traffic": round(max(rx)) if rx else None,
             "traffic_source": ("NVLink RX user-data bytes per launch (nvlrx__bytes_data_user.sum, all links) from "
-                               "CUPTI PM sampling of each GPU across the timed calls (+1 untimed), max over ranks; "
+                               "CUPTI PM sampling of each GPU across the K-launch pass after the timed region, max over ranks; "
                                "nvlink_pm_window has the totals incl. packet overhead (nvlrx__bytes.sum)"
                                if rx else "NVLink counters unavailable: " + json.dumps(all_pm[0])[:200]),
             "traffic_over_algorithmic": round(max(rx) / nv_bytes, 4) if rx else None,
@@ -628,7 +656,9 @@ def run_multi(args, rank, world, local_rank):
                           "segment, AG receives every peer's fp32 result; peak = 770 GB/s measured peer copy "
                           "per direction (B200_PROFILING.md fallback; MEASURED_PEAKS.json has no NVLink entry)",
             "frac_of_nominal_900": round(nv_bytes / per_launch / 1e9 / NVLINK_NOMINAL_GBS, 4),
-            "avg_launch_ms": round(per_launch * 1e3, 4)}
+            "avg_launch_ms": round(per_launch * 1e3, 4),
+            "launch_timing": "CUDA events around each of K launches, in a pass right after the timed region "
+                             "(events between launches cost ~5 us each, so they stay out of the timed region)"}
     e2e = None
     if not args.no_e2e:
         phost = host.pin_memory()
@@ -752,7 +782,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-check", action="store_true", help="skip the oracle self-check")
-    ap.add_argument("--no-pm", action="store_true", help="N>=2: no CUPTI PM sampling of the NVLink counters")
+    ap.add_argument("--no-pm", action="store_true", help="no CUPTI PM sampling (N=1: DRAM bytes, N>=2: NVLink bytes)")
     ap.add_argument("--no-protocol", action="store_true", help="N=1: skip the protocol-kernel record")
     ap.add_argument("--unregistered", action="store_true",
                     help="N>=2: buckets are ordinary torch.empty tensors (reference call shape), not pool buffers")

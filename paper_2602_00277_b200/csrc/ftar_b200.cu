@@ -2083,7 +2083,29 @@ struct LocalParams {
   float scale;
   uint32_t flags_in;
   uint32_t contrib;
+  uint32_t stages;          // local_bulk_kernel: smem pipeline stages
 };
+
+// Direct mode's completion: the last CTA to arrive publishes every member's
+// status (outputs were written during the fold; no grid barrier needed).
+template <int N>
+__device__ __forceinline__ void local_direct_finish(const LocalParams& p, uint32_t nf_cta, uint64_t ntiles) {
+  if (threadIdx.x != 0) return;
+  if (nf_cta) atomicOr(p.flags, 1u);
+  __threadfence();
+  if (atomicAdd(p.arrive, 1u) == gridDim.x - 1) {
+    fence_acq_rel_gpu();
+    const bool nonfinite = ld_relaxed_gpu32(p.flags) != 0;
+    *p.flags = 0;
+    *p.arrive = 0;
+    for (int j = 0; j < N; ++j) {
+      p.ctl[j]->progress = ntiles + 1;
+      if (nonfinite) p.ctl[j]->detail = -1;
+    }
+    if (nonfinite) __threadfence_system();
+    for (int j = 0; j < N; ++j) p.ctl[j]->done = mk_flag(p.tag[j], nonfinite ? ST_NUMERICAL : ST_OK);
+  }
+}
 
 template <int N, class In>
 __global__ void __launch_bounds__(kThreads, 1) local_oneshot_kernel(const __grid_constant__ LocalParams p) {
@@ -2138,29 +2160,15 @@ __global__ void __launch_bounds__(kThreads, 1) local_oneshot_kernel(const __grid
   }
   if (__any_sync(0xffffffffu, nf != 0) && (tid & 31) == 0) atomicOr(&s_nf, 1u);
   __syncthreads();
-  if (tid == 0 && s_nf) atomicOr(p.flags, 1u);
   if (direct) {
     // Direct mode wrote every output during the fold (outputs are undefined
     // after a non-finite sum, as for out-of-place calls), so only the status
     // needs every CTA: an arrival counter instead of a grid barrier, which
     // also lets this mode launch without the cooperative-launch overhead.
-    if (tid == 0) {
-      __threadfence();
-      if (atomicAdd(p.arrive, 1u) == gridDim.x - 1) {
-        fence_acq_rel_gpu();
-        const bool nonfinite = ld_relaxed_gpu32(p.flags) != 0;
-        *p.flags = 0;
-        *p.arrive = 0;
-        for (int j = 0; j < N; ++j) {
-          p.ctl[j]->progress = ntiles + 1;
-          if (nonfinite) p.ctl[j]->detail = -1;
-        }
-        if (nonfinite) __threadfence_system();
-        for (int j = 0; j < N; ++j) p.ctl[j]->done = mk_flag(p.tag[j], nonfinite ? ST_NUMERICAL : ST_OK);
-      }
-    }
+    local_direct_finish<N>(p, s_nf, ntiles);
     return;
   }
+  if (tid == 0 && s_nf) atomicOr(p.flags, 1u);
   grid.sync();
   const bool bad = ld_relaxed_sys32(p.flags) != 0;
   if (!bad && !direct) {
@@ -2205,6 +2213,202 @@ __global__ void __launch_bounds__(kThreads, 1) local_oneshot_kernel(const __grid
       p.ctl[j]->done = mk_flag(p.tag[j], st);
     }
   }
+}
+
+// In-process one-shot, direct mode, through the bulk-copy engine.  The
+// register form above alternates a burst of loads with a burst of stores, so
+// HBM sees reads and writes in phases; here warp 15 keeps S-1 stages of every
+// member's tile in flight (cp.async.bulk global -> shared, mbarrier
+// complete_tx) while warps 0..14 fold the landed stage in the reference order
+// and stream the sums to every member's output.  Tiles are grid-strided so
+// all CTAs work in one compact window of each input.
+__host__ __device__ constexpr uint32_t lb_vecs(int n, int in_bytes) {
+  // ~32 KB per stage over all n members (>= 6 stages in 227 KB up to n = 4)
+  const uint32_t per_vec = (uint32_t)n * kTmaConsumers * 4u * (uint32_t)in_bytes;
+  const uint32_t v = 32768u / per_vec;
+  return v < 1 ? 1u : (v > 4 ? 4u : v);
+}
+__host__ __device__ constexpr uint32_t lb_tile(int n, int in_bytes) {
+  return kTmaConsumers * 4u * lb_vecs(n, in_bytes);
+}
+__host__ __device__ __forceinline__ uint64_t lb_stage_bytes(int n, int in_bytes) {
+  return (uint64_t)n * lb_tile(n, in_bytes) * (uint64_t)in_bytes;
+}
+__host__ __device__ __forceinline__ uint32_t lb_stages_for(int n, int in_bytes) {
+  const uint64_t s = (kTmaSmemMax - tma_stage_off()) / lb_stage_bytes(n, in_bytes);
+  return (uint32_t)(s > kTmaMaxStages ? kTmaMaxStages : s);
+}
+
+template <int N, class In>
+__device__ __forceinline__ float lb_fold_one(const char* stage, uint32_t off, int own, uint32_t contrib) {
+  constexpr uint32_t TE = lb_tile(N, In::kBytes);
+  float acc = 0.0f;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    int m = own + k;
+    if (m >= N) m -= N;
+    float x = 0.0f;
+    if ((contrib >> m) & 1u) {
+      const uint64_t at = (uint64_t)m * TE + off;
+      if (In::kBytes == 4) x = *reinterpret_cast<const float*>(stage + at * 4);
+      else x = __uint_as_float((uint32_t)*reinterpret_cast<const uint16_t*>(stage + at * 2) << 16);
+    }
+    acc = k == 0 ? x : __fadd_rn(acc, x);
+  }
+  return acc;
+}
+
+template <int N, class In>
+__global__ void __launch_bounds__(kThreads, 1) local_bulk_kernel(const __grid_constant__ LocalParams p) {
+  using T = typename In::T;
+  using Raw = typename In::Raw;
+  constexpr uint32_t V = lb_vecs(N, In::kBytes);
+  constexpr uint32_t TE = lb_tile(N, In::kBytes);
+  extern __shared__ __align__(1024) char smem[];
+  __shared__ uint32_t s_nf;
+  const int tid = threadIdx.x;
+  const uint32_t S = p.stages;
+  uint64_t* full = tma_full(smem);
+  uint64_t* empty = tma_empty(smem);
+  TmaMeta* meta = tma_meta(smem);
+  if (tid == 0) {
+    s_nf = 0;
+    for (uint32_t s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTmaConsumers / 32);
+    }
+    fence_mbar_init();
+    if (blockIdx.x == 0)
+      for (int j = 0; j < N; ++j) p.ctl[j]->started = p.tag[j];
+  }
+  __syncthreads();
+  LaunchParams g{};
+  g.p_base = p.p_base;
+  g.p_rem = p.p_rem;
+  g.ebase = p.ebase;
+  const uint32_t contrib = p.contrib & ((1u << N) - 1u);
+  const bool do_scale = (p.flags_in & FTAR_F_SCALE) != 0;
+  const uint64_t E = p.nelems, Ev = E & ~7ull;  // bulk part: 16-byte granules
+  const uint64_t ntiles = (Ev + TE - 1) / TE;
+  const uint64_t G = gridDim.x;
+  const uint64_t run = blockIdx.x < ntiles ? (ntiles - blockIdx.x + G - 1) / G : 0;
+  uint32_t nf = 0;
+  if (tid >= (int)kTmaConsumers) {
+    if (tid == kTmaProducer) {
+      OwnerRun orun;
+      for (uint64_t j = 0; j < run; ++j) {
+        const uint32_t s = (uint32_t)(j % S);
+        if (j >= S) mbar_wait(&empty[s], (uint32_t)(((j / S) - 1) & 1));
+        const uint64_t a = (blockIdx.x + j * G) * TE;
+        const uint32_t cnt = (uint32_t)umin(TE, Ev - a);
+        if (a < orun.sbeg || a >= orun.send) {
+          owner_of(a, g, N, orun.owner, orun.send);
+          orun.sbeg = a;
+        }
+        TmaMeta m;
+        m.a = a;
+        m.cnt = cnt;
+        m.s0 = m.s1 = orun.owner;
+        m.bnd = 0xffffffffu;
+        if (orun.send < a + cnt) {  // one owner change inside the tile (segments >= a tile)
+          const uint64_t b = orun.send;
+          owner_of(b, g, N, orun.owner, orun.send);
+          orun.sbeg = b;
+          m.s1 = orun.owner;
+          m.bnd = (uint32_t)(b - a);
+        }
+        meta[s] = m;
+        char* stage = smem + tma_stage_off() + (uint64_t)s * lb_stage_bytes(N, In::kBytes);
+        if (contrib == 0) {
+          mbar_arrive(&full[s]);
+          continue;
+        }
+        const uint32_t bytes = cnt * (uint32_t)In::kBytes;
+        mbar_expect_tx(&full[s], bytes * (uint32_t)__popc(contrib));
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+          if ((contrib >> k) & 1u)
+            bulk_g2s(stage + (uint64_t)k * TE * In::kBytes, static_cast<const T*>(p.in[k]) + a, bytes, &full[s]);
+      }
+    }
+  } else {
+    for (uint64_t j = 0; j < run; ++j) {
+      const uint32_t s = (uint32_t)(j % S);
+      mbar_wait(&full[s], (uint32_t)((j / S) & 1));
+      const TmaMeta m = meta[s];
+      const char* stage = smem + tma_stage_off() + (uint64_t)s * lb_stage_bytes(N, In::kBytes);
+      float acc[V][4];
+#pragma unroll
+      for (uint32_t v = 0; v < V; ++v) {
+        const uint32_t off = (v * kTmaConsumers + (uint32_t)tid) * 4;
+        acc[v][0] = acc[v][1] = acc[v][2] = acc[v][3] = 0.f;
+        if (off < m.cnt) {
+          if (off + 4 <= m.bnd || off >= m.bnd) {
+            const int own = off >= m.bnd ? m.s1 : m.s0;
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+              int mm = own + k;
+              if (mm >= N) mm -= N;
+              float x[4];
+              if ((contrib >> mm) & 1u)
+                In::cvt4(*reinterpret_cast<const Raw*>(stage + ((uint64_t)mm * TE + off) * In::kBytes), x);
+              else
+                x[0] = x[1] = x[2] = x[3] = 0.0f;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) acc[v][i] = k == 0 ? x[i] : __fadd_rn(acc[v][i], x[i]);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              acc[v][i] = lb_fold_one<N, In>(stage, off + i, off + i >= m.bnd ? m.s1 : m.s0, contrib);
+          }
+        }
+      }
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+      for (uint32_t v = 0; v < V; ++v) {
+        const uint32_t off = (v * kTmaConsumers + (uint32_t)tid) * 4;
+        if (off < m.cnt) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            nf |= nonfinite_bits(acc[v][i]) ? 1u : 0u;
+            if (do_scale) acc[v][i] = __fmul_rn(acc[v][i], p.scale);
+          }
+          const uint4 r = make_uint4(__float_as_uint(acc[v][0]), __float_as_uint(acc[v][1]),
+                                     __float_as_uint(acc[v][2]), __float_as_uint(acc[v][3]));
+#pragma unroll
+          for (int k = 0; k < N; ++k) st_stream(p.out[k] + m.a + off, r);
+        }
+      }
+    }
+    // the < 8-element ragged tail: plain loads by the last CTA's first warp
+    if (Ev < E && blockIdx.x == G - 1 && tid < 32) {
+      const T* srcs[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) srcs[k] = static_cast<const T*>(p.in[k]);
+      for (uint64_t e = Ev + tid; e < E; e += 32) {
+        int own;
+        uint64_t send;
+        owner_of(e, g, N, own, send);
+        float acc = 0.0f;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          int mm = own + k;
+          if (mm >= N) mm -= N;
+          const float x = ((contrib >> mm) & 1u) ? In::scalar(srcs[mm], e) : 0.0f;
+          acc = k == 0 ? x : __fadd_rn(acc, x);
+        }
+        nf |= nonfinite_bits(acc) ? 1u : 0u;
+        if (do_scale) acc = __fmul_rn(acc, p.scale);
+#pragma unroll
+        for (int k = 0; k < N; ++k) p.out[k][e] = acc;
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, nf != 0) && (tid & 31) == 0) atomicOr(&s_nf, 1u);
+  __syncthreads();
+  local_direct_finish<N>(p, s_nf, ntiles);
 }
 
 // ---------------------------------------------------------------- diagnostics
@@ -2807,6 +3011,32 @@ cudaError_t oneshot_dispatch(int n, const LocalParams& lp, dim3 grid, cudaStream
   // the staged (in-place) mode needs its grid barrier; direct mode does not
   if (lp.stage == nullptr) return cudaLaunchKernel(fn, grid, dim3(kThreads), args, 0, st);
   return cudaLaunchCooperativeKernel(fn, grid, dim3(kThreads), args, 0, st);
+}
+
+template <int N, class In>
+cudaError_t local_bulk_launch_n(const LocalParams& lp, dim3 grid, cudaStream_t st) {
+  auto fn = local_bulk_kernel<N, In>;
+  static bool attr_set[64] = {};  // per template instance and device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemMax);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
+  const size_t dyn = (size_t)(tma_stage_off() + (uint64_t)lp.stages * lb_stage_bytes(N, In::kBytes));
+  fn<<<grid, kThreads, dyn, st>>>(lp);
+  return cudaGetLastError();
+}
+
+template <class In>
+cudaError_t local_bulk_dispatch(int n, const LocalParams& lp, dim3 grid, cudaStream_t st) {
+  switch (n) {
+#define CASE(K) case K: return local_bulk_launch_n<K, In>(lp, grid, st);
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 template <class In>
@@ -3489,10 +3719,25 @@ static int launch_local(ftar_ctx** ctxs, int n, const void* const* ins, int in_d
     lp.scale = scale;
     lp.flags_in = flags;
     lp.contrib = p.contrib;
-    const int bps = in_dtype == FTAR_DT_BF16 ? oneshot_blocks_per_sm<BF16In>(n) : oneshot_blocks_per_sm<F32In>(n);
-    const dim3 grid(std::max(1, sms * std::max(bps, 1)));
-    cudaError_t e = in_dtype == FTAR_DT_BF16 ? oneshot_dispatch<BF16In>(n, lp, grid, st)
-                                              : oneshot_dispatch<F32In>(n, lp, grid, st);
+    const int esz = in_dtype == FTAR_DT_BF16 ? 2 : 4;
+    uint64_t orbits = 0;
+    for (int i = 0; i < n; ++i) orbits |= reinterpret_cast<uint64_t>(ins[i]) | reinterpret_cast<uint64_t>(outs[i]);
+    // the bulk-copy form: direct mode, 16-byte aligned buffers, every
+    // segment at least one tile (at most one owner change per tile)
+    const bool bulk = !alias && (orbits & 15u) == 0 && tma_on() && env_int("FTAR_LOCAL_BULK", 1) != 0 &&
+                      n_elems >= 8 && p.p_base / (uint64_t)n >= lb_tile(n, esz);
+    cudaError_t e;
+    if (bulk) {
+      lp.stages = lb_stages_for(n, esz);
+      const dim3 grid(std::max(1, env_int("FTAR_LOCAL_BULK_CTAS", sms)));
+      e = in_dtype == FTAR_DT_BF16 ? local_bulk_dispatch<BF16In>(n, lp, grid, st)
+                                   : local_bulk_dispatch<F32In>(n, lp, grid, st);
+    } else {
+      const int bps = in_dtype == FTAR_DT_BF16 ? oneshot_blocks_per_sm<BF16In>(n) : oneshot_blocks_per_sm<F32In>(n);
+      const dim3 grid(std::max(1, sms * std::max(bps, 1)));
+      e = in_dtype == FTAR_DT_BF16 ? oneshot_dispatch<BF16In>(n, lp, grid, st)
+                                   : oneshot_dispatch<F32In>(n, lp, grid, st);
+    }
     if (e != cudaSuccess) {
       for (int i = 0; i < n; ++i) ctxs[i]->pop_last();
       return cuda_fail(e, "local one-shot cooperative launch");

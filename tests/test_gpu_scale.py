@@ -165,12 +165,15 @@ def _tma_cases():
     return out
 
 
+@pytest.mark.parametrize("protocol", [True, False], ids=["protocol", "oneshot"])
 @pytest.mark.parametrize("c", _tma_cases(), ids=lambda c: f"n{c['n']}-{c['dtype']}-e{c['elems']}-S{c['chunk']}-C{c['C']}"
                                                         f"-b{len(c['behind'])}{'-inplace' if c['inplace'] else ''}")
-def test_tma_geometry_edges(ftar, c):
+def test_tma_geometry_edges(ftar, c, protocol):
     """Multi-partition buckets whose segment boundaries fall at every offset
     within a tile, ragged slice tails, garbage in behind replicas' buffers;
-    the bulk-copy path and the register path both bit-exact."""
+    the bulk-copy path and the register path both bit-exact -- in the
+    multi-GPU protocol kernel and in the in-process one-shot (local_bulk_kernel
+    vs local_oneshot_kernel)."""
     n = c["n"]
     arrays = orc.member_inputs(n, c["elems"], seed=c["elems"], dtype=c["dtype"])
     contrib = [m not in c["behind"] for m in range(n)]
@@ -182,7 +185,7 @@ def test_tma_geometry_edges(ftar, c):
     assert min(p for _, p in plan) // n >= 2048
     cfg = ftar.PipelineConfig(chunk_bytes=c["chunk"], max_in_flight=c["C"], per_chunk_timeout_s=10.0)
     tdt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
-    ring = ftar.LocalRing(n, device=DEV, max_bucket_bytes=c["elems"] * 4, protocol=True)
+    ring = ftar.LocalRing(n, device=DEV, max_bucket_bytes=c["elems"] * 4, protocol=protocol)
     try:
         ring.reconfig(contributors=[m for m in range(n) if contrib[m]])
         for tma in ("1", "0"):
