@@ -607,10 +607,11 @@ def run_multi(args, rank, world, local_rank):
         total, _ = timed_loop(step, args.steps, stream, torch, drain)
         c1 = nvl.read()
         # the launch pass: per-launch events and the PM counters (neither in
-        # the timed region); the untimed call first is the device-side barrier
-        step()
+        # the timed region); the untimed call after the sampler's start is
+        # the device-side barrier that absorbs the ranks' start skew
         if pm is not None:
             pm.start()
+        step()
         per_launch = launch_times(step, args.steps, stream, torch, drain)
         pmw = pm.stop() if pm is not None else None
     if pm is not None:
@@ -629,7 +630,7 @@ def run_multi(args, rank, world, local_rank):
     if nv_meas is None and pmw is not None:
         # user data bytes (what the kernels moved; the link also carries
         # packet headers: nvlrx__bytes ~1.25x, reported beside)
-        nv_meas = [pmw["tx_user"] / args.steps, pmw["rx_user"] / args.steps]
+        nv_meas = [pmw["tx_user"] / (args.steps + 1), pmw["rx_user"] / (args.steps + 1)]
     all_nv = [None] * n
     dist.all_gather_object(all_nv, nv_meas)
     all_pm = [None] * n
@@ -643,7 +644,7 @@ def run_multi(args, rank, world, local_rank):
             "unit": "GB/s", "frac": round(nv_bytes / per_launch / 1e9 / NVLINK_PEER_GBS, 4),
             "traffic": round(max(rx)) if rx else None,
             "traffic_source": ("NVLink RX user-data bytes per launch (nvlrx__bytes_data_user.sum, all links) from "
-                               "CUPTI PM sampling of each GPU across the K-launch pass after the timed region, max over ranks; "
+                               "CUPTI PM sampling of each GPU across the K-launch pass after the timed region (+1 untimed call), max over ranks; "
                                "nvlink_pm_window has the totals incl. packet overhead (nvlrx__bytes.sum)"
                                if rx else "NVLink counters unavailable: " + json.dumps(all_pm[0])[:200]),
             "traffic_over_algorithmic": round(max(rx) / nv_bytes, 4) if rx else None,

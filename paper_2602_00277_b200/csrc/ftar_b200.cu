@@ -94,8 +94,7 @@ struct LaunchParams {
   int diag;                      // timing diagnostics: 1 = RS stores skipped, 2 = RS reads local only
   int rs_ctas;                   // CTAs that reduce (the rest only all-gather); <= gridDim.x
   uint32_t tma_stages;           // > 0: bulk-copy (TMA) data path with this many smem stages
-  uint32_t tma_piece;            // elements per bulk copy (a tile's per-peer part is split; 0 = whole)
-  uint32_t tma_l2pf;             // 1: the producer also prefetches my own tile into L2
+  uint32_t early_trigger;        // 1: PDL trigger once the peers have read my entry record
   uint64_t my_in_va;             // real mode: my input as this process addresses it
   uint64_t region_va[kMaxMembers][kMaxRegions];  // member i's registered region r, mapped here (0 = none)
   uint32_t intra_op;             // intra-replica collective (kIntraRS / kIntraAG), 0 = FTAR
@@ -711,9 +710,6 @@ __device__ __forceinline__ void tma_issue(const LaunchParams& p, const typename 
   }
   meta[s] = m;
   const uint32_t bytes = cnt * (uint32_t)In::kBytes;
-  // my own copy is read by the consumers with plain loads S-1 tiles later:
-  // start it towards L2 now so those loads do not pay the HBM latency
-  if (p.tma_l2pf && ((p.contrib >> me) & 1u)) bulk_prefetch_l2(src[me] + a, bytes);
   const uint32_t peers = p.contrib & ((1u << N) - 1u) & ~(1u << me);
   char* stage = smem + tma_stage_off() + (uint64_t)s * tma_stage_bytes(N, In::kBytes);
   if (peers == 0) {
@@ -721,17 +717,9 @@ __device__ __forceinline__ void tma_issue(const LaunchParams& p, const typename 
     return;
   }
   mbar_expect_tx(&full[s], bytes * (uint32_t)__popc(peers));
-  // several smaller copies per peer where the ring is small: an SM's copy
-  // engine needs many copies in flight, not just many bytes
-  const uint32_t pe = p.tma_piece && p.tma_piece < cnt ? p.tma_piece : cnt;
-  for (uint32_t o = 0; o < cnt; o += pe) {
-    const uint32_t c = (uint32_t)umin(pe, cnt - o);
 #pragma unroll
-    for (int k = 0; k < N; ++k)
-      if ((peers >> k) & 1u)
-        bulk_g2s(stage + ((uint64_t)tma_slot(k, me) * TE + o) * In::kBytes, src[k] + a + o, c * (uint32_t)In::kBytes,
-                 &full[s]);
-  }
+  for (int k = 0; k < N; ++k)
+    if ((peers >> k) & 1u) bulk_g2s(stage + (uint64_t)tma_slot(k, me) * TE * In::kBytes, src[k] + a, bytes, &full[s]);
 }
 
 // Fold one 4-element vector (elements off..off+3 of the tile) whose fold
@@ -1095,6 +1083,9 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
           const bool unmapped = !p.emulated && ((is_region_ref(in_off) && s_pin[j] == 0) ||
                                                 (oo != ~0ull && is_region_ref(oo) && s_pout[j] == 0));
           if (st == ST_OK && unmapped) st = ST_PROTOCOL;
+          // tell member j its record is consumed (after the loads above: the
+          // store is control-dependent on their values)
+          if (st == ST_OK) st_relaxed_sys(&ph->ent_ack[me], tag);
         }
       }
     }
@@ -1109,7 +1100,31 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
       }
       s_pushok = ((p.flags & kFlagPush) && !nopush) ? 1u : 0u;
     }
+    // Early PDL trigger.  The next call on this stream may run its entry
+    // (which writes only the entry slots and its own control slot) as soon
+    // as every peer has consumed my record of this call -- it then overlaps
+    // this call's whole reduce-scatter instead of only its completion tail.
+    // A peer that does not ack within 100 us just leaves the trigger to the
+    // end of the call.
+    if (N > 1 && !p.emulated && !bad && p.early_trigger) {
+      bool acked = true;
+      if (j < N && j != me) {
+        acked = false;
+        const uint64_t ta = globaltimer_ns();
+        for (uint32_t it = 0;; ++it) {
+          if (ld_relaxed_sys(&hdr->ent_ack[j]) == tag) {
+            acked = true;
+            break;
+          }
+          if ((it & 15u) == 15u && globaltimer_ns() - ta > 100000ull) break;
+          if (it > 4) __nanosleep(64);
+        }
+      }
+      if (__all_sync(0xffffffffu, acked) && tid == 0) pdl_trigger();
+    }
   }
+  // CTAs other than 0 gate nothing the next call's entry touches
+  if (blockIdx.x != 0 && tid == 0 && p.early_trigger) pdl_trigger();
   // The previous kernel on this stream (if it let us start early) has now
   // completed and its writes are visible; a no-op for ordinary launches.
   pdl_wait();
@@ -2648,14 +2663,6 @@ int tma_ctas(uint64_t slice_bytes) {
   const uint64_t per = (uint64_t)env_int("FTAR_TMA_BYTES_PER_CTA", 128 << 10);
   return (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)std::max(cap, 1), (slice_bytes + per - 1) / per));
 }
-// elements per bulk copy of the bulk-copy path (FTAR_TMA_PIECE_BYTES; 0 =
-// one copy per peer per tile), a multiple of 8 elements (16-byte granules)
-// L2 prefetch of the local tile by the bulk-copy producer (FTAR_TMA_L2PF=0 disables)
-uint32_t tma_l2pf() { return env_int("FTAR_TMA_L2PF", 1) != 0 ? 1u : 0u; }
-uint32_t tma_piece(uint64_t esz) {
-  const int b = env_int("FTAR_TMA_PIECE_BYTES", 0);
-  return b <= 0 ? 0u : (uint32_t)std::max<uint64_t>(8, ((uint64_t)b / esz) & ~7ull);
-}
 int small_ctas(uint64_t bytes) { return (int)std::max<uint64_t>(1, std::min<uint64_t>(16, (bytes + (32u << 10) - 1) >> 15)); }
 
 // The data path and grid of one call (launch_real and ftar_inflight_bound
@@ -2665,10 +2672,9 @@ struct PathChoice {
   int kind;
   int ctas;
   uint32_t stages;  // bulk-copy pipeline stages (0: not the bulk path)
-  uint32_t piece;   // elements per bulk copy (0: one per peer per tile)
 };
 PathChoice choose_path(int n, const LaunchParams& p, uint64_t esz, bool small, bool sgd, bool push) {
-  PathChoice pc{kPathRegister, real_ctas(push), 0, 0};
+  PathChoice pc{kPathRegister, real_ctas(push), 0};
   // fewer CTAs for small slices (CTA arrival + fences dominate): ~64 KB of
   // my slice per CTA, at least 1, at most the tuned shape
   const uint64_t per = (uint64_t)env_int("FTAR_BYTES_PER_CTA", 64 << 10);
@@ -2683,7 +2689,6 @@ PathChoice choose_path(int n, const LaunchParams& p, uint64_t esz, bool small, b
     pc.kind = kPathBulk;
     pc.stages = tma_stages_for(n, (int)esz);
     pc.ctas = tma_ctas(p.slice * esz);
-    pc.piece = tma_piece(esz);
   }
   return pc;
 }
@@ -3413,7 +3418,7 @@ int ftar_inflight_bound(int n, uint64_t n_elems, int in_dtype, uint64_t chunk_by
   fill_geometry(p, n_elems, chunk_bytes, max_in_flight, n);
   p.nelems = n_elems;
   const bool small = n >= 2 && in_bytes > 0 && in_bytes <= small_bytes();
-  PathChoice pc{kPathNone, 0, 0, 0};
+  PathChoice pc{kPathNone, 0, 0};
   uint64_t bound = 0;
   if (n >= 2 && in_bytes > 0) {
     pc = choose_path(n, p, esz, small, false, push != 0);
@@ -3568,8 +3573,15 @@ static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, ui
     p.flags &= ~(kFlagPush | kFlagDirect);
   }
   p.tma_stages = pc.stages;
-  p.tma_piece = pc.piece;
-  p.tma_l2pf = tma_l2pf();
+  {
+    // Early PDL trigger (FTAR_PDL_EARLY: 0 off, 1 register-path calls, 2
+    // every call).  N=4 f32, queue depth 3 (tools/tune_tma.py --early,
+    // profiles/r02/tune/pdl_early_n4.jsonl): +8-15% from 2 to 16 MiB, but
+    // -2..-5% on the bulk-copy path (64 MiB and up), also when only CTA 0
+    // triggers early, so the bulk path keeps the end-of-call trigger.
+    const int early = env_int("FTAR_PDL_EARLY", 1);
+    p.early_trigger = (pdl_on() && (early >= 2 || (early == 1 && pc.kind != kPathBulk))) ? 1u : 0u;
+  }
   const dim3 grid(pc.ctas, 1);
   cudaError_t e = small ? (in_dtype == FTAR_DT_BF16 ? launch_small<BF16In>(c->n, p, grid, st, false, pdl_on())
                                                     : launch_small<F32In>(c->n, p, grid, st, false, pdl_on()))
@@ -3765,8 +3777,6 @@ static int launch_local(ftar_ctx** ctxs, int n, const void* const* ins, int in_d
   }
   if (!sgd_p && n >= 2 && tma_on() && p.p_base / (uint64_t)n >= tma_tile(n, in_dtype == FTAR_DT_BF16 ? 2 : 4)) {
     p.tma_stages = tma_stages_for(n, in_dtype == FTAR_DT_BF16 ? 2 : 4);
-    p.tma_piece = tma_piece(in_dtype == FTAR_DT_BF16 ? 2 : 4);
-    p.tma_l2pf = tma_l2pf();
     if (g_local_ctas <= 0) G = std::min(G, tma_ctas(p.slice * (in_dtype == FTAR_DT_BF16 ? 2 : 4)));
   }
   const dim3 grid(G, n);

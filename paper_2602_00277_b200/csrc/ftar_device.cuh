@@ -76,6 +76,7 @@ __host__ __device__ inline uint64_t entry_sum(uint64_t tag, uint64_t fp, uint64_
 
 struct alignas(128) ArenaHdr {
   EntryIn ent_in[kMaxMembers];      // member j's entry record for my current call
+  uint64_t ent_ack[kMaxMembers];    // member j has read my entry record of call <tag> (PDL gate)
   alignas(128) uint64_t rs_done;    // flag: my slice is reduced (+kBitNonFinite)
   alignas(128) uint64_t poison;     // flag: I aborted this call (bits = reason)
   alignas(128) uint32_t rs_arrive;  // CTA arrival counters (local atomics)
@@ -253,10 +254,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-// global -> L2 prefetch (no completion to wait for)
-__device__ __forceinline__ void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gsrc), "r"(bytes) : "memory");
 }
 // shared -> global (local or peer), tracked by bulk groups
 __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {

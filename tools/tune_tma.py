@@ -27,10 +27,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--ag", default="push", help="comma list of all-gather modes: push (into registered outs), "
                                                   "pull (FTAR_NO_PUSH=1: members pull the reduced slices)")
-    ap.add_argument("--pieces", default="0", help="comma list of FTAR_TMA_PIECE_BYTES for the tma cells "
-                                                   "(bytes per bulk copy; 0 = one copy per peer per tile)")
-    ap.add_argument("--l2pf", default="1", help="comma list of FTAR_TMA_L2PF for the tma cells "
-                                                 "(1: the producer prefetches my own tile into L2)")
+    ap.add_argument("--auto", action="store_true", help="add a cell with the library's default policy")
+    ap.add_argument("--early", default="1", help="comma list of FTAR_PDL_EARLY (every cell)")
+    ap.add_argument("--repeat", type=int, default=1, help="run every cell this many times (interleaved)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -87,22 +86,21 @@ def main():
             buf.copy_(torch.randn(elems, device=dev).to(tdt))
             out = group.alloc_bucket(elems, torch.float32)
             steps = max(5, min(args.steps * 8, int(args.steps * 256 / max(mib, 1))))
-            cells = [("tma", c, pc, pf) for pf in args.l2pf.split(",") for pc in args.pieces.split(",")
-                     for c in args.tma_ctas.split(",") if c] + \
-                    [("ldg", c, "0", "0") for c in args.ldg_ctas.split(",") if c]
+            cells = [("tma", c) for c in args.tma_ctas.split(",") if c] + \
+                    [("ldg", c) for c in args.ldg_ctas.split(",") if c] + ([("auto", "0")] if args.auto else [])
+            cells = [(*cell, e) for _ in range(args.repeat) for cell in cells for e in args.early.split(",")]
             for ag in args.ag.split(","):
                 os.environ["FTAR_NO_PUSH"] = "1" if ag == "pull" else "0"
-                for path, c, piece, pf in cells:
-                    os.environ["FTAR_TMA"] = "1" if path == "tma" else "0"
-                    os.environ["FTAR_TMA_PIECE_BYTES"] = piece
-                    os.environ["FTAR_TMA_L2PF"] = pf
+                for path, c, early in cells:
+                    os.environ["FTAR_PDL_EARLY"] = early
+                    os.environ["FTAR_TMA"] = "0" if path == "ldg" else "1"
                     _lib.lib.ftar_set_tuning(int(c), 0)
                     t = timed(buf, out, steps)
                     if rank == 0:
                         busbw = elems * ib / t * 2 * (n - 1) / n / 1e9
                         ingress = (n - 1) / n * elems * (ib + 4) / t / 1e9
                         print(json.dumps({"n": n, "dtype": dt, "MiB": mib, "path": path, "ag": ag, "ctas": int(c),
-                                          "piece": int(piece), "l2pf": int(pf),
+                                          "early": int(early),
                                           "us": round(t * 1e6, 2), "busbw": round(busbw, 1),
                                           "nvlink_ingress_GBps": round(ingress, 1)}), flush=True)
             os.environ["FTAR_NO_PUSH"] = "0"
