@@ -95,6 +95,7 @@ struct LaunchParams {
   int rs_ctas;                   // CTAs that reduce (the rest only all-gather); <= gridDim.x
   uint32_t tma_stages;           // > 0: bulk-copy (TMA) data path with this many smem stages
   uint32_t early_trigger;        // 1: PDL trigger once the peers have read my entry record
+  uint32_t entry_fence;          // 1: system fence between the entry record and its flag
   uint64_t my_in_va;             // real mode: my input as this process addresses it
   uint64_t region_va[kMaxMembers][kMaxRegions];  // member i's registered region r, mapped here (0 = none)
   uint32_t intra_op;             // intra-replica collective (kIntraRS / kIntraAG), 0 = FTAR
@@ -128,6 +129,24 @@ __device__ __forceinline__ uint64_t call_fingerprint(const LaunchParams& p, int 
 // real (one GPU per member) launch, the live mask and contributor mask must
 // be the ones the launch was built from — a queued op never runs against a
 // membership the control plane has since replaced.
+struct CtlWords {
+  uint64_t epoch, masks;
+};
+// the 16-byte PCIe read, issued on its own so that its latency overlaps
+// whatever the caller issues next (the result is consumed by ctl_check)
+__device__ __forceinline__ CtlWords ctl_load(const HostCtl* ctl) {
+  CtlWords w;
+  asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];" : "=l"(w.epoch), "=l"(w.masks) : "l"(ctl) : "memory");
+  return w;
+}
+__device__ __forceinline__ bool ctl_check(const CtlWords& w, uint64_t tag, int n, uint32_t contrib, bool real,
+                                          bool check_contrib) {
+  if (w.epoch != tag_gen(tag)) return true;
+  if (!real) return false;
+  const uint32_t all = (n >= 32) ? 0xffffffffu : ((1u << n) - 1u);
+  if ((uint32_t)w.masks != all) return true;
+  return check_contrib && (uint32_t)(w.masks >> 32) != contrib;
+}
 __device__ __forceinline__ bool ctl_mismatch(const HostCtl* ctl, uint64_t tag, int n, uint32_t contrib, bool real,
                                              bool check_contrib) {
   uint64_t e, m;
@@ -146,7 +165,7 @@ __device__ __forceinline__ bool ctl_mismatch(const HostCtl* ctl, uint64_t tag, i
 // it must not write anything there.  Returns the mask of such peers.
 __device__ __forceinline__ uint32_t newer_peers(const LaunchParams& p, int n, int me, uint64_t tag) {
   bool newer = false;
-  const int j = threadIdx.x;
+  const int j = threadIdx.x & 31;
   if (j < n && j != me)
     newer = ld_relaxed_sys(&reinterpret_cast<const ArenaHdr*>(p.base[j])->gen_word) > tag_gen(tag);
   return __ballot_sync(0xffffffffu, newer);
@@ -1000,12 +1019,13 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
       fence_mbar_init();
     }
   }
-  if (tid < 32 && !p.emulated && (p.flags & kFlagPush)) {
-    // push mode writes into peers' outputs: never from an abandoned generation
-    const uint32_t m = newer_peers(p, N, me, tag);
-    if (tid == 0) s_newer = m;
-  } else if (tid == 0) {
-    s_newer = 0;
+  // push mode writes into peers' outputs: never from an abandoned generation.
+  // (Warp 1 in CTA 0, whose warp 0 runs the entry concurrently: the remote
+  // reads cost an NVLink round trip.)  s_newer is read after __syncthreads.
+  const int zw = blockIdx.x == 0 ? 1 : 0;
+  if ((tid >> 5) == zw) {
+    const uint32_t m = (!p.emulated && (p.flags & kFlagPush)) ? newer_peers(p, N, me, tag) : 0u;
+    if ((tid & 31) == 0) s_newer = m;
   }
   if (blockIdx.x == 0 && tid < 32) {
     // ---- 1a. entry (may overlap the previous call's tail: PDL) ------------
@@ -1015,9 +1035,16 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
     // previous kernel on this stream may still be resetting.
     __syncwarp();
     if (tid == 0) {
+      // Epoch fence: an op queued under an older decision must not run
+      // against the membership the control plane has since installed.  The
+      // PCIe read is issued first and checked after the entry pushes, so its
+      // ~1.5 us overlaps them and the flags' flight.  (A stale op that
+      // already published is harmless: its tag matches no current peer call,
+      // and it poisons itself below.)
+      const CtlWords cw = ctl_load(ctl);
       if (N > 1) {
         // push my entry record into slot `me` of every peer's header: posted
-        // writes, ONE sys fence, then the flags (the peers poll locally)
+        // writes, then the flags (the peers poll locally)
         const uint64_t fp = call_fingerprint(p, N);
         const uint64_t oo = (p.flags & kFlagPush) ? p.out_off[me] : ~0ull;
         const uint64_t sum = entry_sum(tag, fp, p.in_off[me], p.res_off[me], oo);
@@ -1029,16 +1056,15 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
           st_relaxed_sys(&e->out_off, oo);
           st_relaxed_sys(&e->sum, sum);
         }
-        fence_acq_rel_sys();
+        // No fence between the record and its flag: the reader re-reads the
+        // record until its checksum (over this call's tag) holds, which
+        // costs nothing once the writes land, where a system fence waits a
+        // full NVLink round trip for their acks (FTAR_ENTRY_FENCE=1 restores it)
+        if (p.entry_fence) fence_acq_rel_sys();
         for (int jj = 1; jj < N; ++jj)
           st_relaxed_sys(&reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->ent_in[me].flag, mk_flag(tag, 0));
       }
-      // Epoch fence: an op queued under an older decision must not run
-      // against the membership the control plane has since installed.  (A
-      // PCIe read, so it runs while the entry flags travel; a stale op that
-      // already published is harmless: its tag matches no current peer call,
-      // and it poisons itself below.)
-      if (ctl_mismatch(ctl, tag, N, p.contrib, !p.emulated, true)) {
+      if (ctl_check(cw, tag, N, p.contrib, !p.emulated, true)) {
         s_status = ST_PROTOCOL;
         s_blame = me;
       }
@@ -1061,12 +1087,24 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         // own_err = null: hdr->err still belongs to the previous call here
         st = wait_flag(&e->flag, tag, &ph->poison, ctl, nullptr, s_t0, p.hard_timeout_ns, nullptr);
         if (st == ST_OK) {
-          const uint64_t fp = ld_relaxed_sys(&e->fp), in_off = ld_relaxed_sys(&e->in_off);
-          const uint64_t res_off = ld_relaxed_sys(&e->res_off);
-          oo = ld_relaxed_sys(&e->out_off);
-          const uint64_t sum = ld_relaxed_sys(&e->sum);
-          if (fp != want_fp) st = ST_PROTOCOL;  // a different call
-          else if (sum != entry_sum(tag, fp, in_off, res_off, oo)) st = ST_PEER_RESET;
+          // the flag can overtake the record (no writer fence): re-read until
+          // the record is this call's (its checksum covers the tag); a writer
+          // that died mid-record leaves it torn -> PEER_RESET after 200 us
+          uint64_t fp, in_off, res_off, sum;
+          const uint64_t tr = globaltimer_ns();
+          for (uint32_t it = 0;; ++it) {
+            fp = ld_relaxed_sys(&e->fp);
+            in_off = ld_relaxed_sys(&e->in_off);
+            res_off = ld_relaxed_sys(&e->res_off);
+            oo = ld_relaxed_sys(&e->out_off);
+            sum = ld_relaxed_sys(&e->sum);
+            if (sum == entry_sum(tag, fp, in_off, res_off, oo)) break;
+            if ((it & 15u) == 15u && globaltimer_ns() - tr > 200000ull) {
+              st = ST_PEER_RESET;
+              break;
+            }
+          }
+          if (st == ST_OK && fp != want_fp) st = ST_PROTOCOL;  // a different call
           // arena offsets, or references to member j's registered buffers
           // (mapped here by RingGroup.register); an unmapped region is a
           // protocol error, never a guess
@@ -3582,6 +3620,7 @@ static int launch_real(ftar_ctx* c, const void* in, int in_dtype, float* out, ui
     const int early = env_int("FTAR_PDL_EARLY", 1);
     p.early_trigger = (pdl_on() && (early >= 2 || (early == 1 && pc.kind != kPathBulk))) ? 1u : 0u;
   }
+  p.entry_fence = env_int("FTAR_ENTRY_FENCE", 0) != 0 ? 1u : 0u;
   const dim3 grid(pc.ctas, 1);
   cudaError_t e = small ? (in_dtype == FTAR_DT_BF16 ? launch_small<BF16In>(c->n, p, grid, st, false, pdl_on())
                                                     : launch_small<F32In>(c->n, p, grid, st, false, pdl_on()))

@@ -28,7 +28,8 @@ def main():
     ap.add_argument("--ag", default="push", help="comma list of all-gather modes: push (into registered outs), "
                                                   "pull (FTAR_NO_PUSH=1: members pull the reduced slices)")
     ap.add_argument("--auto", action="store_true", help="add a cell with the library's default policy")
-    ap.add_argument("--early", default="1", help="comma list of FTAR_PDL_EARLY (every cell)")
+    ap.add_argument("--env", action="append", default=[], metavar="NAME=v1,v2",
+                    help="sweep an environment knob over every cell (repeatable; e.g. FTAR_PDL_EARLY=0,1)")
     ap.add_argument("--repeat", type=int, default=1, help="run every cell this many times (interleaved)")
     args = ap.parse_args()
     import torch
@@ -88,11 +89,15 @@ def main():
             steps = max(5, min(args.steps * 8, int(args.steps * 256 / max(mib, 1))))
             cells = [("tma", c) for c in args.tma_ctas.split(",") if c] + \
                     [("ldg", c) for c in args.ldg_ctas.split(",") if c] + ([("auto", "0")] if args.auto else [])
-            cells = [(*cell, e) for _ in range(args.repeat) for cell in cells for e in args.early.split(",")]
+            combos = [{}]
+            for spec in args.env:
+                name, vals = spec.split("=", 1)
+                combos = [{**c, name: v} for c in combos for v in vals.split(",")]
+            cells = [(*cell, e) for _ in range(args.repeat) for cell in cells for e in combos]
             for ag in args.ag.split(","):
                 os.environ["FTAR_NO_PUSH"] = "1" if ag == "pull" else "0"
-                for path, c, early in cells:
-                    os.environ["FTAR_PDL_EARLY"] = early
+                for path, c, env in cells:
+                    os.environ.update(env)
                     os.environ["FTAR_TMA"] = "0" if path == "ldg" else "1"
                     _lib.lib.ftar_set_tuning(int(c), 0)
                     t = timed(buf, out, steps)
@@ -100,7 +105,7 @@ def main():
                         busbw = elems * ib / t * 2 * (n - 1) / n / 1e9
                         ingress = (n - 1) / n * elems * (ib + 4) / t / 1e9
                         print(json.dumps({"n": n, "dtype": dt, "MiB": mib, "path": path, "ag": ag, "ctas": int(c),
-                                          "early": int(early),
+                                          "env": env,
                                           "us": round(t * 1e6, 2), "busbw": round(busbw, 1),
                                           "nvlink_ingress_GBps": round(ingress, 1)}), flush=True)
             os.environ["FTAR_NO_PUSH"] = "0"
