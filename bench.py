@@ -218,6 +218,22 @@ def digest(t) -> str:
     return hashlib.sha256(t.detach().float().cpu().numpy().tobytes()).hexdigest()
 
 
+def device_digest(t) -> tuple:
+    """Position-weighted 64-bit sums of a large fp32 tensor's bit patterns,
+    computed on the device in 64 Mi-element chunks (a host sha256 of GiBs
+    would take seconds)."""
+    import torch
+    x = t.detach().reshape(-1).view(torch.int32)
+    s1 = s2 = 0
+    step = 64 << 20
+    w = (torch.arange(step, device=t.device, dtype=torch.int64) % 65521) + 1
+    for i in range(0, x.numel(), step):
+        c = x[i:i + step].to(torch.int64)
+        s1 += int(c.sum())
+        s2 += int((c * w[:c.numel()]).sum())
+    return (s1, s2)
+
+
 # --------------------------------------------------------------------------- GPU
 
 METRIC = "FTAR bus GB/s vs bucket size at 2/4/8 B200 (% NVLink peak); catch-up ms/GB"
@@ -687,6 +703,10 @@ def run_multi(args, rank, world, local_rank):
     if not args.no_nccl:
         nccl = nccl_busbw(args, n, elems, tdtype, dev, stream)
     group.close()
+    del buf, out
+    catchup = None
+    if args.catchup_gib > 0:
+        catchup = catchup_ms_per_gb(args, rank, n, dev, fabric)
     if rank == 0:
         parity = {"checked": "every rank's output of one call (before the timed region) vs the oracle digest"
                              + ("" if args.inplace else "; outputs after the timed steps identical"),
@@ -702,8 +722,68 @@ def run_multi(args, rank, world, local_rank):
                 "algbw_gbs": round(elems * in_bytes / t_step / 1e9, 3),
                 "pct_nvlink_nominal": round(100 * value / NVLINK_NOMINAL_GBS, 2),
                 "phases_us_rank0": phases,
-                "nccl_allreduce": nccl}
+                "nccl_allreduce": nccl, "catchup": catchup}
         print(json.dumps(line), flush=True)
+
+
+def catchup_ms_per_gb(args, rank, n, dev, fabric):
+    """The metric's second half: catch-up ms/GB.  Ranks 0..n-2 hold the same
+    retention-1 snapshot (params + momentum, fp32, --catchup-gib in total);
+    rank n-1 pulls it striped over all of them with the catch-up kernel on
+    its side stream (checkpoint.start_fetch), alone on the GPUs (config 4's
+    'pull alone' number; tools/bench_catchup.py measures it inside a running
+    ring).  CUDA events on the pulling stream around each pull, best of 3,
+    bytes checked against the donors' digest."""
+    import torch
+    import torch.distributed as dist
+    from paper_2602_00277_b200 import checkpoint as ck
+    rec, donors = n - 1, list(range(n - 1))
+    half = int(args.catchup_gib * (1 << 30) / 2) // 4
+    nbytes = 2 * half * 4
+    snap = ck.SnapshotStore(capacity_bytes=nbytes, device=dev, fabric=fabric, rank=0, replica_id=rank)
+    want = None
+    if rank != rec:
+        g = torch.Generator(device=dev).manual_seed(7)
+        p = torch.randn(half, device=dev, generator=g)
+        m = torch.randn(half, device=dev, generator=g)
+        snap.capture(3, p, m)
+        torch.cuda.synchronize()
+        want = (device_digest(p), device_digest(m))
+        del p, m
+    dist.barrier()
+    res = None
+    if rank == rec:
+        p_out = torch.empty(half, device=dev)
+        m_out = torch.empty(half, device=dev)
+        side = ck.catchup_stream(dev)
+        times = []
+        for i in range(4):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(side)
+            h = ck.start_fetch(snap, donors, 3, 0, p_out, m_out, timeout_s=60, ctas=args.catchup_ctas,
+                               refresh=(i == 0))
+            h.wait()
+            e.record(side)
+            torch.cuda.synchronize()
+            if i:
+                times.append(s.elapsed_time(e))
+        got = (device_digest(p_out), device_digest(m_out))
+        ms = min(times)
+        res = {"gib": args.catchup_gib, "bytes": nbytes, "ms": round(ms, 3),
+               "ms_per_gb": round(ms / (nbytes / 1e9), 3), "gbs": round(nbytes / ms / 1e6, 1),
+               "ctas": args.catchup_ctas, "donors": donors, "recovering_rank": rec, "got": got,
+               "how": "rank n-1 pulls params+momentum striped over ranks 0..n-2 (checkpoint.start_fetch), "
+                      "alone on the GPUs; CUDA events on the pulling stream, best of 3"}
+        del p_out, m_out
+    box = [None] * n
+    dist.all_gather_object(box, res if rank == rec else want)
+    dist.barrier()
+    snap.close()
+    if rank == 0:
+        res = box[rec]
+        res["bit_exact"] = res.pop("got") == box[0]
+        return res
+    return None
 
 
 def phase_us(group):
@@ -783,6 +863,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-check", action="store_true", help="skip the oracle self-check")
+    ap.add_argument("--catchup-gib", type=float, default=8.0,
+                    help="N>=2: also time the catch-up pull of this many GiB of params+momentum (0: skip)")
+    ap.add_argument("--catchup-ctas", type=int, default=32, help="CTAs of the catch-up pull in that measurement")
     ap.add_argument("--no-pm", action="store_true", help="no CUPTI PM sampling (N=1: DRAM bytes, N>=2: NVLink bytes)")
     ap.add_argument("--no-protocol", action="store_true", help="N=1: skip the protocol-kernel record")
     ap.add_argument("--unregistered", action="store_true",
