@@ -508,12 +508,18 @@ def manifest_path(ckpt_dir: str, step: int) -> str:
 
 
 def _atomic_write(path: str, data: bytes) -> None:
-    tmp = path + ".tmp"
-    with open(tmp, "wb") as fh:
-        fh.write(data)
-        fh.flush()
-        os.fsync(fh.fileno())
-    os.rename(tmp, path)
+    """Durable replace: the bytes reach the disk under a side name first, so a
+    reader never sees a partial file under `path`."""
+    side = f"{path}.tmp"
+    fd = os.open(side, os.O_WRONLY | os.O_CREAT | os.O_TRUNC, 0o644)
+    try:
+        view = memoryview(data)
+        while view:
+            view = view[os.write(fd, view):]
+        os.fsync(fd)
+    finally:
+        os.close(fd)
+    os.replace(side, path)
 
 
 def _as_bytes(x) -> bytes:
@@ -587,14 +593,34 @@ def write_manifest(ckpt_dir: str, step: int, n_ranks: int, dims: tuple[int, ...]
     return path
 
 
-_MANIFEST_RE = re.compile(r"^state_(\d{8})\.json$")
+_MANIFEST_RE = re.compile(r"state_(\d{8})\.json")
+
+
+def _manifest_ok(ckpt_dir: str, step: int):
+    try:
+        with open(manifest_path(ckpt_dir, step), "rb") as fh:
+            doc = json.load(fh)
+    except (OSError, json.JSONDecodeError):
+        return None
+    if doc.get("magic") != MAGIC.decode() or doc.get("step") != step:
+        return None
+    shards_present = all(os.path.exists(shard_path(ckpt_dir, step, r)) for r in range(doc.get("n_ranks", 0)))
+    return doc if shards_present else None
 
 
 def find_latest(ckpt_dir: str):
     """checkpoint.py:219-230: newest step whose manifest parses and whose shard
     files all exist, as (step, manifest)."""
-    if not os.path.isdir(ckpt_dir):
+    try:
+        names = os.listdir(ckpt_dir)
+    except (FileNotFoundError, NotADirectoryError):
         return None
+    candidates = {int(m.group(1)) for m in map(_MANIFEST_RE.fullmatch, names) if m}
+    for step in sorted(candidates, reverse=True):
+        doc = _manifest_ok(ckpt_dir, step)
+        if doc is not None:
+            return step, doc
+    return None
     steps = sorted((int(m.group(1)) for name in os.listdir(ckpt_dir) if (m := _MANIFEST_RE.match(name))),
                    reverse=True)
     for step in steps:
