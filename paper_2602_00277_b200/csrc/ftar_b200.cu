@@ -1516,29 +1516,31 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
   __shared__ int s_blame;
   __shared__ uint64_t s_t0;
   __shared__ uint64_t s_t1;
-  if (tid < 32) {
-    // zombie guard (remote reads, overlapping the previous kernel's tail):
-    // a member dropped from the ring must not push into the regrouped one
+  __shared__ uint32_t s_newer, s_ctlbad;
+  if (tid >= 32 && tid < 64) {
+    // zombie guard on warp 1 (remote reads, overlapping the previous
+    // kernel's tail and warp 0's PCIe read): a member dropped from the ring
+    // must not push into the regrouped one
     const uint32_t newer = p.emulated ? 0u : newer_peers(p, N, me, tag);
-    if (tid == 0) {
-      s_status = newer ? ST_PEER_RESET : ST_OK;
-      s_blame = newer ? __ffs(newer) - 1 : -1;
-    }
+    if (tid == 32) s_newer = newer;
   }
   if (tid == 0) {
     s_nf = 0;
     s_t0 = globaltimer_ns();
     s_t1 = 0;
+    s_ctlbad = 0;
     if (blockIdx.x == 0) {
       // Epoch fence (a PCIe read, overlapping the previous kernel's tail):
       // a stale op's pushes carry a tag no current peer call waits for, and
       // it poisons itself.
-      if (ctl_mismatch(ctl, tag, N, p.contrib, !p.emulated, true)) {
-        s_status = ST_PROTOCOL;
-        s_blame = me;
-      }
+      if (ctl_mismatch(ctl, tag, N, p.contrib, !p.emulated, true)) s_ctlbad = 1;
       ctl->started = tag;
     }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    s_status = s_newer ? ST_PEER_RESET : (s_ctlbad ? ST_PROTOCOL : ST_OK);
+    s_blame = s_newer ? __ffs(s_newer) - 1 : (s_ctlbad ? me : -1);
   }
   // The input may be the output of the previous kernel on this stream (an
   // in-place chain, or an intra-replica reduce-scatter feeding this call):
@@ -1609,16 +1611,17 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
     fold_tiles<N, In>(g, s_src, SinkOne{res}, 0, E, vec_ok, (p.flags & FTAR_F_SCALE) != 0, nf, ctl, 0x7fffffff);
   }
   __syncthreads();
-  if (tid == 0 && s_status == ST_OK) {
+  if (tid < 32 && s_status == ST_OK) {
     // every copy I folded must still be the one its sender flagged for this
-    // call: a zombie's late push is followed by its (older) flag
-    for (int jj = 1; jj < N; ++jj) {
-      const int j = (me + jj) % N;
-      if (flag_tag(ld_acquire_sys(&hdr->sm_in[j])) != tag || ld_relaxed_sys(&hdr->sm_meta[j]) != fp) {
-        s_status = ST_PEER_RESET;
-        s_blame = j;
-        break;
-      }
+    // call: a zombie's late push is followed by its (older) flag (lane j
+    // re-reads member j's flag and fingerprint; all peers at once)
+    const int j = tid;
+    const bool stale = j < N && j != me &&
+                       (flag_tag(ld_relaxed_sys(&hdr->sm_in[j])) != tag || ld_relaxed_sys(&hdr->sm_meta[j]) != fp);
+    const uint32_t bad = __ballot_sync(0xffffffffu, stale);
+    if (tid == 0 && bad) {
+      s_status = ST_PEER_RESET;
+      s_blame = __ffs(bad) - 1;
     }
   }
   if (__any_sync(0xffffffffu, nf != 0) && (tid & 31) == 0) atomicOr(&s_nf, 1u);

@@ -15,6 +15,7 @@ import ctypes as C
 import json
 import os
 import sys
+import time
 
 import torch
 import torch.distributed as dist
@@ -63,6 +64,7 @@ def main():
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(st)
         pend = []
+        h0 = time.perf_counter()
         for _ in range(args.iters):
             pend.append(ftar.ftar_all_reduce_async(g, b, 0, cfg, out=o))
             if len(pend) >= 3:
@@ -70,6 +72,7 @@ def main():
         while pend:
             pend.pop(0).wait()
         ev1.record(st)
+        host_call = (time.perf_counter() - h0) * 1e6 / args.iters  # host time per call incl. its wait
         torch.cuda.synchronize()
         per_call = ev0.elapsed_time(ev1) * 1e3 / args.iters
         t = (C.c_uint64 * 6)()
@@ -103,11 +106,13 @@ def main():
         _lib.lib.ftar_geometry(e, n, C.byref(slice_e), C.byref(ctas), C.byref(thr))
         rows = [None] * n
         dist.all_gather_object(rows, {"rank": rank, "phases_us": ph, "per_call_us": round(per_call, 2),
+                                      "host_per_call_us": round(host_call, 2),
                                       "queued_phases_us": q_ph, "queued_t0": q_t0, "detail": det,
                                       "queued_host_ns": q_host})
         if rank == 0:
             busbw = nb / (per_call * 1e-6) * 2 * (n - 1) / n / 1e9
             print(json.dumps({"n": n, "dtype": args.dtype, "bytes": nb, "per_call_us": round(per_call, 2),
+                              "host_per_call_us": [r["host_per_call_us"] for r in rows],
                               "busbw": round(busbw, 1), "slice_elems": slice_e.value,
                               "phases_entry_rs_wait_tail_us": [r["phases_us"] for r in rows],
                               "queued_phases_us": [r["queued_phases_us"] for r in rows],
