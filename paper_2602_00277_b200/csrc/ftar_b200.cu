@@ -1138,13 +1138,22 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
       }
       s_pushok = ((p.flags & kFlagPush) && !nopush) ? 1u : 0u;
     }
-    // Early PDL trigger.  The next call on this stream may run its entry
-    // (which writes only the entry slots and its own control slot) as soon
-    // as every peer has consumed my record of this call -- it then overlaps
-    // this call's whole reduce-scatter instead of only its completion tail.
+    // Early PDL trigger (push mode only).  The next call on this stream may
+    // run its entry (which writes only the entry slots and its own control
+    // slot) as soon as every peer has consumed my record of this call -- it
+    // then overlaps this call's whole reduce-scatter instead of only its
+    // completion tail.  Its record lets a peer that has finished this call
+    // start the next one's reduce-scatter while I am still in this one:
+    //  - push mode: that peer writes only my out of the next call (stream
+    //    order makes that the next call's buffer) and the ag_in slot of the
+    //    next call's parity;
+    //  - pull mode would let it overwrite its result region while I still
+    //    pull this call's slice from it, so pull-mode calls (including the
+    //    fused optimizer) keep the end-of-call trigger.
     // A peer that does not ack within 100 us just leaves the trigger to the
     // end of the call.
-    if (N > 1 && !p.emulated && !bad && p.early_trigger) {
+    __syncwarp();
+    if (N > 1 && !p.emulated && !bad && p.early_trigger && s_pushok) {
       bool acked = true;
       if (j < N && j != me) {
         acked = false;
@@ -1307,7 +1316,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
           for (int j = 0; j < N; ++j) {
             if (j == me) continue;
             ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
-            st_relaxed_sys(&ph->ag_in[me], mk_flag(tag, bits));
+            st_relaxed_sys(&ph->ag_in[tag & 1][me], mk_flag(tag, bits));
           }
         }
         hdr->tph[2] = globaltimer_ns();
@@ -1330,7 +1339,7 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         const int j = (me + jj) % N;
         ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
         uint32_t b = 0;
-        const uint32_t st = wait_flag(&hdr->ag_in[j], tag, &ph->poison, ctl, &hdr->err, s_t0,
+        const uint32_t st = wait_flag(&hdr->ag_in[tag & 1][j], tag, &ph->poison, ctl, &hdr->err, s_t0,
                                       p.hard_timeout_ns, &b);
         if (st != ST_OK) {
           s_status = st;
@@ -1845,7 +1854,7 @@ __global__ void __launch_bounds__(kThreads, 1) intra_kernel(const __grid_constan
         // every CTA's loads have returned (their values are stored): tell the
         // peers they may let their callers reuse the buffers I read
         for (int jj = 1; jj < N; ++jj)
-          st_relaxed_sys(&reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->ag_in[me], mk_flag(tag, 0));
+          st_relaxed_sys(&reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->ag_in[tag & 1][me], mk_flag(tag, 0));
       }
       hdr->tph[2] = globaltimer_ns();
     }
@@ -1853,7 +1862,7 @@ __global__ void __launch_bounds__(kThreads, 1) intra_kernel(const __grid_constan
   if (blockIdx.x == 0 && tid == 0 && s_status == ST_OK) {
     for (int jj = 1; jj < N; ++jj) {
       const int j = (me + jj) % N;
-      const uint32_t st = wait_flag(&hdr->ag_in[j], tag, &reinterpret_cast<ArenaHdr*>(p.base[j])->poison, ctl,
+      const uint32_t st = wait_flag(&hdr->ag_in[tag & 1][j], tag, &reinterpret_cast<ArenaHdr*>(p.base[j])->poison, ctl,
                                     &hdr->err, s_t0, p.hard_timeout_ns, nullptr);
       if (st != ST_OK) {
         s_status = st;
@@ -2715,7 +2724,11 @@ struct PathChoice {
   uint32_t stages;  // bulk-copy pipeline stages (0: not the bulk path)
 };
 PathChoice choose_path(int n, const LaunchParams& p, uint64_t esz, bool small, bool sgd, bool push) {
-  PathChoice pc{kPathRegister, real_ctas(push), 0};
+  // the fused optimizer's all-gather also streams params + momentum through
+  // HBM: 128 CTAs (tools/sgd_bench.py, N=4, 128 Mi bf16 elements per bucket:
+  // 1.19 ms at 64 CTAs, 1.04 at 128, 1.11 at 148; the plain all-reduce 0.89)
+  const int sgd_ctas = g_ctas > 0 ? g_ctas : env_int("FTAR_CTAS_SGD", 128);
+  PathChoice pc{kPathRegister, sgd ? sgd_ctas : real_ctas(push), 0};
   // fewer CTAs for small slices (CTA arrival + fences dominate): ~64 KB of
   // my slice per CTA, at least 1, at most the tuned shape
   const uint64_t per = (uint64_t)env_int("FTAR_BYTES_PER_CTA", 64 << 10);

@@ -100,7 +100,11 @@ struct alignas(128) ArenaHdr {
   alignas(128) uint64_t go2;              // direct mode: (tag << 8) | mask of members whose slice is reduced
   uint64_t peer_out[kMaxMembers];         // push mode: members' `out` element 0 (my VA)
   uint32_t push_ok;                       // push mode agreed for this call
-  alignas(128) uint64_t ag_in[kMaxMembers];  // push mode: member k finished writing its slice into my out
+  // push mode: member k finished writing its slice of call <tag> into my out,
+  // one slot per call parity (with the early PDL trigger a peer can finish
+  // call t and start call t+1's reduce-scatter before I have read its flag
+  // of call t; call t+2 cannot start before my call t is done)
+  alignas(128) uint64_t ag_in[2][kMaxMembers];
   alignas(128) uint64_t sm_in[kMaxMembers];  // small one-shot: member k's whole input is in my recv slot
   uint64_t sm_meta[kMaxMembers];             // its call fingerprint (validated like an entry record)
   alignas(128) uint32_t sm_arrive[2];        // small one-shot: push-arrival counter per call parity

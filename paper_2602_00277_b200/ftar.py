@@ -649,6 +649,19 @@ def ftar_all_reduce_sgd(group: RingGroup, grad: torch.Tensor, step: int, cfg: Pi
     never modified (the reference applies the optimizer only after its commit
     vote, replica.py:616-633); returns (params_out, momentum_out).  grad_out
     (optional, must not alias grad) receives g."""
+    return ftar_all_reduce_sgd_async(group, grad, step, cfg, params=params, momentum=momentum, lr=lr, beta=beta,
+                                     scale=scale, params_out=params_out, momentum_out=momentum_out,
+                                     grad_out=grad_out).wait()
+
+
+def ftar_all_reduce_sgd_async(group: RingGroup, grad: torch.Tensor, step: int, cfg: PipelineConfig | None = None,
+                              *, params: torch.Tensor, momentum: torch.Tensor, lr: float, beta: float,
+                              scale: float | None = None, params_out: torch.Tensor | None = None,
+                              momentum_out: torch.Tensor | None = None,
+                              grad_out: torch.Tensor | None = None) -> PendingAllReduce:
+    """ftar_all_reduce_sgd, enqueued (the same queue as ftar_all_reduce_async:
+    up to 4 buckets per group in flight, collected in launch order); .wait()
+    returns (params_out, momentum_out)."""
     cfg = cfg or PipelineConfig()
     if group._local:
         raise Fatal(INTERNAL_INVARIANT, "in-process groups: use LocalRing.all_reduce_sgd")
@@ -668,24 +681,23 @@ def ftar_all_reduce_sgd(group: RingGroup, grad: torch.Tensor, step: int, cfg: Pi
     if group.n > 1 and not group.links_ready():
         raise Recoverable(PEER_RESET, "ring links not established")
     q = group._pending
-    while q:
+    while len(q) >= 4:
         q[0].wait()
     flags = _lib.F_SCALE if scale is not None else 0
     f_scale = _f32(scale) if scale is not None else 1.0
+    rc = _lib.lib.ftar_allreduce_sgd_launch(
+        group.ctx, grad.data_ptr(), code, grad_out.data_ptr() if grad_out is not None else None, grad.numel(),
+        cfg.chunk_bytes, cfg.max_in_flight, f_scale, flags, params.data_ptr(), momentum.data_ptr(),
+        params_out.data_ptr(), momentum_out.data_ptr(), _f32(lr), _f32(beta), _stream_ptr(group.device))
     try:
-        rc = _lib.lib.ftar_allreduce_sgd_launch(
-            group.ctx, grad.data_ptr(), code, grad_out.data_ptr() if grad_out is not None else None, grad.numel(),
-            cfg.chunk_bytes, cfg.max_in_flight, f_scale, flags, params.data_ptr(), momentum.data_ptr(),
-            params_out.data_ptr(), momentum_out.data_ptr(), _f32(lr), _f32(beta), _stream_ptr(group.device))
         _lib.check(rc, "ftar_allreduce_sgd_launch")
-        det = C.c_int(-1)
-        st = _lib.lib.ftar_wait(group.ctx, cfg.per_chunk_timeout_s, C.byref(det))
-        if st:
-            raise from_status(st, _lib.last_error() if st == 10 else "")
     except FtdpError:
         group.close_links()
         raise
-    return params_out, momentum_out
+    p = PendingAllReduce(group, (params_out, momentum_out), cfg)
+    p._keep = (grad, params, momentum, grad_out)
+    q.append(p)
+    return p
 
 
 def _host_all_reduce(group, buf, step, cfg, out, scale):

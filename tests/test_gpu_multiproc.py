@@ -155,6 +155,22 @@ def _worker(rank, world, port, scenario, outdir):
             pw, mw = orc.sgd_momentum(p0.copy(), m0.copy(), gw, 0.9, 0.01)
             good = np.array_equal(po.cpu().numpy(), pw) and np.array_equal(mo.cpu().numpy(), mw)
             (res["ok"] if good else res["errors"]).append("sgd")
+            # queued: three buckets (bucket k = the same data x (k+1)) in flight at once, each with its
+            # own optimizer state, collected in launch order
+            pend, wants = [], []
+            for k in range(3):
+                gk = (g.float() * (k + 1)).to(torch.bfloat16)
+                pend.append(ftar.ftar_all_reduce_sgd_async(group, gk, 2, params=pt, momentum=mt, lr=0.01,
+                                                           beta=0.9, scale=1.0 / world))
+                ak = [(torch.from_numpy(a).to(torch.bfloat16).float() * (k + 1)).to(torch.bfloat16).float().numpy()
+                      for a in arrays]
+                gwk = orc.normalize(orc.oracle_reduce(ak, 8 << 20, 4), world)
+                wants.append(orc.sgd_momentum(p0.copy(), m0.copy(), gwk, 0.9, 0.01))
+            good = True
+            for pk, (pwk, mwk) in zip(pend, wants):
+                pok, mok = pk.wait()
+                good &= np.array_equal(pok.cpu().numpy(), pwk) and np.array_equal(mok.cpu().numpy(), mwk)
+            (res["ok"] if good else res["errors"]).append("sgd_async")
         elif scenario == "death":
             # a member PROCESS dies with its kernel in flight and its arena
             # still mapped by the others: survivors get Recoverable (no CUDA
@@ -420,6 +436,50 @@ def _worker(rank, world, port, scenario, outdir):
             (res["ok"] if np.array_equal(uo.cpu().numpy(), want) else res["errors"]).append("bench_unregistered")
             ftar.ftar_all_reduce(group, u, 7, cfg, scale=1.0 / world)
             (res["ok"] if np.array_equal(u.cpu().numpy(), want) else res["errors"]).append("bench_unreg_inplace")
+        elif scenario == "queued":
+            # back-to-back queued calls with DIFFERENT data per call: the early
+            # PDL trigger lets a peer start call t+1 while this member is still
+            # in call t, so every queued result must still be call t's own --
+            # push mode with per-call outs and with one reused out (the last
+            # call's result wins), pull mode (no early trigger), and the early
+            # trigger forced everywhere, also on the bulk-copy path
+            # (FTAR_PDL_EARLY=2, FTAR_TMA_MIN_SLICE_MIB=0); 2 MiB and 24 MiB buckets
+            cfg = ftar.PipelineConfig(per_chunk_timeout_s=10)
+            for gen, e in ((10, 512 << 10), (11, 6 << 20)):
+                group.close()
+                group = ftar.RingGroup(rank, 0, fabric, device=dev, max_bucket_bytes=e * 4,
+                                       pool_bytes=12 * e * 4 + 4096)
+                group.reconfig({r: ftar.PeerAddress(r) for r in range(world)}, gen, deadline_s=60)
+                K = 6
+                hosts = [[np.random.default_rng((k, r, e)).standard_normal(e).astype(np.float32) for r in range(world)]
+                         for k in range(K)]
+                wants = [orc.oracle_reduce(h, cfg.chunk_bytes, cfg.max_in_flight) for h in hosts]
+                xs = [group.alloc_bucket(e) for _ in range(K)]
+                for x, h in zip(xs, hosts):
+                    x.copy_(torch.from_numpy(h[rank]))
+                outs = [group.alloc_bucket(e) for _ in range(K - 1)]
+                for mode, env in (("push", {}), ("pull", {"FTAR_NO_PUSH": "1"}), ("early2", {"FTAR_PDL_EARLY": "2", "FTAR_TMA_MIN_SLICE_MIB": "0"})):
+                    old_env = {k: os.environ.get(k) for k in env}
+                    os.environ.update(env)
+                    try:
+                        for _ in range(3):
+                            pend = [ftar.ftar_all_reduce_async(group, xs[k], k, cfg, out=outs[k]) for k in range(K - 1)]
+                            for p_ in pend:
+                                p_.wait()
+                            good = all(np.array_equal(outs[k].cpu().numpy(), wants[k]) for k in range(K - 1))
+                            (res["ok"] if good else res["errors"]).append(f"queued_{mode}_{e}")
+                            shared = outs[0]
+                            pend = [ftar.ftar_all_reduce_async(group, xs[k], k, cfg, out=shared) for k in range(K)]
+                            for p_ in pend:
+                                p_.wait()
+                            good = np.array_equal(shared.cpu().numpy(), wants[K - 1])
+                            (res["ok"] if good else res["errors"]).append(f"queued_shared_{mode}_{e}")
+                    finally:
+                        for k, v in old_env.items():
+                            if v is None:
+                                os.environ.pop(k, None)
+                            else:
+                                os.environ[k] = v
         elif scenario == "register":
             # ordinary torch tensors registered with the ring (RingGroup.register):
             # zero-copy in place and push into a registered out; a member that
@@ -661,11 +721,18 @@ def test_host_buffers_over_nvlink():
         assert "host_inplace" in r["ok"] and "host_bf16" in r["ok"]
 
 
+def test_queued_calls_keep_their_own_results():
+    res = run("queued", world_size())
+    for r in res:
+        assert not r["errors"], r["errors"]
+        assert any(x.startswith("queued_push") for x in r["ok"]) and any(x.startswith("queued_pull") for x in r["ok"])
+
+
 def test_fused_sgd_over_nvlink():
     res = run("sgd", world_size())
     for r in res:
         assert not r["errors"], r["errors"]
-        assert "sgd" in r["ok"]
+        assert "sgd" in r["ok"] and "sgd_async" in r["ok"]
 
 
 def test_member_process_death_is_recoverable():

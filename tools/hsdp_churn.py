@@ -169,10 +169,12 @@ def main():
             if fused:
                 # §8f: all-reduce + x f32(1/h) + SGD-momentum in one kernel per
                 # bucket, out of place (applied by the swap at commit)
-                for o, n in buckets:
-                    ftar.ftar_all_reduce_sgd(group, grads[o:o + n], target, cfg, params=params[o:o + n],
-                                             momentum=mom[o:o + n], lr=args.lr, beta=args.beta, scale=d.scale(),
-                                             params_out=nxt[0][o:o + n], momentum_out=nxt[1][o:o + n])
+                pend = [ftar.ftar_all_reduce_sgd_async(group, grads[o:o + n], target, cfg, params=params[o:o + n],
+                                                       momentum=mom[o:o + n], lr=args.lr, beta=args.beta,
+                                                       scale=d.scale(), params_out=nxt[0][o:o + n],
+                                                       momentum_out=nxt[1][o:o + n]) for o, n in buckets]
+                for p_ in pend:
+                    p_.wait()
                     bucket_ms.append(round((time.monotonic() - t_ar) * 1e3, 2))
             else:
                 pend = [ftar.ftar_all_reduce_async(group, grads[o:o + n], target, cfg, out=red[o:o + n],
