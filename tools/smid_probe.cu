@@ -4,7 +4,7 @@
 // to study why an early PDL trigger slows the bulk-copy all-reduce.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/_build/smid_probe tools/smid_probe.cu
-//   tools/_build/smid_probe [ctas=48]
+//   tools/_build/smid_probe [ctas=48] [peer=0]   (peer=1: read a buffer on GPU 1 over NVLink)
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -69,6 +69,20 @@ int main(int argc, char** argv) {
     }
     return 2.0 * n * 16 / (best * 1e-3) / 1e9;
   };
+  // optional: the copy reads a PEER GPU's buffer (NVLink) instead of local HBM
+  int ndev = 0;
+  cudaGetDeviceCount(&ndev);
+  const bool peer = argc > 2 && atoi(argv[2]) != 0 && ndev > 1;
+  if (peer) {
+    cudaSetDevice(1);
+    float4* rsrc;
+    cudaMalloc(&rsrc, n * 16);
+    cudaMemset(rsrc, 1, n * 16);
+    cudaDeviceSynchronize();
+    cudaSetDevice(0);
+    cudaDeviceEnablePeerAccess(1, 0);
+    src = rsrc;
+  }
   // 1. alone
   const double alone = timed_copy(idc);
   // 2. while `hold` occupies `ctas` SMs
@@ -91,7 +105,8 @@ int main(int argc, char** argv) {
     for (int i = 0; i < ctas; ++i) printf("%s%u", i ? "," : "", v[i]);
     printf("]");
   };
-  printf("{\"ctas\": %d, \"copy_alone_gbs\": %.1f, \"copy_beside_hold_gbs\": %.1f, ", ctas, alone, beside);
+  printf("{\"ctas\": %d, \"peer_src\": %d, \"copy_alone_gbs\": %.1f, \"copy_beside_hold_gbs\": %.1f, ", ctas, (int)peer,
+         alone, beside);
   dump("smid_alone", c);
   printf(", ");
   dump("smid_hold", a);
