@@ -1088,10 +1088,10 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
         st = wait_flag(&e->flag, tag, &ph->poison, ctl, nullptr, s_t0, p.hard_timeout_ns, nullptr);
         if (st == ST_OK) {
           // the flag can overtake the record (no writer fence): re-read until
-          // the record is this call's (its checksum covers the tag); a writer
-          // that died mid-record leaves it torn -> PEER_RESET after 200 us
+          // the record is this call's (its checksum covers the tag).  A writer
+          // that died mid-record leaves it torn: its poison word, the host's
+          // abort or the call's hard timeout end the wait, as in wait_flag.
           uint64_t fp, in_off, res_off, sum;
-          const uint64_t tr = globaltimer_ns();
           for (uint32_t it = 0;; ++it) {
             fp = ld_relaxed_sys(&e->fp);
             in_off = ld_relaxed_sys(&e->in_off);
@@ -1099,10 +1099,13 @@ __global__ void __launch_bounds__(kThreads, 1) allreduce_kernel(const __grid_con
             oo = ld_relaxed_sys(&e->out_off);
             sum = ld_relaxed_sys(&e->sum);
             if (sum == entry_sum(tag, fp, in_off, res_off, oo)) break;
-            if ((it & 15u) == 15u && globaltimer_ns() - tr > 200000ull) {
-              st = ST_PEER_RESET;
-              break;
+            if ((it & 63u) == 63u) {
+              if (flag_tag(ld_relaxed_sys(&ph->poison)) >= tag) st = ST_PEER_RESET;
+              else if (ctl->abort_tag == tag) st = ST_ABORTED;
+              else if (globaltimer_ns() - s_t0 > p.hard_timeout_ns) st = ST_TIMEOUT;
+              if (st != ST_OK) break;
             }
+            if (it > 4) __nanosleep(64);
           }
           if (st == ST_OK && fp != want_fp) st = ST_PROTOCOL;  // a different call
           // arena offsets, or references to member j's registered buffers
