@@ -58,8 +58,10 @@ def main():
         b, o = buf[:e], out[:e]
         for _ in range(10):
             ftar.ftar_all_reduce(g, b, 0, cfg, out=o)
-        # queued per-call time
+        # queued per-call time (one untimed call first: a device-side barrier,
+        # so host-side skew out of dist.barrier() stays out of the window)
         dist.barrier()
+        ftar.ftar_all_reduce(g, b, 0, cfg, out=o)
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(st)
