@@ -450,7 +450,11 @@ __device__ __forceinline__ void fold_range(const typename In::T* const* src, con
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint64_t v = v0 + (uint64_t)u * kThreads;
-        const uint64_t vv = v < ve ? v : vb;  // clamp: keep the load unconditional
+        // clamp: keep the load unconditional.  An out-of-range vector
+        // re-reads this thread's own first vector: clamping every thread to
+        // the same vector (vb) piled up to 512 x (U-1) x N loads on ONE line
+        // at the end of every short range (~3.5 us of the small kernel's fold)
+        const uint64_t vv = v < ve ? v : v0;
 #pragma unroll
         for (int k = 0; k < N; ++k) raw[u][k] = kAll ? In::load4(rs[k], vv * 4) : In::load4_if(rs[k], vv * 4, cb[k]);
       }
@@ -484,19 +488,22 @@ __device__ __forceinline__ void fold_range(const typename In::T* const* src, con
 // Fold [lo, hi) in grid-strided tiles (the CTAs' working set stays one
 // compact window, which keeps NVLink/TLB locality), caching the current owner
 // run so owner_of only runs when a tile crosses a segment boundary.
-template <int N, class In, class Sink>
+template <int N, class In, class Sink, bool kOneForm = false>
 __device__ __forceinline__ int fold_tiles(const LaunchParams& p, const typename In::T* const* src,
                                           const Sink& sink, uint64_t lo, uint64_t hi, bool vec_ok,
-                                          bool do_scale, uint32_t& nf, HostCtl* ctl, int max_tiles) {
+                                          bool do_scale, uint32_t& nf, HostCtl* ctl, int max_tiles,
+                                          int layout = -1, int rs_ctas = -1) {
+  // layout / rs_ctas override p.rs_layout / p.rs_ctas when >= 0
   constexpr int U = Unroll<N, In>::U;
   const uint64_t TL = (uint64_t)kThreads * 4 * U;
   int done = 0;
   int s = 0;
   uint64_t sbeg = 1, send = 0;  // cached run [sbeg, send) with owner s
-  const uint64_t G = (p.rs_ctas > 0 && p.rs_ctas < (int)gridDim.x) ? (uint64_t)p.rs_ctas : gridDim.x;
+  const int rc = rs_ctas >= 0 ? rs_ctas : p.rs_ctas;
+  const uint64_t G = (rc > 0 && rc < (int)gridDim.x) ? (uint64_t)rc : gridDim.x;
   if (blockIdx.x >= G) return 0;  // all-gather-only CTA
   uint64_t first = lo + (uint64_t)blockIdx.x * TL, step = G * TL;
-  if (p.rs_layout == 0) {  // one contiguous span per CTA
+  if ((layout >= 0 ? layout : p.rs_layout) == 0) {  // one contiguous span per CTA
     const uint64_t per = ((hi - lo + G - 1) / G + 7) & ~7ull;
     first = umin(lo + (uint64_t)blockIdx.x * per, hi);
     hi = umin(first + per, hi);
@@ -512,7 +519,9 @@ __device__ __forceinline__ int fold_tiles(const LaunchParams& p, const typename 
         sbeg = cur;
       }
       const uint64_t end = umin(send, b);
-      if (((p.contrib >> 0) & ((1u << N) - 1u)) == ((1u << N) - 1u))
+      // kOneForm: only the predicated form (half the code: latency-bound
+      // callers pay for instruction-cache misses, not for the predicates)
+      if (!kOneForm && ((p.contrib >> 0) & ((1u << N) - 1u)) == ((1u << N) - 1u))
         fold_range<N, In, U, Sink, true>(src, sink, cur, end, s, p.contrib, vec_ok, do_scale, p.scale, nf);
       else
         fold_range<N, In, U, Sink, false>(src, sink, cur, end, s, p.contrib, vec_ok, do_scale, p.scale, nf);
@@ -852,7 +861,9 @@ __device__ int fold_tiles_tma(const LaunchParams& p, const typename In::T* const
 #pragma unroll
       for (uint32_t v = 0; v < V; ++v) {
         const uint32_t off = (v * kTmaConsumers + (uint32_t)tid) * 4;
-        dst[v] = In::load4_if(mine_g, a + (off < tcnt ? off : 0), i_contribute);
+        // past the tile's end: re-read a vector of the tile spread by thread
+        // (one shared address would queue every such load on one line)
+        dst[v] = In::load4_if(mine_g, a + (off < tcnt ? off : ((uint32_t)tid * 4) % tcnt), i_contribute);
       }
     };
     if (run > 0) load_mine(0, ahead);
@@ -1529,6 +1540,15 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
   __shared__ uint64_t s_t0;
   __shared__ uint64_t s_t1;
   __shared__ uint32_t s_newer, s_ctlbad;
+#ifdef FTAR_DIAGNOSTICS
+  // per-step stamps of CTA 0 (tools/small_probe.py): dbg_trace[0..9]
+  uint64_t* const strace = (blockIdx.x == 0 && (p.emulated == 0 || blockIdx.y == 0)) ? hdr->dbg_trace : nullptr;
+#define SMALL_STAMP(k) \
+  if (strace && tid == 0) strace[k] = globaltimer_ns();
+#else
+#define SMALL_STAMP(k)
+#endif
+  SMALL_STAMP(0)
   if (tid >= 32 && tid < 64) {
     // zombie guard on warp 1 (remote reads, overlapping the previous
     // kernel's tail and warp 0's PCIe read): a member dropped from the ring
@@ -1554,12 +1574,14 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
     s_status = s_newer ? ST_PEER_RESET : (s_ctlbad ? ST_PROTOCOL : ST_OK);
     s_blame = s_newer ? __ffs(s_newer) - 1 : (s_ctlbad ? me : -1);
   }
+  SMALL_STAMP(1)
   // The input may be the output of the previous kernel on this stream (an
   // in-place chain, or an intra-replica reduce-scatter feeding this call):
   // griddepcontrol.launch_dependents does not make that kernel's writes
   // visible, so nothing reads my input before griddepcontrol.wait.
   pdl_wait();
   __syncthreads();
+  SMALL_STAMP(2)
   const uint64_t fp = call_fingerprint(p, N);
   const bool contributes = (p.contrib >> me) & 1u;
   // 1. push my input to every peer (grid-stride 16-byte copies)
@@ -1572,6 +1594,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
     }
   }
   __syncthreads();
+  SMALL_STAMP(3)
   if (tid == 0) {
     if (gridDim.x > 1) __threadfence();
     const uint32_t old = gridDim.x > 1 ? atomicAdd(&hdr->sm_arrive[parity], 1u) : 0u;
@@ -1585,6 +1608,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
       s_t1 = globaltimer_ns();
     }
   }
+  SMALL_STAMP(4)
   __syncthreads();
   if (tid == 0 && blockIdx.x == 0) {
     hdr->tph[0] = s_t0;
@@ -1608,6 +1632,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
     if (blockIdx.x == 0) hdr->tph[2] = globaltimer_ns();
   }
   __syncthreads();
+  SMALL_STAMP(5)
   // 3. fold locally (reference order) into out directly (out-of-place calls:
   // out is undefined after an error) or into the staging region (in place)
   const bool sdirect = (p.flags & kFlagSmallDirect) != 0;
@@ -1617,12 +1642,33 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
     uint64_t orbits = reinterpret_cast<uint64_t>(res) | reinterpret_cast<uint64_t>(p.out[me]);
     for (int j = 0; j < N; ++j) orbits |= reinterpret_cast<uint64_t>(s_src[j]);
     const bool vec_ok = (orbits & 15u) == 0;
-    LaunchParams g = p;
-    g.rs_layout = 1;
-    g.rs_ctas = 0;
-    fold_tiles<N, In>(g, s_src, SinkOne{res}, 0, E, vec_ok, (p.flags & FTAR_F_SCALE) != 0, nf, ctl, 0x7fffffff);
+#ifdef FTAR_DIAGNOSTICS
+    if (strace && tid == 0) {
+      // one dependent load of a peer-written slot and of my input
+      const uint64_t t0 = globaltimer_ns();
+      const float a = *(volatile const float*)s_src[(me + 1) % N];
+      const uint64_t t1 = globaltimer_ns();
+      const float b = *(volatile const float*)s_src[me];
+      const uint64_t t2 = globaltimer_ns();
+      strace[10] = t1 - t0;
+      strace[11] = t2 - t1;
+      strace[14] = __float_as_uint(a + b);
+    }
+#endif
+    fold_tiles<N, In, SinkOne, true>(p, s_src, SinkOne{res}, 0, E, vec_ok, (p.flags & FTAR_F_SCALE) != 0, nf, ctl,
+                                     0x7fffffff, /*layout=*/1, /*rs_ctas=*/0);
+#ifdef FTAR_DIAGNOSTICS
+    if (strace && tid == 0) strace[12] = globaltimer_ns();
+    if (p.diag == 5) {  // the same fold again: warm instruction cache, TLB and L2
+      uint32_t nf2 = 0;
+      fold_tiles<N, In, SinkOne, true>(p, s_src, SinkOne{res}, 0, E, vec_ok, (p.flags & FTAR_F_SCALE) != 0, nf2, ctl,
+                                       0x7fffffff, /*layout=*/1, /*rs_ctas=*/0);
+      if (strace && tid == 0) strace[13] = globaltimer_ns();
+    }
+#endif
   }
   __syncthreads();
+  SMALL_STAMP(6)
   if (tid < 32 && s_status == ST_OK) {
     // every copy I folded must still be the one its sender flagged for this
     // call: a zombie's late push is followed by its (older) flag (lane j
@@ -1638,6 +1684,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
   }
   if (__any_sync(0xffffffffu, nf != 0) && (tid & 31) == 0) atomicOr(&s_nf, 1u);
   __syncthreads();
+  SMALL_STAMP(7)
   if (tid == 0 && s_nf) atomicOr(&hdr->nonfinite, 1u);
   if (tid == 0 && s_status != ST_OK && s_status != ST_FOLLOW) {
     atomicMax(&hdr->err, severity_code(s_status));
@@ -1655,6 +1702,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
     if (!s_blame || sdirect) pdl_trigger();
   }
   __syncthreads();
+  SMALL_STAMP(8)
   if (s_blame == 1) {
     if (tid == 0) fence_acq_rel_gpu();
     __syncthreads();
@@ -1680,6 +1728,9 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
       const int64_t blame = hdr->err_peer;
       hdr->tph[3] = hdr->tph[2];
       hdr->tph[4] = globaltimer_ns();  // device memory only: `done` is the one PCIe write
+#ifdef FTAR_DIAGNOSTICS
+      hdr->dbg_trace[9] = hdr->tph[4];
+#endif
       hdr->rs_arrive = 0;
       hdr->done_arrive = 0;
       hdr->nonfinite = 0;
@@ -1693,6 +1744,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
     }
   }
 }
+#undef SMALL_STAMP
 
 // ------------------------------------------------- intra-replica collectives
 // IntraGroup.reduce_scatter / all_gather (replica.py:241-262)
