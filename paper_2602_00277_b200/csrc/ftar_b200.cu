@@ -2761,10 +2761,13 @@ bool tma_on() { return env_int("FTAR_TMA", 1) != 0; }
 // the register path wins at <= 4 MiB slices, the bulk path from 16 MiB)
 uint64_t tma_min_slice() { return (uint64_t)env_int("FTAR_TMA_MIN_SLICE_MIB", 16) << 20; }
 // CTAs of the bulk-copy path: ~128 KB of my slice per CTA, at most
-// FTAR_CTAS_TMA (default 48, a third of the SMs: N=4 f32 busbw 597 / 661 /
-// 680 GB/s at 64 MiB / 256 MiB / 1 GiB; 16 CTAs already give 648 at 256 MiB)
-int tma_ctas(uint64_t slice_bytes) {
-  const int cap = g_ctas > 0 ? g_ctas : env_int("FTAR_CTAS_TMA", 48);
+// FTAR_CTAS_TMA (default 48 from N=3, a third of the SMs: N=4 f32 busbw
+// 597 / 661 / 680 GB/s at 64 MiB / 256 MiB / 1 GiB; 16 CTAs already give 648
+// at 256 MiB.  At N=2 each stage holds a single peer's tile and 96 CTAs are
+// needed: 652 -> 666 GB/s f32 and 436 -> 453 bf16 at 256 MiB, 128 no better;
+// tools/tune_tma.py, profiles/r02/tune/ctas_n2.jsonl)
+int tma_ctas(int n, uint64_t slice_bytes) {
+  const int cap = g_ctas > 0 ? g_ctas : env_int("FTAR_CTAS_TMA", n <= 2 ? 96 : 48);
   const uint64_t per = (uint64_t)env_int("FTAR_TMA_BYTES_PER_CTA", 128 << 10);
   return (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)std::max(cap, 1), (slice_bytes + per - 1) / per));
 }
@@ -2797,7 +2800,7 @@ PathChoice choose_path(int n, const LaunchParams& p, uint64_t esz, bool small, b
     // every segment spans >= one tile and the slice is large: the bulk-copy data path
     pc.kind = kPathBulk;
     pc.stages = tma_stages_for(n, (int)esz);
-    pc.ctas = tma_ctas(p.slice * esz);
+    pc.ctas = tma_ctas(n, p.slice * esz);
   }
   return pc;
 }
@@ -3887,7 +3890,7 @@ static int launch_local(ftar_ctx** ctxs, int n, const void* const* ins, int in_d
   }
   if (!sgd_p && n >= 2 && tma_on() && p.p_base / (uint64_t)n >= tma_tile(n, in_dtype == FTAR_DT_BF16 ? 2 : 4)) {
     p.tma_stages = tma_stages_for(n, in_dtype == FTAR_DT_BF16 ? 2 : 4);
-    if (g_local_ctas <= 0) G = std::min(G, tma_ctas(p.slice * (in_dtype == FTAR_DT_BF16 ? 2 : 4)));
+    if (g_local_ctas <= 0) G = std::min(G, tma_ctas(n, p.slice * (in_dtype == FTAR_DT_BF16 ? 2 : 4)));
   }
   const dim3 grid(G, n);
   cudaError_t e = in_dtype == FTAR_DT_BF16 ? launch_dispatch<BF16In>(n, p, grid, st, true)

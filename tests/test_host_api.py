@@ -111,7 +111,7 @@ def test_inflight_bound_per_path(n, monkeypatch):
     b, g, path = _bound(n, (2 << 20) // 4 * n)  # 2 MiB slices: register path
     assert path == 3 and 1 <= g <= 128 and b % (g * 512 * 16) == 0
     b, g, path = _bound(n, (64 << 20) // 4 * n)  # 64 MiB slices: bulk-copy reduce-scatter
-    assert path == 2 and 1 <= g <= 48 and b < 227 * 1024 * g
+    assert path == 2 and 1 <= g <= (96 if n == 2 else 48) and b < 227 * 1024 * g
     monkeypatch.setenv("FTAR_TMA", "0")
     assert _bound(n, (64 << 20) // 4 * n)[2] == 3
     monkeypatch.setenv("FTAR_CTAS_PUSH", "7")
