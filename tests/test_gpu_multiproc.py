@@ -684,9 +684,18 @@ def _worker(rank, world, port, scenario, outdir):
 
 
 def run(scenario, world):
-    port = free_port()
     with tempfile.TemporaryDirectory() as d:
-        mp.start_processes(_worker, args=(world, port, scenario, d), nprocs=world, join=True, start_method="spawn")
+        for attempt in range(4):
+            # free_port() cannot reserve the port: another process may take it
+            # before rank 0's TCPStore binds (EADDRINUSE) -- then retry on a new one
+            port = free_port()
+            try:
+                mp.start_processes(_worker, args=(world, port, scenario, d), nprocs=world, join=True,
+                                   start_method="spawn")
+                break
+            except mp.ProcessRaisedException as exc:
+                if "EADDRINUSE" not in str(exc) or attempt == 3:
+                    raise
         out = []
         for r in range(world):
             with open(os.path.join(d, f"r{r}.json")) as f:
