@@ -574,10 +574,19 @@ __device__ __forceinline__ void fold_small(const LaunchParams& p, const typename
   const uint32_t contrib = p.contrib;
   const float scale = p.scale;
   const uint64_t gt = (uint64_t)blockIdx.x * kThreads + threadIdx.x, gs = (uint64_t)gridDim.x * kThreads;
+  // owner_of costs ~600 cycles: cache the current segment run [sbeg, send)
+  // (a thread's elements ascend, so most share a segment)
+  uint64_t sbeg = 1, send = 0;
+  int sown = 0;
+  auto owner_at = [&](uint64_t e) {
+    if (e < sbeg || e >= send) {
+      owner_of(e, p, N, sown, send);
+      sbeg = e;
+    }
+    return sown;
+  };
   auto one = [&](uint64_t e) {
-    int own;
-    uint64_t send;
-    owner_of(e, p, N, own, send);
+    const int own = owner_at(e);
     float acc = 0.0f;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
@@ -594,10 +603,6 @@ __device__ __forceinline__ void fold_small(const LaunchParams& p, const typename
     return;
   }
   const uint64_t nv = E >> 2;
-  // owner_of costs ~600 cycles: cache the current segment run [sbeg, send)
-  // (a thread's vectors ascend, grid-stride apart, so most share a segment)
-  uint64_t sbeg = 1, send = 0;
-  int sown = 0;
   // tiles of kThreads x U vectors, grid-strided over the CTAs (each CTA reads
   // one compact block per round, as fold_tiles does)
   const uint64_t tlv = (uint64_t)kThreads * U;
@@ -611,11 +616,7 @@ __device__ __forceinline__ void fold_small(const LaunchParams& p, const typename
     for (int u = 0; u < U; ++u) {
       const uint64_t v = v0 + (uint64_t)u * kThreads;
       const uint64_t e = (v < nv ? v : v0) * 4;  // out of range: re-read my first vector
-      if (e < sbeg || e >= send) {
-        owner_of(e, p, N, sown, send);
-        sbeg = e;
-      }
-      own[u] = sown;
+      own[u] = owner_at(e);
       whole[u] = e + 4 <= send;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
