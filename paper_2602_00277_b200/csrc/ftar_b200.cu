@@ -1723,10 +1723,10 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
     if (old == gridDim.x - 1) hdr->sm_arrive[parity] = 0;  // untouched until the call after next
     if (old == gridDim.x - 1 && s_status != ST_PEER_RESET) {  // (a zombie raises no flags either)
       for (int jj = 1; jj < N; ++jj)
-        st_relaxed_sys(&reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->sm_meta[me], fp);
+        st_relaxed_sys(&reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->sm_meta[parity][me], fp);
       fence_acq_rel_sys();  // all my CTAs' posted writes (and the fingerprints) before the flags
       for (int jj = 1; jj < N; ++jj)
-        st_relaxed_sys(&reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->sm_in[me], mk_flag(tag, 0));
+        st_relaxed_sys(&reinterpret_cast<ArenaHdr*>(p.base[(me + jj) % N])->sm_in[parity][me], mk_flag(tag, 0));
       s_t1 = globaltimer_ns();
     }
   }
@@ -1741,8 +1741,9 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
     for (int jj = 1; jj < N; ++jj) {
       const int j = (me + jj) % N;
       ArenaHdr* ph = reinterpret_cast<ArenaHdr*>(p.base[j]);
-      uint32_t st = wait_flag(&hdr->sm_in[j], tag, &ph->poison, ctl, &hdr->err, s_t0, p.hard_timeout_ns, nullptr);
-      if (st == ST_OK && ld_relaxed_sys(&hdr->sm_meta[j]) != fp) st = ST_PROTOCOL;
+      uint32_t st = wait_flag(&hdr->sm_in[parity][j], tag, &ph->poison, ctl, &hdr->err, s_t0, p.hard_timeout_ns,
+                              nullptr);
+      if (st == ST_OK && ld_relaxed_sys(&hdr->sm_meta[parity][j]) != fp) st = ST_PROTOCOL;
       if (st != ST_OK) {
         s_status = st;
         s_blame = j;
@@ -1795,7 +1796,8 @@ __global__ void __launch_bounds__(kThreads, 1) small_allreduce_kernel(const __gr
     // re-reads member j's flag and fingerprint; all peers at once)
     const int j = tid;
     const bool stale = j < N && j != me &&
-                       (flag_tag(ld_relaxed_sys(&hdr->sm_in[j])) != tag || ld_relaxed_sys(&hdr->sm_meta[j]) != fp);
+                       (flag_tag(ld_relaxed_sys(&hdr->sm_in[parity][j])) != tag ||
+                        ld_relaxed_sys(&hdr->sm_meta[parity][j]) != fp);
     const uint32_t bad = __ballot_sync(0xffffffffu, stale);
     if (tid == 0 && bad) {
       s_status = ST_PEER_RESET;

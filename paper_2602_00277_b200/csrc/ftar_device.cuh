@@ -105,8 +105,13 @@ struct alignas(128) ArenaHdr {
   // call t and start call t+1's reduce-scatter before I have read its flag
   // of call t; call t+2 cannot start before my call t is done)
   alignas(128) uint64_t ag_in[2][kMaxMembers];
-  alignas(128) uint64_t sm_in[kMaxMembers];  // small one-shot: member k's whole input is in my recv slot
-  uint64_t sm_meta[kMaxMembers];             // its call fingerprint (validated like an entry record)
+  // small one-shot: member k's whole input of call <tag> is in my recv slot,
+  // and its call fingerprint (validated like an entry record); one slot per
+  // call parity, as the payload slots: a peer that has finished call t may
+  // already raise call t+1's flag while I still wait for or re-check its
+  // flag of call t (call t+2 cannot start before my call t is done)
+  alignas(128) uint64_t sm_in[2][kMaxMembers];
+  uint64_t sm_meta[2][kMaxMembers];
   alignas(128) uint32_t sm_arrive[2];        // small one-shot: push-arrival counter per call parity
   alignas(128) uint64_t gen_word;            // the generation my host installed (ftar_set_membership):
                                              // a sender whose call is older stops before pushing here

@@ -445,7 +445,9 @@ def _worker(rank, world, port, scenario, outdir):
             # trigger forced everywhere, also on the bulk-copy path
             # (FTAR_PDL_EARLY=2, FTAR_TMA_MIN_SLICE_MIB=0); 2 MiB and 24 MiB buckets
             cfg = ftar.PipelineConfig(per_chunk_timeout_s=10)
-            for gen, e in ((10, 512 << 10), (11, 6 << 20)):
+            # (64 Ki elements: the small one-shot, also forced onto 32 CTAs, where
+            # its flags once raced with a peer's next call)
+            for gen, e in ((9, 64 << 10), (10, 512 << 10), (11, 6 << 20)):
                 group.close()
                 group = ftar.RingGroup(rank, 0, fabric, device=dev, max_bucket_bytes=e * 4,
                                        pool_bytes=12 * e * 4 + 4096)
@@ -458,9 +460,16 @@ def _worker(rank, world, port, scenario, outdir):
                 for x, h in zip(xs, hosts):
                     x.copy_(torch.from_numpy(h[rank]))
                 outs = [group.alloc_bucket(e) for _ in range(K - 1)]
-                for mode, env in (("push", {}), ("pull", {"FTAR_NO_PUSH": "1"}), ("early2", {"FTAR_PDL_EARLY": "2", "FTAR_TMA_MIN_SLICE_MIB": "0"})):
+                modes = [("push", {}), ("pull", {"FTAR_NO_PUSH": "1"}),
+                         ("early2", {"FTAR_PDL_EARLY": "2", "FTAR_TMA_MIN_SLICE_MIB": "0"})]
+                if e == 64 << 10:
+                    modes.append(("small32", {"FTAR_TEST_CTAS": "32"}))
+                for mode, env in modes:
                     old_env = {k: os.environ.get(k) for k in env}
                     os.environ.update(env)
+                    if "FTAR_TEST_CTAS" in env:
+                        from paper_2602_00277_b200 import _lib as lib_
+                        lib_.lib.ftar_set_tuning(int(env["FTAR_TEST_CTAS"]), 0)
                     try:
                         for _ in range(3):
                             pend = [ftar.ftar_all_reduce_async(group, xs[k], k, cfg, out=outs[k]) for k in range(K - 1)]
@@ -475,6 +484,8 @@ def _worker(rank, world, port, scenario, outdir):
                             good = np.array_equal(shared.cpu().numpy(), wants[K - 1])
                             (res["ok"] if good else res["errors"]).append(f"queued_shared_{mode}_{e}")
                     finally:
+                        if "FTAR_TEST_CTAS" in env:
+                            lib_.lib.ftar_set_tuning(0, 0)
                         for k, v in old_env.items():
                             if v is None:
                                 os.environ.pop(k, None)
