@@ -2893,7 +2893,12 @@ int tma_ctas(int n, uint64_t slice_bytes) {
   const uint64_t per = (uint64_t)env_int("FTAR_TMA_BYTES_PER_CTA", 128 << 10);
   return (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)std::max(cap, 1), (slice_bytes + per - 1) / per));
 }
-int small_ctas(uint64_t bytes) { return (int)std::max<uint64_t>(1, std::min<uint64_t>(16, (bytes + (32u << 10) - 1) >> 15)); }
+// CTAs of the small one-shot: ~20 KB of the bucket each, at most 48 (N=4,
+// 1 MiB f32: 21.7 us per call at 16 CTAs, 19.3 at 48; bf16 24.5 -> 20.9;
+// tools/tune_tma.py --mib 1, profiles/r02/tune/small_ctas_n4.jsonl)
+int small_ctas(uint64_t bytes) {
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(48, (bytes + 20479) / 20480));
+}
 
 // The data path and grid of one call (launch_real and ftar_inflight_bound
 // share it, so the in-flight meter reports the path the call really takes).
