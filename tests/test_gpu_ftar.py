@@ -576,3 +576,30 @@ def test_local_ring_queued_launches(ftar):
     finally:
         for g in ring.groups:
             g.close()
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+@pytest.mark.parametrize("elems", [1, 257, 4099, 65_537, 262_143])
+def test_small_one_shot_unaligned_and_behind(ftar, n, elems):
+    """The small one-shot's fold (fold_small) on buffers that are NOT 16-byte
+    aligned (the per-element path with its cached owner run), with a behind
+    member whose buffer is garbage, every bucket at most 1 MiB: bit-exact."""
+    ring = ftar.LocalRing(n, device=DEV, max_bucket_bytes=4 << 20, protocol=True)
+    try:
+        arrays = member_inputs(n, elems, seed=900 + n + elems)
+        contrib = [m != n - 1 for m in range(n)]
+        ring.reconfig(contributors=[m for m in range(n) if contrib[m]])
+        cfg = ftar.PipelineConfig(chunk_bytes=4096, max_in_flight=2)
+        base = [torch.full((elems + 1,), float("nan"), device=DEV) for _ in range(n)]
+        bufs = []
+        for m, (b, a) in enumerate(zip(base, arrays)):
+            if contrib[m]:
+                b[1:].copy_(to_dev(a))
+            bufs.append(b[1:])  # 4 bytes past an aligned allocation
+        outs = [torch.full((elems + 1,), float("nan"), device=DEV)[1:] for _ in range(n)]
+        ring.all_reduce(bufs, cfg, outs=outs, scale=1.0 / n)
+        want = orc.normalize(orc.oracle_reduce(arrays, cfg.chunk_bytes, cfg.max_in_flight, contrib=contrib), n)
+        for o in outs:
+            np.testing.assert_array_equal(o.cpu().numpy(), want)
+    finally:
+        ring.close()
